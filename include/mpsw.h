@@ -1,0 +1,189 @@
+/*
+ * mpsw.h — model-parallel swapping (Computron, arXiv 2306.13835) on B200: the C-ABI boundary.
+ *
+ * One mpsw_ctx is one single-process deployment of ONE tensor-parallel group of t ranks
+ * (§3.1 P:72 "Workers are launched per GPU"; every model instance uses the same
+ * parallel configuration). Inside the library there is one engine thread (the paper's
+ * centralised engine) and one worker thread per rank. Each rank owns:
+ *   - a parameter region of `param_budget_bytes_per_gpu` bytes in HBM, allocated ONCE at
+ *     mpsw_init and carved into k = floor(budget / S_r) slots (reading #8);
+ *   - a compute stream plus two copy streams, load (H2D) and offload (D2H) ("two
+ *     additional streams to run loading and offloading operations concurrently");
+ *   - page-locked host arenas, one contiguous blob per (model, rank) ("the parameters
+ *     are kept pinned in CPU memory").
+ * Ranks map to CUDA devices through `device_ids`; repeated ids are allowed and give
+ * "virtual ranks" that share one GPU (used to test TP > 1 semantics on a single B200).
+ *
+ * Every call returns mpsw_status (0 = OK, < 0 = error) and never throws across the ABI.
+ * On error, mpsw_last_error() returns a thread-local message describing the failure.
+ * Pointers are plain host pointers unless stated otherwise; sizes are bytes.
+ * Thread safety: all calls may be made from any host thread; calls on one ctx are
+ * serialised internally except mpsw_wait / mpsw_poll which only read completion state.
+ */
+#ifndef MPSW_H
+#define MPSW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MPSW_OK = 0,
+    MPSW_EINVAL = -1,      /* bad argument / unsupported configuration               */
+    MPSW_ENOMEM = -2,      /* budget cannot hold one shard; pinning or cudaMalloc failed      */
+    MPSW_EBUSY = -3,       /* swap_out of a model with in-flight batches or a pending load    */
+    MPSW_ENOENT = -4,      /* unknown model / ticket / request id              */
+    MPSW_EAGAIN = -5,      /* not finished yet (poll/wait with timeout)                       */
+    MPSW_ECUDA = -6,       /* a CUDA runtime call failed; ctx is poisoned                     */
+    MPSW_ENCCL = -7,       /* reserved: collective backend failure                            */
+    MPSW_EINVARIANT = -8,  /* engine invariant violated; ctx poisoned   */
+    MPSW_ETIMEDOUT = -9    /* mpsw_wait timed out                                             */
+} mpsw_status;
+
+enum { MPSW_BF16 = 0, MPSW_FP32 = 1 };                                 /* parameter/compute dtype */
+enum { MPSW_SWAP_AUTO = 0, MPSW_SWAP_COPY_ENGINE = 1, MPSW_SWAP_ZERO_COPY = 2 };
+enum { MPSW_EVICTED = 0, MPSW_LOADING = 1, MPSW_RESIDENT = 2, MPSW_OFFLOADING = 3 };
+
+typedef struct mpsw_ctx mpsw_ctx;   /* opaque; owns arenas, slots, streams, threads */
+
+typedef struct {
+    int n_gpus;                   /* ranks in the TP group (t)                                  */
+    const int* device_ids;        /* n_gpus CUDA ordinals (caller-owned, read during init)     */
+    int tp;                       /* must equal n_gpus: one TP group per ctx; replicas = ctxs  */
+    uint64_t param_budget_bytes_per_gpu;  /* parameter slots per rank (the swapping budget)    */
+    uint64_t workspace_bytes_per_gpu;     /* 0 = auto (activations, partials, logits staging)  */
+    int max_batch;                /* requests per batch entry, 1..256 (P:168 uses 8, P:196 32) */
+    int max_tokens;               /* tokens per request, 1..128 (P:138 uses 2, P:166 uses 8)   */
+    int dtype;                    /* MPSW_BF16 (1e-2 parity) or MPSW_FP32 (1e-5 parity)        */
+    int max_inflight_batches;     /* D per TP group (reading #26); 0 => 1            */
+    int swap_mode;                /* MPSW_SWAP_*: copy engine, zero-copy kernel, or auto       */
+    uint64_t chunk_bytes;         /* swap chunk c (multiple of 4096); 0 => 64 MiB              */
+    int writeback;                /* 1 = offload copies the slot back to the arena      */
+    int trace;                    /* 1 = record the NDJSON event/decision trace                */
+    int zc_ctas;                  /* CTAs of the zero-copy kernel; 0 => auto                   */
+} mpsw_config;
+
+typedef struct { int n_layers, hidden, heads, ffn, vocab, max_pos; } mpsw_opt_dims;
+
+typedef struct {
+    char name[64];                /* HF parameter name, e.g. "decoder.layers.3.fc1.weight"    */
+    uint64_t offset, bytes;       /* byte range inside the rank's arena (offset % 256 == 0)    */
+    int rows, cols;               /* shard shape (cols == 1 for vectors)                      */
+    int split;                    /* 0 replicated, 1 row-block (column-parallel / vocab),     */
+                                  /* 2 column-block (row-parallel), reading #12 */
+} mpsw_tensor_desc;
+
+/* Create a ctx. Allocates each rank's parameter region (one cudaMalloc of the budget) and
+ * workspace, creates streams and starts the engine and worker threads.
+ * Errors: EINVAL (tp != n_gpus, bad sizes), ENOMEM (cudaMalloc), ECUDA. */
+mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out);
+
+/* Wait for all in-flight work, stop threads, free every arena, slot, stream. NULL is OK. */
+mpsw_status mpsw_shutdown(mpsw_ctx* ctx);
+
+/* Pure function (no ctx, no GPU): the per-rank arena layout of an OPT model at TP degree
+ * `tp` (P:138 every shard keeps all T = 16*L+4 tensors). Writes up to
+ * `cap` descriptors to `out` (may be NULL), the tensor count to *n and the arena size to
+ * *shard_bytes. `dtype` MPSW_BF16 (2-byte elements) or MPSW_FP32. EINVAL if tp does not
+ * divide heads, vocab, ffn and hidden. */
+mpsw_status mpsw_shard_layout(const mpsw_opt_dims* dims, int tp, int rank, int dtype,
+                              mpsw_tensor_desc* out, int cap, int* n, uint64_t* shard_bytes);
+
+/* Register a model (P:72 co-located instances). `tp` must equal the ctx's. `shards` is an
+ * array of tp caller-owned host blobs in the mpsw_shard_layout format, each of
+ * shard_bytes[r] == S_r bytes; they are COPIED into library-owned pinned arenas before
+ * return. shards == NULL allocates the arenas and leaves them for in-place filling via
+ * mpsw_model_arena / mpsw_synth_fill. All models of a ctx must have identical dims
+ * (homogeneous slots). The model starts EVICTED.
+ * Errors: EINVAL (dims/tp/sizes), ENOMEM (budget < S_r, or pinning failed). */
+mpsw_status mpsw_register_model(mpsw_ctx* ctx, const mpsw_opt_dims* dims, int tp,
+                                const void* const* shards, const uint64_t* shard_bytes,
+                                int* model_id);
+
+/* Host pointer and size of (model, rank)'s pinned arena, for in-place filling before the
+ * first swap-in. Writing it while the model is LOADING/OFFLOADING is undefined. */
+mpsw_status mpsw_model_arena(mpsw_ctx* ctx, int model_id, int rank, void** host, uint64_t* bytes);
+
+/* Input-generation helper (not the hot path): fill (model, rank)'s arena with the
+ * counter-based synthetic weights of DESIGN.md §Inputs (C0) for `model_seed`, using
+ * `threads` host threads (0 = all). rank = -1 fills every rank. */
+mpsw_status mpsw_synth_fill(mpsw_ctx* ctx, int model_id, int rank, uint64_t model_seed, int threads);
+
+/* Explicit load entry: asynchronously copy every rank's shard into a free slot.
+ * Goes through the engine queue, ordered with requests. *ticket identifies the entry.
+ * OK with an already-complete ticket if RESIDENT or LOADING (no-op). ENOMEM if no slot
+ * is free (explicit swaps never evict), EBUSY if the model is OFFLOADING. */
+mpsw_status mpsw_swap_in(mpsw_ctx* ctx, int model_id, uint64_t* ticket);
+
+/* Explicit offload entry: write the slot back to the arena (writeback=1) and free it.
+ * EBUSY if the model has in-flight batches or is LOADING (eviction never races a request).
+ * OK no-op if EVICTED/OFFLOADING. */
+mpsw_status mpsw_swap_out(mpsw_ctx* ctx, int model_id, uint64_t* ticket);
+
+/* Block until every rank acked `ticket` ("completed when every worker finishes").
+ * t_submit: engine time of the decision; t_done_per_rank: array of tp ack times (may be
+ * NULL). Times are seconds since mpsw_init (steady clock). timeout_s < 0 waits forever.
+ * Errors: ENOENT unknown ticket, ETIMEDOUT. */
+mpsw_status mpsw_wait(mpsw_ctx* ctx, uint64_t ticket, double timeout_s, double* t_submit,
+                      double* t_done_per_rank);
+
+/* Per-rank device time of a swap entry's copies, from CUDA events on the copy stream
+ * (ms, array of tp), plus entry kind (0 load, 1 offload) and model. EAGAIN if not done. */
+mpsw_status mpsw_entry_gpu_ms(mpsw_ctx* ctx, uint64_t ticket, int* kind, int* model_id,
+                              float* gpu_ms_per_rank);
+
+/* Submit a request (pushed with a timestamp into the model's queue). The engine
+ * batches it with other queued requests of the model (oldest first, <= max_batch), swaps
+ * the model in via LRU if needed, runs the TP forward and writes the fp32 logits
+ * of the LAST token ([vocab] floats) to logits_out, which must stay valid until mpsw_poll
+ * returns OK. tokens are copied before return.
+ * Errors: ENOENT unknown model (counted), EINVAL n_tokens not in [1, max_tokens] or a
+ * token outside [0, vocab). */
+mpsw_status mpsw_request(mpsw_ctx* ctx, int model_id, const int32_t* tokens, int n_tokens,
+                         float* logits_out, int64_t* request_id);
+
+/* OK once the request's logits are in logits_out (t_arrival, t_done in engine seconds);
+ * EAGAIN while pending; ENOENT unknown id. */
+mpsw_status mpsw_poll(mpsw_ctx* ctx, int64_t request_id, double* t_arrival, double* t_done);
+
+/* Blocking variant of mpsw_poll (timeout_s < 0 = forever). */
+mpsw_status mpsw_wait_request(mpsw_ctx* ctx, int64_t request_id, double timeout_s,
+                              double* t_arrival, double* t_done);
+
+/* 64-bit order-independent checksum (C4) of (model, rank)'s bytes:
+ * on_device = 1 hashes the resident slot with the sm_100a checksum kernel (EINVAL unless
+ * RESIDENT); on_device = 0 hashes the pinned host arena on the host. */
+mpsw_status mpsw_checksum(mpsw_ctx* ctx, int model_id, int rank, int on_device, uint64_t* out);
+
+/* Copy `bytes` at `offset` of a RESIDENT model's device slot (rank) into host `dst`
+ * (verification: sampled parity against the oracle). */
+mpsw_status mpsw_peek(mpsw_ctx* ctx, int model_id, int rank, uint64_t offset, uint64_t bytes,
+                      void* dst);
+
+/* MPSW_EVICTED / LOADING / RESIDENT / OFFLOADING as seen by the engine. */
+mpsw_status mpsw_residency(mpsw_ctx* ctx, int model_id, int* state);
+
+/* Write the recorded events and decisions, in engine order, as NDJSON (trace = 1). */
+mpsw_status mpsw_trace_dump(mpsw_ctx* ctx, const char* ndjson_path);
+
+typedef struct {
+    uint64_t kernel_launches;     /* kernels this library launched (all ranks)              */
+    uint64_t h2d_bytes, d2h_bytes;/* bytes moved by swaps                                   */
+    uint64_t swaps_in, swaps_out; /* load / offload entries completed                       */
+    uint64_t batches, requests;   /* batch entries / requests completed                     */
+    uint64_t rejected;            /* requests rejected with ENOENT                          */
+    int k_slots;                  /* slots per rank (0 before the first registration)       */
+    uint64_t shard_bytes;         /* S_r                                                    */
+} mpsw_stats;
+
+mpsw_status mpsw_get_stats(mpsw_ctx* ctx, mpsw_stats* out);
+
+/* Thread-local description of the last error on this thread ("" if none). */
+const char* mpsw_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPSW_H */

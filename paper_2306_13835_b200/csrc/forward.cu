@@ -1,0 +1,429 @@
+// TP OPT forward kernels for sm_100a (one rank). The model is HF OPT (PAPER.md P:127 serves
+// OPT-13B): pre-LN decoder, ReLU MLP, learned positions (+2 offset), tied lm_head.
+// TP layout (reading #12): column-parallel q/k/v/fc1, row-parallel out_proj/fc2
+// whose fp32 partials are summed across ranks by the all-reduce fused into fwd_reduce_ln
+// ("TP communication is done through distributed collectives").
+//
+// Numerics contract (reading #20): weights bf16 (or fp32), fp32 accumulation,
+// fp32 residual stream / LN statistics / softmax / partials; bf16 rounding (RNE) only where a
+// GEMM reads its A operand: LN outputs, attention output, ReLU output.
+//
+// The skinny GEMMs (M = B*L <= 64 at the paper's shapes) are weight-streaming and HBM-bound
+// (arithmetic intensity ~M flop/B << ridge ~212), so they run on CUDA cores with 128-bit
+// coalesced weight loads; the per-element reduction order depends only on (n, K) — never on
+// M or on the batch composition — so a request's logits are bitwise batch-invariant.
+#include "internal.h"
+
+#include <cuda_bf16.h>
+
+namespace mpsw {
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+template <typename T> struct Vec;
+template <> struct Vec<bf16> {
+    static constexpr int N = 8;
+    __device__ __forceinline__ static void load(const bf16* p, float* f) {
+        const uint4 u = *reinterpret_cast<const uint4*>(p);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 t = __bfloat1622float2(h[i]);
+            f[2 * i] = t.x;
+            f[2 * i + 1] = t.y;
+        }
+    }
+};
+template <> struct Vec<float> {
+    static constexpr int N = 4;
+    __device__ __forceinline__ static void load(const float* p, float* f) {
+        const float4 u = *reinterpret_cast<const float4*>(p);
+        f[0] = u.x; f[1] = u.y; f[2] = u.z; f[3] = u.w;
+    }
+};
+
+__device__ __forceinline__ float to_f(bf16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float to_f(float v) { return v; }
+template <typename T> __device__ __forceinline__ T from_f(float v);
+template <> __device__ __forceinline__ bf16 from_f<bf16>(float v) { return __float2bfloat16_rn(v); }
+template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
+
+// ------------------------------------------------------------------ GEMM (weight streaming)
+enum Epi { EPI_F32 = 0, EPI_RELU_T = 1 };
+
+struct Seg {
+    const void* W;      // [N, K] row-major
+    const void* bias;   // [N] or null
+    int N;
+    float scale;        // applied after the bias (q: hd^-0.5, HF:opt.py:151)
+    int out_col0;
+};
+
+struct GemmArgs {
+    const void* A;      // [rows, K]
+    const int32_t* a_rows;   // optional gather of A rows (lm_head: last token of each request)
+    int M, K, lda;
+    Seg seg[3];
+    int nseg, n_total;
+    void* out;
+    int ldo;
+};
+
+constexpr int kGemmWarps = 4;
+constexpr int kGemmR = 2;   // W rows per warp
+
+template <typename T, int MT, int EPI>
+__global__ void __launch_bounds__(kGemmWarps * 32) gemm_rows_kernel(GemmArgs g) {
+    constexpr int V = Vec<T>::N;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int n0 = (blockIdx.x * kGemmWarps + warp) * kGemmR;
+    if (n0 >= g.n_total) return;
+    const T* wrow[kGemmR];
+    const T* brow[kGemmR];
+    float scale[kGemmR];
+    int ocol[kGemmR];
+    bool valid[kGemmR];
+#pragma unroll
+    for (int r = 0; r < kGemmR; ++r) {
+        int n = n0 + r;
+        valid[r] = n < g.n_total;
+        int s = 0;
+        if (!valid[r]) n = n0;
+        while (s + 1 < g.nseg && n >= g.seg[s].N) { n -= g.seg[s].N; ++s; }
+        wrow[r] = reinterpret_cast<const T*>(g.seg[s].W) + (size_t)n * g.K;
+        brow[r] = g.seg[s].bias ? reinterpret_cast<const T*>(g.seg[s].bias) + n : nullptr;
+        scale[r] = g.seg[s].scale;
+        ocol[r] = g.seg[s].out_col0 + n;
+    }
+    const T* A = reinterpret_cast<const T*>(g.A);
+    for (int m0 = 0; m0 < g.M; m0 += MT) {
+        float acc[kGemmR][MT];
+#pragma unroll
+        for (int r = 0; r < kGemmR; ++r)
+#pragma unroll
+            for (int m = 0; m < MT; ++m) acc[r][m] = 0.f;
+        const T* arow[MT];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            const int mm = min(m0 + m, g.M - 1);
+            const int ar = g.a_rows ? g.a_rows[mm] : mm;
+            arow[m] = A + (size_t)ar * g.lda;
+        }
+        for (int k = lane * V; k < g.K; k += 32 * V) {
+            float w[kGemmR][V];
+#pragma unroll
+            for (int r = 0; r < kGemmR; ++r) Vec<T>::load(wrow[r] + k, w[r]);
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                float a[V];
+                Vec<T>::load(arow[m] + k, a);
+#pragma unroll
+                for (int r = 0; r < kGemmR; ++r)
+#pragma unroll
+                    for (int v = 0; v < V; ++v) acc[r][m] = fmaf(w[r][v], a[v], acc[r][m]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kGemmR; ++r)
+#pragma unroll
+            for (int m = 0; m < MT; ++m)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc[r][m] += __shfl_xor_sync(0xffffffffu, acc[r][m], o);
+        if (lane == 0) {
+#pragma unroll
+            for (int r = 0; r < kGemmR; ++r) {
+                if (!valid[r]) continue;
+                const float b = brow[r] ? to_f(*brow[r]) : 0.f;
+#pragma unroll
+                for (int m = 0; m < MT; ++m) {
+                    if (m0 + m >= g.M) break;
+                    float v = acc[r][m];
+                    if (brow[r]) v = v + b;
+                    if (EPI == EPI_F32) {
+                        v = v * scale[r];
+                        reinterpret_cast<float*>(g.out)[(size_t)(m0 + m) * g.ldo + ocol[r]] = v;
+                    } else {
+                        v = fmaxf(v, 0.f);
+                        reinterpret_cast<T*>(g.out)[(size_t)(m0 + m) * g.ldo + ocol[r]] = from_f<T>(v);
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <typename T, int EPI>
+void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
+    const int rows_per_cta = kGemmWarps * kGemmR;
+    const int grid = (g.n_total + rows_per_cta - 1) / rows_per_cta;
+    const int threads = kGemmWarps * 32;
+    if (g.M <= 1) gemm_rows_kernel<T, 1, EPI><<<grid, threads, 0, st>>>(g);
+    else if (g.M <= 2) gemm_rows_kernel<T, 2, EPI><<<grid, threads, 0, st>>>(g);
+    else if (g.M <= 4) gemm_rows_kernel<T, 4, EPI><<<grid, threads, 0, st>>>(g);
+    else gemm_rows_kernel<T, 8, EPI><<<grid, threads, 0, st>>>(g);
+    MPSW_CU(cudaGetLastError());
+}
+
+void launch_gemm(int dtype, int epi, GemmArgs& g, cudaStream_t st) {
+    g.n_total = 0;
+    for (int i = 0; i < g.nseg; ++i) g.n_total += g.seg[i].N;
+    if (dtype == MPSW_BF16) {
+        if (epi == EPI_F32) launch_gemm_t<bf16, EPI_F32>(g, st);
+        else launch_gemm_t<bf16, EPI_RELU_T>(g, st);
+    } else {
+        if (epi == EPI_F32) launch_gemm_t<float, EPI_F32>(g, st);
+        else launch_gemm_t<float, EPI_RELU_T>(g, st);
+    }
+}
+
+// ------------------------------------------------------------------ embedding (vocab-parallel)
+template <typename T>
+__global__ void embed_kernel(const int32_t* __restrict__ tokens, const T* __restrict__ E, int lo, int Vl,
+                             int h, float* __restrict__ partial) {
+    const int m = blockIdx.x;
+    const int tok = tokens[m];
+    const bool in = tok >= lo && tok < lo + Vl;
+    const T* row = E + (size_t)(in ? tok - lo : 0) * h;
+    for (int j = threadIdx.x; j < h; j += blockDim.x) partial[(size_t)m * h + j] = in ? to_f(row[j]) : 0.f;
+}
+
+// ------------------------------------------------------------------ all-reduce + residual + LN
+struct Peers {
+    const float* p[8];
+    int n;
+};
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    float s = 0.f;
+    for (int i = 0; i < nw; ++i) s += red[i];
+    return s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) reduce_ln_kernel(Peers peers, const float* __restrict__ residual,
+                                                        const T* __restrict__ bias, const T* __restrict__ pos_table,
+                                                        const int32_t* __restrict__ pos, const T* __restrict__ gamma,
+                                                        const T* __restrict__ beta, float* __restrict__ x_out,
+                                                        T* __restrict__ ln_out, int h) {
+    extern __shared__ float xs[];
+    __shared__ float red[32];
+    const int m = blockIdx.x;
+    const size_t row = (size_t)m * h;
+    float lsum = 0.f;
+    for (int j = threadIdx.x; j < h; j += blockDim.x) {
+        float s = peers.p[0][row + j];
+        for (int r = 1; r < peers.n; ++r) s += peers.p[r][row + j];   // TP all-reduce (rank order)
+        if (bias) s = s + to_f(bias[j]);
+        if (pos_table) s = s + to_f(pos_table[(size_t)pos[m] * h + j]);
+        if (residual) s = residual[row + j] + s;
+        xs[j] = s;
+        x_out[row + j] = s;
+        lsum += s;
+    }
+    const float mean = block_sum(lsum, red) / (float)h;
+    float lvar = 0.f;
+    for (int j = threadIdx.x; j < h; j += blockDim.x) {
+        const float d = xs[j] - mean;
+        lvar += d * d;
+    }
+    const float var = block_sum(lvar, red) / (float)h;
+    const float den = sqrtf(var + 1e-5f);
+    for (int j = threadIdx.x; j < h; j += blockDim.x)
+        ln_out[row + j] = from_f<T>(((xs[j] - mean) / den) * to_f(gamma[j]) + to_f(beta[j]));
+}
+
+// ------------------------------------------------------------------ attention (L <= 128)
+template <typename T>
+__global__ void __launch_bounds__(128) attention_kernel(const float* __restrict__ qkv, const int32_t* __restrict__ seq_start,
+                                                        T* __restrict__ o, int hl, int hd) {
+    __shared__ float sc[4][128];
+    const int b = blockIdx.x, head = blockIdx.y;
+    const int s0 = seq_start[b], L = seq_start[b + 1] - s0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ld = 3 * hl;
+    // lane owns head dims d = lane + 32u (u < 4, d < hd): any hd <= 128
+    for (int i = warp; i < L; i += 4) {
+        const float* q = qkv + (size_t)(s0 + i) * ld + head * hd;
+        float qv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) qv[u] = lane + 32 * u < hd ? q[lane + 32 * u] : 0.f;
+        float mx = -INFINITY;
+        for (int j = 0; j <= i; ++j) {
+            const float* k = qkv + (size_t)(s0 + j) * ld + hl + head * hd;
+            float d = 0.f;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) if (lane + 32 * u < hd) d = fmaf(qv[u], k[lane + 32 * u], d);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
+            if (lane == 0) sc[warp][j] = d;
+            mx = fmaxf(mx, d);
+        }
+        __syncwarp();
+        float sum = 0.f;
+        for (int j = lane; j <= i; j += 32) {
+            const float e = expf(sc[warp][j] - mx);
+            sc[warp][j] = e;
+            sum += e;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        __syncwarp();
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int j = 0; j <= i; ++j) {
+            const float p = sc[warp][j] / sum;
+            const float* v = qkv + (size_t)(s0 + j) * ld + 2 * hl + head * hd;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) if (lane + 32 * u < hd) acc[u] = fmaf(p, v[lane + 32 * u], acc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (lane + 32 * u < hd) o[(size_t)(s0 + i) * hl + head * hd + lane + 32 * u] = from_f<T>(acc[u]);
+        __syncwarp();
+    }
+}
+
+inline size_t esz(int dtype) { return dtype == MPSW_BF16 ? 2 : 4; }
+
+}  // namespace
+
+// ------------------------------------------------------------------ workspace
+static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t workspace_bytes(const FwdShape& s, int max_rows, int max_batch) {
+    const size_t e = esz(s.dtype), M = max_rows, h = s.hidden, hl = (size_t)s.heads_local * s.head_dim;
+    size_t b = 0;
+    b += align_up(M * h * 4);                    // x
+    b += align_up(M * h * e);                    // a
+    b += align_up(M * 3 * hl * 4);               // qkv
+    b += align_up(M * hl * e);                   // o
+    b += align_up(M * (size_t)s.ffn_local * e);  // r
+    b += 2 * align_up(M * h * 4);                // partials
+    b += align_up((size_t)max_batch * s.vocab_local * 4);   // logits
+    b += align_up(M * 4);                        // tokens
+    b += align_up((3 * (size_t)max_batch + 2 + M) * 4);     // meta
+    return b;
+}
+
+void workspace_carve(FwdWorkspace& w, const FwdShape& s, int max_rows, int max_batch, void* base) {
+    const size_t e = esz(s.dtype), M = max_rows, h = s.hidden, hl = (size_t)s.heads_local * s.head_dim;
+    char* p = (char*)base;
+    auto take = [&](size_t n) { void* r = p; p += align_up(n); return r; };
+    w.base = base;
+    w.x = (float*)take(M * h * 4);
+    w.a = take(M * h * e);
+    w.qkv = (float*)take(M * 3 * hl * 4);
+    w.o = take(M * hl * e);
+    w.r = take(M * (size_t)s.ffn_local * e);
+    w.partial[0] = (float*)take(M * h * 4);
+    w.partial[1] = (float*)take(M * h * 4);
+    w.logits = (float*)take((size_t)max_batch * s.vocab_local * 4);
+    w.tokens = (int32_t*)take(M * 4);
+    w.meta = (int32_t*)take((3 * (size_t)max_batch + 2 + M) * 4);
+    w.bytes = (size_t)(p - (char*)base);
+}
+
+// ------------------------------------------------------------------ launchers
+int fwd_embed(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, int M, float* partial,
+              cudaStream_t st) {
+    const int lo = s.rank * s.vocab_local;
+    if (s.dtype == MPSW_BF16)
+        embed_kernel<bf16><<<M, 256, 0, st>>>(ws.tokens, (const bf16*)W.embed_tok, lo, s.vocab_local, s.hidden, partial);
+    else
+        embed_kernel<float><<<M, 256, 0, st>>>(ws.tokens, (const float*)W.embed_tok, lo, s.vocab_local, s.hidden, partial);
+    MPSW_CU(cudaGetLastError());
+    return 1;
+}
+
+int fwd_reduce_ln(const FwdShape& s, int M, const float* const* peer_partials, int n_peers, const float* residual,
+                  const void* bias, const void* pos_table, const int32_t* pos, const void* gamma, const void* beta,
+                  float* x_out, void* ln_out, cudaStream_t st) {
+    Peers P{};
+    if (n_peers < 1 || n_peers > 8) throw Error(MPSW_EINVAL, "1..8 peers");
+    for (int i = 0; i < n_peers; ++i) P.p[i] = peer_partials[i];
+    P.n = n_peers;
+    const size_t smem = (size_t)s.hidden * 4;
+    if (s.dtype == MPSW_BF16)
+        reduce_ln_kernel<bf16><<<M, 256, smem, st>>>(P, residual, (const bf16*)bias, (const bf16*)pos_table, pos,
+                                                     (const bf16*)gamma, (const bf16*)beta, x_out, (bf16*)ln_out, s.hidden);
+    else
+        reduce_ln_kernel<float><<<M, 256, smem, st>>>(P, residual, (const float*)bias, (const float*)pos_table, pos,
+                                                      (const float*)gamma, (const float*)beta, x_out, (float*)ln_out,
+                                                      s.hidden);
+    MPSW_CU(cudaGetLastError());
+    return 1;
+}
+
+int fwd_qkv(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M, cudaStream_t st) {
+    const int hl = s.heads_local * s.head_dim;
+    GemmArgs g{};
+    g.A = ws.a; g.a_rows = nullptr; g.M = M; g.K = s.hidden; g.lda = s.hidden;
+    // output layout [M, 3*hl] = [q | k | v]; q scaled after its bias (HF:opt.py:151)
+    g.seg[0] = {L.q_w, L.q_b, hl, 1.0f / sqrtf((float)s.head_dim), 0};
+    g.seg[1] = {L.k_w, L.k_b, hl, 1.0f, hl};
+    g.seg[2] = {L.v_w, L.v_b, hl, 1.0f, 2 * hl};
+    g.nseg = 3; g.out = ws.qkv; g.ldo = 3 * hl;
+    launch_gemm(s.dtype, EPI_F32, g, st);
+    return 1;
+}
+
+int fwd_attention(const FwdShape& s, const FwdWorkspace& ws, int B, cudaStream_t st) {
+    const int hl = s.heads_local * s.head_dim;
+    dim3 grid(B, s.heads_local);
+    const int32_t* seq_start = ws.meta;
+    if (s.dtype == MPSW_BF16)
+        attention_kernel<bf16><<<grid, 128, 0, st>>>(ws.qkv, seq_start, (bf16*)ws.o, hl, s.head_dim);
+    else
+        attention_kernel<float><<<grid, 128, 0, st>>>(ws.qkv, seq_start, (float*)ws.o, hl, s.head_dim);
+    MPSW_CU(cudaGetLastError());
+    return 1;
+}
+
+int fwd_out_proj(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M, float* partial,
+                 cudaStream_t st) {
+    const int hl = s.heads_local * s.head_dim;
+    GemmArgs g{};
+    g.A = ws.o; g.M = M; g.K = hl; g.lda = hl;
+    g.seg[0] = {L.o_w, nullptr, s.hidden, 1.0f, 0};   // bias added once after the all-reduce
+    g.nseg = 1; g.out = partial; g.ldo = s.hidden;
+    launch_gemm(s.dtype, EPI_F32, g, st);
+    return 1;
+}
+
+int fwd_fc1(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M, cudaStream_t st) {
+    GemmArgs g{};
+    g.A = ws.a; g.M = M; g.K = s.hidden; g.lda = s.hidden;
+    g.seg[0] = {L.fc1_w, L.fc1_b, s.ffn_local, 1.0f, 0};
+    g.nseg = 1; g.out = ws.r; g.ldo = s.ffn_local;
+    launch_gemm(s.dtype, EPI_RELU_T, g, st);
+    return 1;
+}
+
+int fwd_fc2(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M, float* partial,
+            cudaStream_t st) {
+    GemmArgs g{};
+    g.A = ws.r; g.M = M; g.K = s.ffn_local; g.lda = s.ffn_local;
+    g.seg[0] = {L.fc2_w, nullptr, s.hidden, 1.0f, 0};
+    g.nseg = 1; g.out = partial; g.ldo = s.hidden;
+    launch_gemm(s.dtype, EPI_F32, g, st);
+    return 1;
+}
+
+int fwd_lm_head(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, int B, cudaStream_t st) {
+    GemmArgs g{};
+    g.A = ws.a; g.a_rows = ws.meta + (B + 1); g.M = B; g.K = s.hidden; g.lda = s.hidden;
+    g.seg[0] = {W.embed_tok, nullptr, s.vocab_local, 1.0f, 0};
+    g.nseg = 1; g.out = ws.logits; g.ldo = s.vocab_local;
+    launch_gemm(s.dtype, EPI_F32, g, st);
+    return 1;
+}
+
+}  // namespace mpsw

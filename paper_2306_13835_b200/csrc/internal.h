@@ -1,0 +1,111 @@
+// Internal declarations of the mpsw library (not part of the C-ABI).
+#pragma once
+
+#include "../../include/mpsw.h"
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace mpsw {
+
+// ---------------------------------------------------------------- errors
+std::string& tls_error();
+mpsw_status set_error(mpsw_status s, const std::string& msg);
+
+struct Error : std::runtime_error {
+    mpsw_status status;
+    Error(mpsw_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+#define MPSW_CU(call)                                                                        \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            throw ::mpsw::Error(MPSW_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + \
+                                " (" __FILE__ ":" + std::to_string(__LINE__) + ")");         \
+    } while (0)
+
+// ---------------------------------------------------------------- layout (C2, product side)
+struct Layout {
+    std::vector<mpsw_tensor_desc> t;
+    uint64_t bytes = 0;
+};
+mpsw_status compute_layout(const mpsw_opt_dims& d, int tp, int rank, int dtype, Layout& out);
+
+// ---------------------------------------------------------------- synthetic fill (C0, product side)
+void synth_fill_arena(const mpsw_opt_dims& d, int tp, int rank, int dtype, uint64_t seed,
+                      uint8_t* dst, int threads);
+uint64_t host_checksum(const uint8_t* p, uint64_t bytes, int threads);
+
+// ---------------------------------------------------------------- swap / checksum kernels
+// Zero-copy copy: 128-bit loads from `src` (mapped pinned host OR device) and 128-bit stores
+// to `dst` (device OR mapped pinned host). bytes % 16 == 0, pointers 16-B aligned.
+void launch_zero_copy(void* dst, const void* src, uint64_t bytes, int ctas, cudaStream_t s);
+// Order-independent checksum (C4) of a device buffer; result accumulated into *d_out.
+void launch_checksum(const void* buf, uint64_t bytes, unsigned long long* d_out, cudaStream_t s);
+
+// ---------------------------------------------------------------- forward (per rank)
+struct TensorPtrs {          // device pointers of one rank's shard inside a slot
+    const void* embed_tok;   // [V/t, h]
+    const void* embed_pos;   // [P, h]
+    const void* lnf_w;
+    const void* lnf_b;
+    struct Layer {
+        const void *k_w, *k_b, *v_w, *v_b, *q_w, *q_b, *o_w, *o_b;
+        const void *ln1_w, *ln1_b, *fc1_w, *fc1_b, *fc2_w, *fc2_b, *ln2_w, *ln2_b;
+    };
+    std::vector<Layer> layers;
+};
+
+struct FwdShape {
+    int n_layers, hidden, heads_local, head_dim, ffn_local, vocab_local, vocab, tp, rank;
+    int dtype;               // MPSW_BF16 / MPSW_FP32
+};
+
+struct FwdWorkspace {        // device buffers of one rank (sized for max_batch*max_tokens rows)
+    float* x = nullptr;            // residual stream [M, h] fp32
+    void* a = nullptr;             // LN output (GEMM A operand) [M, h]
+    float* qkv = nullptr;          // [M, 3*h/t] fp32 (q pre-scaled)
+    void* o = nullptr;             // attention output [M, h/t]
+    void* r = nullptr;             // relu output [M, ff/t]
+    float* partial[2] = {nullptr, nullptr};   // row-parallel partials [M, h] fp32 (peers read)
+    float* logits = nullptr;       // [B, V/t] fp32
+    int32_t* tokens = nullptr;     // [M]
+    int32_t* meta = nullptr;       // [3*Bmax + M]: seq_start[B+1], last_row[B], pos[M]
+    void* base = nullptr;
+    size_t bytes = 0;
+};
+size_t workspace_bytes(const FwdShape& s, int max_rows, int max_batch);
+void workspace_carve(FwdWorkspace& w, const FwdShape& s, int max_rows, int max_batch, void* base);
+
+// Kernel launchers (forward.cu). Each returns the number of kernels launched.
+int fwd_embed(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, int M, float* partial,
+              cudaStream_t st);
+int fwd_reduce_ln(const FwdShape& s, int M, const float* const* peer_partials, int n_peers,
+                  const float* residual, const void* bias, const void* pos_table, const int32_t* pos,
+                  const void* gamma, const void* beta, float* x_out, void* ln_out, cudaStream_t st);
+int fwd_qkv(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M, cudaStream_t st);
+int fwd_attention(const FwdShape& s, const FwdWorkspace& ws, int B, cudaStream_t st);
+int fwd_out_proj(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M,
+                 float* partial, cudaStream_t st);
+int fwd_fc1(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M, cudaStream_t st);
+int fwd_fc2(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M, float* partial,
+            cudaStream_t st);
+int fwd_lm_head(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, int B, cudaStream_t st);
+
+inline double now_s(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace mpsw

@@ -1,0 +1,231 @@
+"""Thin ctypes binding of libmpsw.so (include/mpsw.h). Argument marshalling only: every step of
+the hot path (swaps, scheduling, the TP forward, checksums) runs inside the C++/CUDA library.
+Fails loudly if the library is missing — there is no CPU fallback.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmpsw.so")
+
+OK, EINVAL, ENOMEM, EBUSY, ENOENT, EAGAIN, ECUDA, ENCCL, EINVARIANT, ETIMEDOUT = 0, -1, -2, -3, -4, -5, -6, -7, -8, -9
+STATUS_NAMES = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "EBUSY", -4: "ENOENT", -5: "EAGAIN", -6: "ECUDA",
+                -7: "ENCCL", -8: "EINVARIANT", -9: "ETIMEDOUT"}
+BF16, FP32 = 0, 1
+SWAP_AUTO, SWAP_COPY_ENGINE, SWAP_ZERO_COPY = 0, 1, 2
+EVICTED, LOADING, RESIDENT, OFFLOADING = 0, 1, 2, 3
+NOOP_TICKET = (1 << 64) - 1
+
+
+class MpswError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [("n_gpus", C.c_int), ("device_ids", C.POINTER(C.c_int)), ("tp", C.c_int),
+                ("param_budget_bytes_per_gpu", C.c_uint64), ("workspace_bytes_per_gpu", C.c_uint64),
+                ("max_batch", C.c_int), ("max_tokens", C.c_int), ("dtype", C.c_int),
+                ("max_inflight_batches", C.c_int), ("swap_mode", C.c_int), ("chunk_bytes", C.c_uint64),
+                ("writeback", C.c_int), ("trace", C.c_int), ("zc_ctas", C.c_int)]
+
+
+class OptDims(C.Structure):
+    _fields_ = [("n_layers", C.c_int), ("hidden", C.c_int), ("heads", C.c_int), ("ffn", C.c_int),
+                ("vocab", C.c_int), ("max_pos", C.c_int)]
+
+
+class TensorDesc(C.Structure):
+    _fields_ = [("name", C.c_char * 64), ("offset", C.c_uint64), ("bytes", C.c_uint64), ("rows", C.c_int),
+                ("cols", C.c_int), ("split", C.c_int)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("swaps_in", C.c_uint64), ("swaps_out", C.c_uint64), ("batches", C.c_uint64),
+                ("requests", C.c_uint64), ("rejected", C.c_uint64), ("k_slots", C.c_int),
+                ("shard_bytes", C.c_uint64)]
+
+
+_P = C.c_void_p
+_SIGS = {
+    "mpsw_init": [C.POINTER(Config), C.POINTER(_P)],
+    "mpsw_shutdown": [_P],
+    "mpsw_shard_layout": [C.POINTER(OptDims), C.c_int, C.c_int, C.c_int, C.POINTER(TensorDesc), C.c_int,
+                          C.POINTER(C.c_int), C.POINTER(C.c_uint64)],
+    "mpsw_register_model": [_P, C.POINTER(OptDims), C.c_int, C.POINTER(_P), C.POINTER(C.c_uint64),
+                            C.POINTER(C.c_int)],
+    "mpsw_model_arena": [_P, C.c_int, C.c_int, C.POINTER(_P), C.POINTER(C.c_uint64)],
+    "mpsw_synth_fill": [_P, C.c_int, C.c_int, C.c_uint64, C.c_int],
+    "mpsw_swap_in": [_P, C.c_int, C.POINTER(C.c_uint64)],
+    "mpsw_swap_out": [_P, C.c_int, C.POINTER(C.c_uint64)],
+    "mpsw_wait": [_P, C.c_uint64, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double)],
+    "mpsw_entry_gpu_ms": [_P, C.c_uint64, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_float)],
+    "mpsw_request": [_P, C.c_int, C.POINTER(C.c_int32), C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_int64)],
+    "mpsw_poll": [_P, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double)],
+    "mpsw_wait_request": [_P, C.c_int64, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double)],
+    "mpsw_checksum": [_P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint64)],
+    "mpsw_peek": [_P, C.c_int, C.c_int, C.c_uint64, C.c_uint64, _P],
+    "mpsw_residency": [_P, C.c_int, C.POINTER(C.c_int)],
+    "mpsw_trace_dump": [_P, C.c_char_p],
+    "mpsw_get_stats": [_P, C.POINTER(Stats)],
+}
+
+_lib = None
+
+
+def lib():
+    """Load libmpsw.so (raises if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built; run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        L.mpsw_last_error.restype = C.c_char_p
+        L.mpsw_last_error.argtypes = []
+        _lib = L
+    return _lib
+
+
+def _check(st):
+    if st != OK:
+        raise MpswError(st, lib().mpsw_last_error().decode())
+    return st
+
+
+def dims_of(d):
+    return OptDims(d.n_layers, d.hidden, d.heads, d.ffn, d.vocab, d.max_pos)
+
+
+def shard_layout(dims, tp, rank=0, dtype=BF16):
+    od = dims_of(dims)
+    n = C.c_int()
+    sb = C.c_uint64()
+    _check(lib().mpsw_shard_layout(C.byref(od), tp, rank, dtype, None, 0, C.byref(n), C.byref(sb)))
+    arr = (TensorDesc * n.value)()
+    _check(lib().mpsw_shard_layout(C.byref(od), tp, rank, dtype, arr, n.value, C.byref(n), C.byref(sb)))
+    return [(t.name.decode(), t.offset, t.bytes, t.rows, t.cols, t.split) for t in arr], sb.value
+
+
+class Ctx:
+    """One TP group (see include/mpsw.h). Methods mirror the C-ABI names."""
+
+    def __init__(self, device_ids=(0,), budget=1 << 30, max_batch=8, max_tokens=8, dtype=BF16,
+                 max_inflight=1, swap_mode=SWAP_AUTO, chunk_bytes=0, writeback=1, trace=0, zc_ctas=0):
+        self._ids = (C.c_int * len(device_ids))(*device_ids)
+        self.tp = len(device_ids)
+        cfg = Config(len(device_ids), self._ids, len(device_ids), budget, 0, max_batch, max_tokens, dtype,
+                     max_inflight, swap_mode, chunk_bytes, writeback, trace, zc_ctas)
+        h = _P()
+        _check(lib().mpsw_init(C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.dtype = dtype
+        self.vocab = None
+
+    def close(self):
+        if self.h:
+            lib().mpsw_shutdown(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def register_model(self, dims, shards=None):
+        od = dims_of(dims)
+        mid = C.c_int()
+        if shards is None:
+            _check(lib().mpsw_register_model(self.h, C.byref(od), self.tp, None, None, C.byref(mid)))
+        else:
+            arrs = [np.ascontiguousarray(s) for s in shards]
+            ptrs = (_P * self.tp)(*[a.ctypes.data for a in arrs])
+            sizes = (C.c_uint64 * self.tp)(*[a.nbytes for a in arrs])
+            _check(lib().mpsw_register_model(self.h, C.byref(od), self.tp, ptrs, sizes, C.byref(mid)))
+        self.vocab = dims.vocab
+        return mid.value
+
+    def model_arena(self, model_id, rank):
+        """numpy uint8 view of the pinned arena (library-owned memory)."""
+        p = _P()
+        n = C.c_uint64()
+        _check(lib().mpsw_model_arena(self.h, model_id, rank, C.byref(p), C.byref(n)))
+        return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint8)), shape=(n.value,))
+
+    def synth_fill(self, model_id, seed, rank=-1, threads=0):
+        _check(lib().mpsw_synth_fill(self.h, model_id, rank, seed, threads))
+
+    def swap_in(self, model_id):
+        t = C.c_uint64()
+        _check(lib().mpsw_swap_in(self.h, model_id, C.byref(t)))
+        return t.value
+
+    def swap_out(self, model_id):
+        t = C.c_uint64()
+        _check(lib().mpsw_swap_out(self.h, model_id, C.byref(t)))
+        return t.value
+
+    def wait(self, ticket, timeout=-1.0):
+        ts = C.c_double()
+        td = (C.c_double * self.tp)()
+        _check(lib().mpsw_wait(self.h, ticket, timeout, C.byref(ts), td))
+        return ts.value, list(td)
+
+    def entry_gpu_ms(self, ticket):
+        k, m = C.c_int(), C.c_int()
+        ms = (C.c_float * self.tp)()
+        _check(lib().mpsw_entry_gpu_ms(self.h, ticket, C.byref(k), C.byref(m), ms))
+        return k.value, m.value, list(ms)
+
+    def request(self, model_id, tokens, out=None):
+        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        if out is None:
+            out = np.empty(self.vocab, np.float32)
+        rid = C.c_int64()
+        _check(lib().mpsw_request(self.h, model_id, tok.ctypes.data_as(C.POINTER(C.c_int32)), tok.size,
+                                  out.ctypes.data_as(C.POINTER(C.c_float)), C.byref(rid)))
+        return rid.value, out
+
+    def poll(self, rid):
+        a, d = C.c_double(), C.c_double()
+        st = lib().mpsw_poll(self.h, rid, C.byref(a), C.byref(d))
+        if st == EAGAIN:
+            return None
+        _check(st)
+        return a.value, d.value
+
+    def wait_request(self, rid, timeout=-1.0):
+        a, d = C.c_double(), C.c_double()
+        _check(lib().mpsw_wait_request(self.h, rid, timeout, C.byref(a), C.byref(d)))
+        return a.value, d.value
+
+    def checksum(self, model_id, rank, on_device=True):
+        h = C.c_uint64()
+        _check(lib().mpsw_checksum(self.h, model_id, rank, int(on_device), C.byref(h)))
+        return h.value
+
+    def peek(self, model_id, rank, offset, nbytes):
+        buf = np.empty(nbytes, np.uint8)
+        _check(lib().mpsw_peek(self.h, model_id, rank, offset, nbytes, buf.ctypes.data))
+        return buf
+
+    def residency(self, model_id):
+        s = C.c_int()
+        _check(lib().mpsw_residency(self.h, model_id, C.byref(s)))
+        return s.value
+
+    def trace_dump(self, path):
+        _check(lib().mpsw_trace_dump(self.h, path.encode()))
+
+    def stats(self):
+        s = Stats()
+        _check(lib().mpsw_get_stats(self.h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in Stats._fields_}

