@@ -48,7 +48,7 @@ def test_gamma_trace_replay_and_outcomes(tmp_path, tp, D):
     S_ = layout.shard_bytes(d, tp)
     trace = gamma_trace([20, 5, 5], cv=4.0, duration=0.5, seed=1, token_len=8, vocab=d.vocab)
     import time
-    with M.Ctx(device_ids=(0,) * tp, budget=k * ((S_ + (2 << 20) - 1) // (2 << 20)) * (2 << 20), max_batch=mb,
+    with M.Ctx(device_ids=(0,) * tp, budget=k * ((S_ + 4095) // 4096 * 4096), max_batch=mb,
                max_tokens=8, trace=1, max_inflight=D) as ctx:
         ids = [ctx.register_model(d) for _ in range(nm)]
         for m in ids:
@@ -69,6 +69,7 @@ def test_gamma_trace_replay_and_outcomes(tmp_path, tp, D):
         p = str(tmp_path / "trace.ndjson")
         ctx.trace_dump(p)
         st = ctx.stats()
+    assert st["k_slots"] == k
     replay_check(p, nm, k, tp, mb, D)
     assert st["swaps_in"] >= nm
     Ws = {m: layout.full_tensors(d, 500 + m) for m in range(nm)}
