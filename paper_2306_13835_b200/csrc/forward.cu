@@ -71,16 +71,21 @@ struct GemmArgs {
     int ldo;
 };
 
-constexpr int kGemmWarps = 4;
-constexpr int kGemmR = 2;   // W rows per warp
+// One CTA owns kGemmR rows of W; its 8 warps split K (warp w takes 16-byte chunks
+// w*32+lane, w*32+lane+256, ...), so each lane keeps kGemmR*2 independent 16-B weight loads in
+// flight (the k loop is unrolled by 2) and a CTA streams 8 KB of weights per iteration. The
+// reduction order is fixed — lane-sequential, warp butterfly, then warps 0..7 in order — and
+// depends only on K, never on M or on the batch composition (bitwise batch invariance).
+constexpr int kGemmWarps = 8;
+constexpr int kGemmR = 4;   // W rows per CTA
 
 template <typename T, int MT, int EPI>
 __global__ void __launch_bounds__(kGemmWarps * 32) gemm_rows_kernel(GemmArgs g) {
     constexpr int V = Vec<T>::N;
+    __shared__ float red[kGemmWarps][kGemmR * MT];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int n0 = (blockIdx.x * kGemmWarps + warp) * kGemmR;
-    if (n0 >= g.n_total) return;
+    const int n0 = blockIdx.x * kGemmR;
     const T* wrow[kGemmR];
     const T* brow[kGemmR];
     float scale[kGemmR];
@@ -99,6 +104,7 @@ __global__ void __launch_bounds__(kGemmWarps * 32) gemm_rows_kernel(GemmArgs g) 
         ocol[r] = g.seg[s].out_col0 + n;
     }
     const T* A = reinterpret_cast<const T*>(g.A);
+    constexpr int kStep = kGemmWarps * 32 * V;
     for (int m0 = 0; m0 < g.M; m0 += MT) {
         float acc[kGemmR][MT];
 #pragma unroll
@@ -112,53 +118,78 @@ __global__ void __launch_bounds__(kGemmWarps * 32) gemm_rows_kernel(GemmArgs g) 
             const int ar = g.a_rows ? g.a_rows[mm] : mm;
             arow[m] = A + (size_t)ar * g.lda;
         }
-        for (int k = lane * V; k < g.K; k += 32 * V) {
-            float w[kGemmR][V];
+        int k = (warp * 32 + lane) * V;
+        for (; k + kStep < g.K; k += 2 * kStep) {
+            float w0[kGemmR][V], w1[kGemmR][V];
 #pragma unroll
-            for (int r = 0; r < kGemmR; ++r) Vec<T>::load(wrow[r] + k, w[r]);
+            for (int r = 0; r < kGemmR; ++r) {
+                Vec<T>::load(wrow[r] + k, w0[r]);
+                Vec<T>::load(wrow[r] + k + kStep, w1[r]);
+            }
 #pragma unroll
             for (int m = 0; m < MT; ++m) {
-                float a[V];
-                Vec<T>::load(arow[m] + k, a);
+                float a0[V], a1[V];
+                Vec<T>::load(arow[m] + k, a0);
+                Vec<T>::load(arow[m] + k + kStep, a1);
+#pragma unroll
+                for (int r = 0; r < kGemmR; ++r) {
+#pragma unroll
+                    for (int v = 0; v < V; ++v) acc[r][m] = fmaf(w0[r][v], a0[v], acc[r][m]);
+#pragma unroll
+                    for (int v = 0; v < V; ++v) acc[r][m] = fmaf(w1[r][v], a1[v], acc[r][m]);
+                }
+            }
+        }
+        if (k < g.K) {
+            float w0[kGemmR][V];
+#pragma unroll
+            for (int r = 0; r < kGemmR; ++r) Vec<T>::load(wrow[r] + k, w0[r]);
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                float a0[V];
+                Vec<T>::load(arow[m] + k, a0);
 #pragma unroll
                 for (int r = 0; r < kGemmR; ++r)
 #pragma unroll
-                    for (int v = 0; v < V; ++v) acc[r][m] = fmaf(w[r][v], a[v], acc[r][m]);
+                    for (int v = 0; v < V; ++v) acc[r][m] = fmaf(w0[r][v], a0[v], acc[r][m]);
             }
         }
 #pragma unroll
         for (int r = 0; r < kGemmR; ++r)
 #pragma unroll
-            for (int m = 0; m < MT; ++m)
+            for (int m = 0; m < MT; ++m) {
+                float v = acc[r][m];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) acc[r][m] += __shfl_xor_sync(0xffffffffu, acc[r][m], o);
-        if (lane == 0) {
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) red[warp][r * MT + m] = v;
+            }
+        __syncthreads();
+        if (threadIdx.x < kGemmR * MT) {
+            const int r = threadIdx.x / MT, m = threadIdx.x % MT;
+            float v = red[0][threadIdx.x];
 #pragma unroll
-            for (int r = 0; r < kGemmR; ++r) {
-                if (!valid[r]) continue;
-                const float b = brow[r] ? to_f(*brow[r]) : 0.f;
+            for (int w = 1; w < kGemmWarps; ++w) v += red[w][threadIdx.x];
+            // select this thread's row (r is not a compile-time index here)
+            bool ok = false; const T* b = nullptr; float sc = 1.f; int oc = 0;
 #pragma unroll
-                for (int m = 0; m < MT; ++m) {
-                    if (m0 + m >= g.M) break;
-                    float v = acc[r][m];
-                    if (brow[r]) v = v + b;
-                    if (EPI == EPI_F32) {
-                        v = v * scale[r];
-                        reinterpret_cast<float*>(g.out)[(size_t)(m0 + m) * g.ldo + ocol[r]] = v;
-                    } else {
-                        v = fmaxf(v, 0.f);
-                        reinterpret_cast<T*>(g.out)[(size_t)(m0 + m) * g.ldo + ocol[r]] = from_f<T>(v);
-                    }
+            for (int rr = 0; rr < kGemmR; ++rr)
+                if (rr == r) { ok = valid[rr]; b = brow[rr]; sc = scale[rr]; oc = ocol[rr]; }
+            if (ok && m0 + m < g.M) {
+                if (b) v = v + to_f(*b);
+                if (EPI == EPI_F32) {
+                    reinterpret_cast<float*>(g.out)[(size_t)(m0 + m) * g.ldo + oc] = v * sc;
+                } else {
+                    reinterpret_cast<T*>(g.out)[(size_t)(m0 + m) * g.ldo + oc] = from_f<T>(fmaxf(v, 0.f));
                 }
             }
         }
+        __syncthreads();
     }
 }
 
 template <typename T, int EPI>
 void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
-    const int rows_per_cta = kGemmWarps * kGemmR;
-    const int grid = (g.n_total + rows_per_cta - 1) / rows_per_cta;
+    const int grid = (g.n_total + kGemmR - 1) / kGemmR;
     const int threads = kGemmWarps * 32;
     if (g.M <= 1) gemm_rows_kernel<T, 1, EPI><<<grid, threads, 0, st>>>(g);
     else if (g.M <= 2) gemm_rows_kernel<T, 2, EPI><<<grid, threads, 0, st>>>(g);
@@ -208,37 +239,80 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
     return s;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256) reduce_ln_kernel(Peers peers, const float* __restrict__ residual,
-                                                        const T* __restrict__ bias, const T* __restrict__ pos_table,
-                                                        const int32_t* __restrict__ pos, const T* __restrict__ gamma,
-                                                        const T* __restrict__ beta, float* __restrict__ x_out,
-                                                        T* __restrict__ ln_out, int h) {
-    extern __shared__ float xs[];
+// One CTA (512 threads) per row; each thread owns VPT float4 column groups kept in registers,
+// so every global load of the row (t peer partials, residual, bias, position row) is issued
+// before the first use — the kernel is latency-bound at M = 2 rows and this keeps one round
+// trip per operand instead of one per element.
+constexpr int kLnThreads = 512;
+
+template <typename T> __device__ __forceinline__ float4 ld4(const T* p);
+template <> __device__ __forceinline__ float4 ld4<float>(const float* p) { return *reinterpret_cast<const float4*>(p); }
+template <> __device__ __forceinline__ float4 ld4<bf16>(const bf16* p) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+}
+
+template <typename T, int VPT>
+__global__ void __launch_bounds__(kLnThreads) reduce_ln_kernel(Peers peers, const float* __restrict__ residual,
+                                                              const T* __restrict__ bias, const T* __restrict__ pos_table,
+                                                              const int32_t* __restrict__ pos, const T* __restrict__ gamma,
+                                                              const T* __restrict__ beta, float* __restrict__ x_out,
+                                                              T* __restrict__ ln_out, int h) {
     __shared__ float red[32];
     const int m = blockIdx.x;
     const size_t row = (size_t)m * h;
+    const int h4 = h / 4;
+    float4 x[VPT];
     float lsum = 0.f;
-    for (int j = threadIdx.x; j < h; j += blockDim.x) {
-        float s = peers.p[0][row + j];
-        for (int r = 1; r < peers.n; ++r) s += peers.p[r][row + j];   // TP all-reduce (rank order)
-        if (bias) s = s + to_f(bias[j]);
-        if (pos_table) s = s + to_f(pos_table[(size_t)pos[m] * h + j]);
-        if (residual) s = residual[row + j] + s;
-        xs[j] = s;
-        x_out[row + j] = s;
-        lsum += s;
+    const T* prow = pos_table ? pos_table + (size_t)pos[m] * h : nullptr;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int j4 = threadIdx.x + i * kLnThreads;
+        if (j4 >= h4) break;
+        const int j = 4 * j4;
+        float4 s = *reinterpret_cast<const float4*>(peers.p[0] + row + j);
+#pragma unroll
+        for (int r = 1; r < 8; ++r) {                          // TP all-reduce in rank order
+            if (r < peers.n) {
+                const float4 q = *reinterpret_cast<const float4*>(peers.p[r] + row + j);
+                s.x += q.x; s.y += q.y; s.z += q.z; s.w += q.w;
+            }
+        }
+        if (bias) { const float4 b = ld4<T>(bias + j); s.x = s.x + b.x; s.y = s.y + b.y; s.z = s.z + b.z; s.w = s.w + b.w; }
+        if (prow) { const float4 p = ld4<T>(prow + j); s.x = s.x + p.x; s.y = s.y + p.y; s.z = s.z + p.z; s.w = s.w + p.w; }
+        if (residual) {
+            const float4 q = *reinterpret_cast<const float4*>(residual + row + j);
+            s.x = q.x + s.x; s.y = q.y + s.y; s.z = q.z + s.z; s.w = q.w + s.w;
+        }
+        x[i] = s;
+        *reinterpret_cast<float4*>(x_out + row + j) = s;
+        lsum += (s.x + s.y) + (s.z + s.w);
     }
     const float mean = block_sum(lsum, red) / (float)h;
     float lvar = 0.f;
-    for (int j = threadIdx.x; j < h; j += blockDim.x) {
-        const float d = xs[j] - mean;
-        lvar += d * d;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int j4 = threadIdx.x + i * kLnThreads;
+        if (j4 >= h4) break;
+        const float a = x[i].x - mean, b = x[i].y - mean, c = x[i].z - mean, d = x[i].w - mean;
+        lvar += (a * a + b * b) + (c * c + d * d);
     }
     const float var = block_sum(lvar, red) / (float)h;
     const float den = sqrtf(var + 1e-5f);
-    for (int j = threadIdx.x; j < h; j += blockDim.x)
-        ln_out[row + j] = from_f<T>(((xs[j] - mean) / den) * to_f(gamma[j]) + to_f(beta[j]));
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int j4 = threadIdx.x + i * kLnThreads;
+        if (j4 >= h4) break;
+        const int j = 4 * j4;
+        const float4 g4 = ld4<T>(gamma + j), b4 = ld4<T>(beta + j);
+        T* o = ln_out + row + j;
+        o[0] = from_f<T>(((x[i].x - mean) / den) * g4.x + b4.x);
+        o[1] = from_f<T>(((x[i].y - mean) / den) * g4.y + b4.y);
+        o[2] = from_f<T>(((x[i].z - mean) / den) * g4.z + b4.z);
+        o[3] = from_f<T>(((x[i].w - mean) / den) * g4.w + b4.w);
+    }
 }
 
 // ------------------------------------------------------------------ attention (L <= 128)
@@ -343,6 +417,30 @@ int fwd_embed(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, in
     return 1;
 }
 
+template <typename T, int VPT>
+static void launch_ln(int M, const Peers& P, const float* residual, const void* bias, const void* pos_table,
+                      const int32_t* pos, const void* gamma, const void* beta, float* x_out, void* ln_out, int h,
+                      cudaStream_t st) {
+    reduce_ln_kernel<T, VPT><<<M, kLnThreads, 0, st>>>(P, residual, (const T*)bias, (const T*)pos_table, pos,
+                                                       (const T*)gamma, (const T*)beta, x_out, (T*)ln_out, h);
+}
+
+template <typename T>
+static void launch_ln_t(int M, const Peers& P, const float* residual, const void* bias, const void* pos_table,
+                        const int32_t* pos, const void* gamma, const void* beta, float* x_out, void* ln_out, int h,
+                        cudaStream_t st) {
+    const int vpt = (h / 4 + kLnThreads - 1) / kLnThreads;
+    switch (vpt) {
+        case 1: launch_ln<T, 1>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, h, st); break;
+        case 2: launch_ln<T, 2>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, h, st); break;
+        case 3: launch_ln<T, 3>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, h, st); break;
+        case 4: launch_ln<T, 4>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, h, st); break;
+        case 5: launch_ln<T, 5>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, h, st); break;
+        case 6: launch_ln<T, 6>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, h, st); break;
+        default: throw Error(MPSW_EINVAL, "hidden too large for reduce_ln (max 12288)");
+    }
+}
+
 int fwd_reduce_ln(const FwdShape& s, int M, const float* const* peer_partials, int n_peers, const float* residual,
                   const void* bias, const void* pos_table, const int32_t* pos, const void* gamma, const void* beta,
                   float* x_out, void* ln_out, cudaStream_t st) {
@@ -350,14 +448,10 @@ int fwd_reduce_ln(const FwdShape& s, int M, const float* const* peer_partials, i
     if (n_peers < 1 || n_peers > 8) throw Error(MPSW_EINVAL, "1..8 peers");
     for (int i = 0; i < n_peers; ++i) P.p[i] = peer_partials[i];
     P.n = n_peers;
-    const size_t smem = (size_t)s.hidden * 4;
     if (s.dtype == MPSW_BF16)
-        reduce_ln_kernel<bf16><<<M, 256, smem, st>>>(P, residual, (const bf16*)bias, (const bf16*)pos_table, pos,
-                                                     (const bf16*)gamma, (const bf16*)beta, x_out, (bf16*)ln_out, s.hidden);
+        launch_ln_t<bf16>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, s.hidden, st);
     else
-        reduce_ln_kernel<float><<<M, 256, smem, st>>>(P, residual, (const float*)bias, (const float*)pos_table, pos,
-                                                      (const float*)gamma, (const float*)beta, x_out, (float*)ln_out,
-                                                      s.hidden);
+        launch_ln_t<float>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, s.hidden, st);
     MPSW_CU(cudaGetLastError());
     return 1;
 }
@@ -367,7 +461,7 @@ int fwd_qkv(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& w
     GemmArgs g{};
     g.A = ws.a; g.a_rows = nullptr; g.M = M; g.K = s.hidden; g.lda = s.hidden;
     // output layout [M, 3*hl] = [q | k | v]; q scaled after its bias (HF:opt.py:151)
-    g.seg[0] = {L.q_w, L.q_b, hl, 1.0f / sqrtf((float)s.head_dim), 0};
+    g.seg[0] = {L.q_w, L.q_b, hl, (float)(1.0 / sqrt((double)s.head_dim)), 0};
     g.seg[1] = {L.k_w, L.k_b, hl, 1.0f, hl};
     g.seg[2] = {L.v_w, L.v_b, hl, 1.0f, 2 * hl};
     g.nseg = 3; g.out = ws.qkv; g.ldo = 3 * hl;

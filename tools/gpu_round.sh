@@ -1,17 +1,11 @@
 #!/bin/bash
-# One GPU round: build, GPU tests, bench (+ writeback variant), ncu launch list + full captures.
+# One GPU round: build, GPU tests, smoke, bench, probes.
 set -x
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()"
 timeout 1500 python -m pytest tests -m gpu -q -rf --tb=short > gpurun_out/pytest_gpu.txt 2>&1
 timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.txt 2>&1
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-timeout 900 python bench.py --writeback 1 --no-cpu-baseline > gpurun_out/bench_wb.json 2> gpurun_out/bench_wb.err
+timeout 300 python tools/ce_multi_probe.py > gpurun_out/ce_multi.txt 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --n-models 2 > gpurun_out/bench_under_ncu.json 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_rows -s 120 -c 3 -f -o gpurun_out/prof_gemm \
-    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --n-models 2 > gpurun_out/prof_gemm.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:zero_copy -c 1 -f -o gpurun_out/prof_zc \
-    python tools/zc_one.py > gpurun_out/prof_zc.log 2>&1
-python tools/zc_one.py opt-1.3b 32 > gpurun_out/zc_timing.txt 2>&1
-python tools/zc_one.py opt-1.3b 148 >> gpurun_out/zc_timing.txt 2>&1
