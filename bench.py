@@ -173,29 +173,43 @@ def run_cpu_baseline(d, S_r, tokens, steps, sample_bytes=1 << 30):
 
 
 # ----------------------------------------------------------------------------- our arm
+def bench_device():
+    """One GPU per rank (LOCAL_RANK). MPSW_BENCH_DEVICE0=1 maps every rank to cuda:0 — only to
+    exercise the N > 1 code path on a one-GPU box (numbers are then meaningless)."""
+    return 0 if os.environ.get("MPSW_BENCH_DEVICE0") == "1" else int(os.environ.get("LOCAL_RANK", 0))
+
+
 def run_ours(args, rank, world):
+    """N = 1: one process, TP = 1. N > 1 (torchrun): one process per GPU forming ONE TP group of
+    t = N ranks (library multi-process mode): every request swaps the next model's t shards in
+    concurrently, one per GPU over its own PCIe link."""
     import torch
+    import torch.distributed as dist
     from paper_2306_13835_b200 import mpsw as M
     from synth import opt_dims, round_robin_blocking
     from oracle import layout as OL_sizes   # sizes only, for reporting (no oracle compute)
 
-    dev = int(os.environ.get("LOCAL_RANK", 0))
+    dev = bench_device()
     torch.cuda.set_device(dev)
     d = opt_dims(args.model)
-    tp = 1                                   # one process per GPU; see DESIGN.md §Multi-GPU
+    tp = world
     M.lib()
     ce_peak = ce_peak_h2d(dev)
     S_r = OL_sizes.shard_bytes(d, tp)
     t_setup = time.perf_counter()
-    ctx = M.Ctx(device_ids=(dev,), budget=S_r + (2 << 20), max_batch=1, max_tokens=max(8, args.tokens),
-                writeback=args.writeback, swap_mode=args.swap_mode, chunk_bytes=args.chunk_mb << 20,
-                trace=1)
+    kw = dict(budget=(S_r + 4095) // 4096 * 4096, max_batch=1, max_tokens=max(8, args.tokens),
+              writeback=args.writeback, swap_mode=args.swap_mode, chunk_bytes=args.chunk_mb << 20, trace=1)
+    if world > 1:
+        from paper_2306_13835_b200.group import open_group_ctx
+        ctx = open_group_ctx(dev, **kw)
+    else:
+        ctx = M.Ctx(device_ids=(dev,), **kw)
     ids = [ctx.register_model(d) for _ in range(args.n_models)]
     t_reg = time.perf_counter() - t_setup
     for i, m in enumerate(ids):
         ctx.synth_fill(m, 1000 + i)
     t_fill = time.perf_counter() - t_setup - t_reg
-    reqs = round_robin_blocking(args.warmup + args.steps, seed=rank, token_len=args.tokens, vocab=d.vocab,
+    reqs = round_robin_blocking(args.warmup + args.steps, seed=0, token_len=args.tokens, vocab=d.vocab,
                                 models=tuple(range(args.n_models)))
     out = np.empty(d.vocab, np.float32)
 
@@ -203,10 +217,11 @@ def run_ours(args, rank, world):
         rid, _ = ctx.request(ids[r.model], r.tokens, out)
         return rid, ctx.wait_request(rid, 600)
 
-    for r in reqs[:args.warmup]:
-        one(r)
+    if rank == 0:
+        for r in reqs[:args.warmup]:
+            one(r)
     if world > 1:
-        torch.distributed.barrier()
+        dist.barrier()
     torch.cuda.synchronize()
     st0 = ctx.stats()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -215,36 +230,44 @@ def run_ours(args, rank, world):
         torch.cuda.synchronize()
         e0.record()
         w0 = time.perf_counter()
-        for r in reqs[args.warmup:]:
-            _, (ta, td) = one(r)
-            lat.append(td - ta)
+        if rank == 0:
+            for r in reqs[args.warmup:]:
+                _, (ta, td) = one(r)
+                lat.append(td - ta)
+        if world > 1:
+            dist.barrier()
         wall = time.perf_counter() - w0
         torch.cuda.synchronize()
         e1.record()
         torch.cuda.synchronize()
     st1 = ctx.stats()
     dev_s = e0.elapsed_time(e1) / 1e3
-    tpath = args.trace or "/tmp/mpsw_bench_trace.ndjson"
-    ctx.trace_dump(tpath)
-    loads = [json.loads(l) for l in open(tpath) if '"dec":"load"' in l]
-    timed_loads = loads[-args.steps:]
+    timed = [None]
+    if rank == 0:
+        tpath = args.trace or "/tmp/mpsw_bench_trace.ndjson"
+        ctx.trace_dump(tpath)
+        loads = [json.loads(l) for l in open(tpath) if '"dec":"load"' in l]
+        timed = [[ld["id"] for ld in loads[-args.steps:]]]
+    if world > 1:
+        dist.broadcast_object_list(timed, src=0)
     h2d_ms, swapin_lat = [], []
-    for ld in timed_loads:
-        _, _, ms = ctx.entry_gpu_ms(ld["id"])
-        ts, tdone = ctx.wait(ld["id"])
-        h2d_ms.append(max(ms))
+    for lid in timed[0]:
+        ts, tdone = ctx.wait(lid, 600)
+        _, _, ms = ctx.entry_gpu_ms(lid)
+        h2d_ms.append(ms[rank])
         swapin_lat.append(max(tdone) - ts)
+    if world > 1:
+        from paper_2306_13835_b200.group import max_over_ranks
+        tdev = "cuda" if dist.get_backend() == "nccl" else None
+        h2d_ms = max_over_ranks(h2d_ms, device=tdev)
+        dev_s = max_over_ranks([dev_s], device=tdev)[0]
+        dist.barrier()
     ctx.close()
-    n_bytes = S_r * tp * len(timed_loads)
-    value = n_bytes / (sum(h2d_ms) / 1e3) / 1e9
-    e2e = n_bytes / dev_s / 1e9
-    res = {
-        "value": value, "e2e": e2e, "dev_s": dev_s, "wall_s": wall, "h2d_ms": h2d_ms, "swapin_lat_s": swapin_lat,
-        "req_lat_s": lat, "launches": st1["kernel_launches"] - st0["kernel_launches"], "S_r": S_r,
+    return {
+        "h2d_ms": h2d_ms, "swapin_lat_s": swapin_lat, "req_lat_s": lat, "dev_s": dev_s, "wall_s": wall,
+        "launches": st1["kernel_launches"] - st0["kernel_launches"], "S_r": S_r, "tp": tp,
         "ce_peak": ce_peak, "clocks": clk.summary(), "setup": {"register_pin_s": t_reg, "synth_fill_s": t_fill},
-        "d": d, "loads": len(timed_loads),
     }
-    return res
 
 
 def main():
@@ -254,20 +277,21 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(bench_device())
+        dist.init_process_group(os.environ.get("MPSW_BENCH_BACKEND", "nccl"))
 
     from synth import opt_dims
     from oracle import layout as OL_sizes
     d = opt_dims(args.model)
-    S_r = OL_sizes.shard_bytes(d, 1)
-    config = {"workload": f"cfg3-t1: {args.n_models}x {args.model.upper()}-shaped bf16, TP=1 per GPU, budget 1 model/GPU, "
-                          f"round-robin blocking requests (every request swaps), L={args.tokens}, B=1",
-              "model": args.model, "n_models": args.n_models, "tp": 1, "shard_bytes": S_r,
+    S_r = OL_sizes.shard_bytes(d, world)
+    config = {"workload": f"cfg3-t{world}: {args.n_models}x {args.model.upper()}-shaped bf16, ONE TP={world} group "
+                          f"(one process per GPU), budget 1 model per GPU, round-robin blocking requests (every "
+                          f"request swaps), L={args.tokens}, B=1",
+              "model": args.model, "n_models": args.n_models, "tp": world, "shard_bytes_per_rank": S_r,
               "writeback": bool(args.writeback), "swap_mode": ["auto", "copy_engine", "zero_copy"][args.swap_mode],
               "chunk_mb": args.chunk_mb, "l2": "inputs larger than L2 (one >=25.7 GB shard per step); no flush needed",
-              "global_batch": world, "seq_len": args.tokens, "parallelism": f"{world} independent ranks (replicas)"}
-    metric = "model swap-in aggregate H2D GB/s (TP shard over PCIe Gen5), OPT-13B cfg3"
+              "global_batch": 1, "seq_len": args.tokens, "parallelism": f"tp{world}"}
+    metric = "model swap-in aggregate H2D GB/s (all TP ranks' shards over PCIe Gen5), OPT-13B cfg3"
 
     if args.impl == "reference":
         if rank != 0:
@@ -284,21 +308,14 @@ def main():
         return
 
     r = run_ours(args, rank, world)
-    vals = [r["value"], r["e2e"], max(r["h2d_ms"])]
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        t = torch.tensor([r["dev_s"], max(r["h2d_ms"])], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_s_max = float(t[0])
-    else:
-        dev_s_max = r["dev_s"]
     if rank != 0:
         return
     steps = len(r["h2d_ms"])
-    achieved = r["S_r"] / (statistics.median(r["h2d_ms"]) / 1e3) / 1e9
-    value = world * r["S_r"] * steps / (sum(r["h2d_ms"]) / 1e3) / 1e9
-    e2e = world * r["S_r"] * steps / dev_s_max / 1e9
+    tp = r["tp"]
+    achieved = tp * r["S_r"] / (statistics.median(r["h2d_ms"]) / 1e3) / 1e9
+    value = tp * r["S_r"] * steps / (sum(r["h2d_ms"]) / 1e3) / 1e9
+    e2e = tp * r["S_r"] * steps / r["dev_s"] / 1e9
+    dev_s_max = r["dev_s"]
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cb = run_cpu_baseline(d, r["S_r"], args.tokens, 5)
@@ -314,12 +331,12 @@ def main():
                                "device_h2d_p50": OM.nearest_rank(r["h2d_ms"], 50)},
         "request_latency_ms": {"p50": 1e3 * OM.nearest_rank(r["req_lat_s"], 50),
                                "p99": 1e3 * OM.nearest_rank(r["req_lat_s"], 99)},
-        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": r["S_r"] + 4 * args.tokens,
-                "d2h_bytes_per_step": (r["S_r"] if args.writeback else 0) + 4 * d.vocab},
-        "roofline": {"bound": "pcie", "achieved": achieved, "peak": PCIE_GEN5_X16_GBPS, "unit": "GB/s",
-                     "frac": achieved / PCIE_GEN5_X16_GBPS, "traffic": None,
+        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": tp * r["S_r"] + 4 * args.tokens * tp,
+                "d2h_bytes_per_step": (tp * r["S_r"] if args.writeback else 0) + 4 * d.vocab},
+        "roofline": {"bound": "pcie", "achieved": achieved, "peak": PCIE_GEN5_X16_GBPS * tp, "unit": "GB/s",
+                     "frac": achieved / (PCIE_GEN5_X16_GBPS * tp), "traffic": None,
                      "peak_source": "nominal PCIe Gen5 x16 per direction (north star); MEASURED_PEAKS.json has no PCIe entry",
-                     "measured_ce_peak_GBps": r["ce_peak"], "frac_of_measured_ce_peak": achieved / r["ce_peak"],
+                     "measured_ce_peak_GBps_per_gpu": r["ce_peak"], "frac_of_measured_ce_peak": achieved / (tp * r["ce_peak"]),
                      "kernel": "swap-in H2D (copy engine cudaMemcpyAsync chunks; not an SM kernel, so ncu dram traffic is n/a)"},
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],

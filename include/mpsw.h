@@ -14,6 +14,15 @@
  * Ranks map to CUDA devices through `device_ids`; repeated ids are allowed and give
  * "virtual ranks" that share one GPU (used to test TP > 1 semantics on a single B200).
  *
+ * Multi-process mode (one process per GPU, e.g. under torchrun): set world_size = t > 1,
+ * world_rank, shm_name and n_gpus = tp = 1 (this process's rank). Rank 0 is the LEADER: it runs
+ * the engine (the only place requests / explicit swaps are accepted) and publishes every
+ * decision to a POSIX shared-memory control plane (`shm_name`); ranks 1..t-1 are FOLLOWERS that
+ * execute the published entries on their GPU and post per-rank acks back through the same
+ * segment ("sends a response back to the engine"). The TP all-reduce of the forward reads
+ * peer partials through CUDA IPC mappings (NVLink). mpsw_init, the FIRST mpsw_register_model,
+ * every mpsw_register_model (same order on every rank) and mpsw_shutdown are collective.
+ *
  * Every call returns mpsw_status (0 = OK, < 0 = error) and never throws across the ABI.
  * On error, mpsw_last_error() returns a thread-local message describing the failure.
  * Pointers are plain host pointers unless stated otherwise; sizes are bytes.
@@ -49,9 +58,9 @@ enum { MPSW_EVICTED = 0, MPSW_LOADING = 1, MPSW_RESIDENT = 2, MPSW_OFFLOADING = 
 typedef struct mpsw_ctx mpsw_ctx;   /* opaque; owns arenas, slots, streams, threads */
 
 typedef struct {
-    int n_gpus;                   /* ranks in the TP group (t)                                  */
+    int n_gpus;                   /* ranks driven by THIS process (t, or 1 in multi-process)   */
     const int* device_ids;        /* n_gpus CUDA ordinals (caller-owned, read during init)     */
-    int tp;                       /* must equal n_gpus: one TP group per ctx; replicas = ctxs  */
+    int tp;                       /* TP degree t: == n_gpus (single-process) or == world_size  */
     uint64_t param_budget_bytes_per_gpu;  /* parameter slots per rank (the swapping budget)    */
     uint64_t workspace_bytes_per_gpu;     /* 0 = auto (activations, partials, logits staging)  */
     int max_batch;                /* requests per batch entry, 1..256 (P:168 uses 8, P:196 32) */
@@ -63,6 +72,9 @@ typedef struct {
     int writeback;                /* 1 = offload copies the slot back to the arena      */
     int trace;                    /* 1 = record the NDJSON event/decision trace                */
     int zc_ctas;                  /* CTAs of the zero-copy kernel; 0 => auto                   */
+    int world_size;               /* processes in the TP group; 0/1 = single-process mode      */
+    int world_rank;               /* this process's TP rank (0 = leader)                       */
+    const char* shm_name;         /* POSIX shm name for the control plane, e.g. "/mpsw_1234"   */
 } mpsw_config;
 
 typedef struct { int n_layers, hidden, heads, ffn, vocab, max_pos; } mpsw_opt_dims;
@@ -77,7 +89,8 @@ typedef struct {
 
 /* Create a ctx. Allocates each rank's parameter region (one cudaMalloc of the budget) and
  * workspace, creates streams and starts the engine and worker threads.
- * Errors: EINVAL (tp != n_gpus, bad sizes), ENOMEM (cudaMalloc), ECUDA. */
+ * Errors: EINVAL (tp inconsistent with n_gpus/world_size, bad sizes), ENOMEM (cudaMalloc),
+ * ECUDA, ETIMEDOUT (multi-process: peers did not join the shm control plane within 120 s). */
 mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out);
 
 /* Wait for all in-flight work, stop threads, free every arena, slot, stream. NULL is OK. */
@@ -110,6 +123,10 @@ mpsw_status mpsw_model_arena(mpsw_ctx* ctx, int model_id, int rank, void** host,
  * counter-based synthetic weights of DESIGN.md §Inputs (C0) for `model_seed`, using
  * `threads` host threads (0 = all). rank = -1 fills every rank. */
 mpsw_status mpsw_synth_fill(mpsw_ctx* ctx, int model_id, int rank, uint64_t model_seed, int threads);
+
+/* Multi-process mode: mpsw_request / mpsw_swap_in / mpsw_swap_out / mpsw_trace_dump are
+ * accepted on the leader only (EINVAL on followers); mpsw_checksum / mpsw_peek / mpsw_wait /
+ * mpsw_entry_gpu_ms / mpsw_residency act on the calling process's rank. */
 
 /* Explicit load entry: asynchronously copy every rank's shard into a free slot.
  * Goes through the engine queue, ordered with requests. *ticket identifies the entry.

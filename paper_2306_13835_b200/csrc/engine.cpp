@@ -1,29 +1,32 @@
 // mpsw runtime: pinned shard store, device slots, per-rank workers, the engine (scheduler)
-// thread and the C-ABI entry points.
+// thread, the multi-process control plane and the C-ABI entry points.
 //
 // Architecture (§3.1 Fig. 1, §3.2, §4):
-//   * one engine thread = the paper's centralised engine: per-model FIFO request queues with
-//     arrival timestamps, oldest-head batch scheduling, LRU replacement via
-//     load/offload entries, ack-based completion;
+//   * one engine thread = the paper's centralised engine (statemachine.h): per-model FIFO
+//     queues, oldest-head batching, LRU replacement via load/offload entries, ack completion;
 //   * one worker thread per rank = the paper's per-GPU worker: it receives every entry in the
-//     same global order ("evaluate batch entries in submitted order") and issues it on
-//     its own streams: compute, load (H2D) and offload (D2H). A worker never waits
-//     for a copy before moving on to the next entry (P:105 asynchronous load entries);
-//   * the engine polls per-rank completion events; an entry is complete when every rank has
-//     acked. Batches for a model are submitted only after its load completed on all
-//     ranks (load dependency).
-// Scheduling semantics are those of DESIGN.md §Scheduler (readings #1-#7, #21, #24, #26);
-// the independent numpy oracle (oracle/scheduler.py) replays this engine's trace.
+//     same global order ("evaluate batch entries in submitted order") and issues it on its
+//     own streams: compute, load (H2D) and offload (D2H). A worker never waits for a
+//     copy before moving on to the next entry (P:105 asynchronous load entries);
+//   * an entry completes when every rank has acked; batches for a model are
+//     submitted only after its load completed on all ranks (load dependency).
+// Deployment modes:
+//   * single process: one ctx drives all t ranks (threads), peers' partials read directly;
+//   * multi-process (one process per GPU): rank 0 = leader runs the engine and publishes
+//     decisions into a POSIX shm ring; followers execute them and post acks into the same
+//     segment; the fused TP all-reduce reads peer partials through CUDA IPC mappings.
 #include "internal.h"
+#include "statemachine.h"
 
+#include <fcntl.h>
 #include <immintrin.h>
 #include <sys/mman.h>
+#include <sys/stat.h>
 #include <sys/syscall.h>
 #include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
-#include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -56,8 +59,7 @@ int gpu_numa_node(int dev) {
     char bus[64] = {0};
     if (cudaDeviceGetPCIBusId(bus, sizeof(bus), dev) != cudaSuccess) return -1;
     for (char* c = bus; *c; ++c) *c = (char)tolower(*c);
-    std::string path = std::string("/sys/bus/pci/devices/") + bus + "/numa_node";
-    std::ifstream f(path);
+    std::ifstream f(std::string("/sys/bus/pci/devices/") + bus + "/numa_node");
     int node = -1;
     if (f) f >> node;
     return node;
@@ -75,7 +77,7 @@ struct PinnedBuf {
 PinnedBuf pin_alloc(uint64_t bytes, int numa_node) {
     PinnedBuf b;
     b.bytes = bytes;
-    b.map_bytes = (std::max<uint64_t>(bytes, 1) + kSlotAlign - 1) / kSlotAlign * kSlotAlign;
+    b.map_bytes = (std::max<uint64_t>(bytes, 1) + (2ull << 20) - 1) / (2ull << 20) * (2ull << 20);
     void* p = mmap(nullptr, b.map_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
     if (p == MAP_FAILED) throw Error(MPSW_ENOMEM, "mmap of pinned arena failed");
     madvise(p, b.map_bytes, MADV_HUGEPAGE);
@@ -85,6 +87,7 @@ PinnedBuf pin_alloc(uint64_t bytes, int numa_node) {
     }
     cudaError_t e = cudaHostRegister(p, b.map_bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
     if (e != cudaSuccess) {
+        cudaGetLastError();
         munmap(p, b.map_bytes);
         throw Error(MPSW_ENOMEM, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
     }
@@ -114,6 +117,11 @@ void parallel_memcpy(uint8_t* dst, const uint8_t* src, uint64_t n) {
     for (auto& x : th) x.join();
 }
 
+inline void spin_pause(int& spins) {
+    if (++spins < 2048) _mm_pause();
+    else std::this_thread::yield();
+}
+
 struct SpinBarrier {
     std::atomic<int> count{0};
     std::atomic<int> gen{0};
@@ -126,18 +134,61 @@ struct SpinBarrier {
             gen.fetch_add(1, std::memory_order_acq_rel);
         } else {
             int spins = 0;
-            while (gen.load(std::memory_order_acquire) == g) {
-                if (++spins < 4096) _mm_pause();
-                else std::this_thread::yield();
-            }
+            while (gen.load(std::memory_order_acquire) == g) spin_pause(spins);
         }
     }
 };
 
-// ----------------------------------------------------------------------------- engine state
-enum { E_LOAD = 0, E_OFFLOAD = 1, E_BATCH = 2 };
-enum { ST_EVICTED = 0, ST_LOADING = 1, ST_RESIDENT = 2, ST_OFFLOADING = 3 };
+// ----------------------------------------------------------------------------- shm control plane
+constexpr uint64_t kShmMagic = 0x314d485357534d50ull;  // "PMSWSHM1"
+constexpr uint64_t kLogCap = 1 << 16;
+constexpr uint64_t kAckCap = 1 << 16;
 
+struct ShmRec {            // one decision published by the leader
+    uint64_t id;
+    int32_t kind, model, slot, ring, B, M;
+};
+
+struct ShmCtl {
+    std::atomic<uint64_t> magic;
+    int32_t world;
+    std::atomic<int32_t> joined;
+    std::atomic<int32_t> stop;            // leader has shut down
+    std::atomic<int32_t> poisoned;
+    char poison_msg[256];
+    std::atomic<int32_t> bar_count, bar_gen;
+    std::atomic<int32_t> stg_ready;       // leader created the staging segment
+    uint64_t stg_bytes;
+    std::atomic<uint64_t> log_tail;       // records published
+    std::atomic<uint64_t> consumed[kMaxRanks];   // records taken by each follower
+    cudaIpcMemHandle_t ws_handle[kMaxRanks];
+    uint64_t partial_off[kMaxRanks][2];
+    cudaIpcEventHandle_t ev_handle[kMaxRanks][2];
+    ShmRec log[kLogCap];
+    std::atomic<uint64_t> ack[kAckCap][kMaxRanks];
+};
+
+void* shm_map(const std::string& name, size_t bytes, bool create) {
+    int fd = create ? shm_open(name.c_str(), O_CREAT | O_RDWR | O_TRUNC, 0600) : shm_open(name.c_str(), O_RDWR, 0600);
+    if (fd < 0) return nullptr;
+    if (create && ftruncate(fd, (off_t)bytes) != 0) {
+        close(fd);
+        throw Error(MPSW_ENOMEM, "ftruncate of shm segment failed");
+    }
+    if (!create) {
+        struct stat st;
+        if (fstat(fd, &st) != 0 || (size_t)st.st_size < bytes) {
+            close(fd);
+            return nullptr;
+        }
+    }
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) throw Error(MPSW_ENOMEM, "mmap of shm segment failed");
+    return p;
+}
+
+// ----------------------------------------------------------------------------- entries
 struct ReqRec {
     int64_t rid;
     int model;
@@ -150,11 +201,10 @@ struct ReqRec {
 struct Entry {
     uint64_t id = 0;
     int kind = 0, model = -1, slot = -1;
-    std::vector<std::shared_ptr<ReqRec>> reqs;
-    int ring = 0, M = 0;
+    std::vector<std::shared_ptr<ReqRec>> reqs;   // leader only
+    int ring = 0, B = 0, M = 0;
     double t_submit = 0;
-    // per rank
-    cudaEvent_t ev_start[kMaxRanks] = {};
+    cudaEvent_t ev_start[kMaxRanks] = {};        // indexed by GLOBAL rank; only local ranks set
     cudaEvent_t ev_done[kMaxRanks] = {};
     std::atomic<int> issued[kMaxRanks];
     int acked[kMaxRanks] = {};
@@ -167,190 +217,6 @@ struct Entry {
 };
 using EntryP = std::shared_ptr<Entry>;
 
-// Decision of the state machine (mirrors oracle/scheduler.py's dicts).
-struct Decision {
-    int kind;  // 0 load, 1 offload, 2 batch, 3 complete, 4 noop, 5 reject
-    uint64_t id = 0;
-    int model = -1, slot = -1;
-    std::vector<int64_t> rids;
-    const char* status = "";
-};
-
-// Deterministic engine state machine.
-struct StateMachine {
-    int n_models = 0, k = 0, tp = 1, max_batch = 1, D = 1;
-    std::vector<std::deque<std::pair<int64_t, double>>> queue;
-    std::vector<int> state, outstanding, slot_of;
-    std::vector<double> last_use;
-    std::vector<int> owner;  // slot -> model or -1
-    struct Pend { int kind, model, left; uint32_t mask; };
-    std::map<uint64_t, Pend> pending;
-    std::map<uint64_t, std::pair<int, std::vector<int64_t>>> batches;
-    int inflight = 0;
-    uint64_t next_id = 0;
-
-    void add_model() {
-        queue.emplace_back();
-        state.push_back(ST_EVICTED);
-        outstanding.push_back(0);
-        slot_of.push_back(-1);
-        last_use.push_back(-INFINITY);
-        ++n_models;
-    }
-    bool head_less(int a, int b) const {  // (head t_arr, reg order)
-        const double ta = queue[a].front().second, tb = queue[b].front().second;
-        return ta < tb || (ta == tb && a < b);
-    }
-    int free_slot() const {
-        for (int s = 0; s < k; ++s)
-            if (owner[s] < 0) return s;
-        return -1;
-    }
-    void load(int m, int s, std::vector<Decision>& out) {
-        Decision d{0, next_id++, m, s};
-        owner[s] = m;
-        slot_of[m] = s;
-        state[m] = ST_LOADING;
-        pending[d.id] = {E_LOAD, m, tp, 0u};
-        out.push_back(d);
-    }
-    int offload(int v, std::vector<Decision>& out) {
-        const int s = slot_of[v];
-        Decision d{1, next_id++, v, s};
-        owner[s] = -1;
-        slot_of[v] = -1;
-        state[v] = ST_OFFLOADING;
-        pending[d.id] = {E_OFFLOAD, v, tp, 0u};
-        out.push_back(d);
-        return s;
-    }
-    void schedule(double now, std::vector<Decision>& out) {
-        std::vector<char> blocked(n_models, 0);
-        for (;;) {
-            int m = -1;
-            for (int i = 0; i < n_models; ++i)
-                if (!queue[i].empty() && !blocked[i] && (m < 0 || head_less(i, m))) m = i;
-            if (m < 0) return;
-            const int st = state[m];
-            if (st == ST_RESIDENT) {
-                if (inflight < D) {
-                    const int n = std::min<int>(max_batch, (int)queue[m].size());
-                    Decision d{2, next_id++, m};
-                    for (int i = 0; i < n; ++i) {
-                        d.rids.push_back(queue[m].front().first);
-                        queue[m].pop_front();
-                    }
-                    batches[d.id] = {m, d.rids};
-                    last_use[m] = now;
-                    ++outstanding[m];
-                    ++inflight;
-                    out.push_back(std::move(d));
-                } else {
-                    blocked[m] = 1;
-                }
-            } else if (st == ST_LOADING || st == ST_OFFLOADING) {
-                blocked[m] = 1;
-            } else {
-                const int s = free_slot();
-                if (s >= 0) {
-                    load(m, s, out);
-                } else {
-                    int best = -1;
-                    auto key_less = [&](int a, int b) {  // prefer empty queue, then LRU, then reg order
-                        const int qa = queue[a].empty() ? 0 : 1, qb = queue[b].empty() ? 0 : 1;
-                        if (qa != qb) return qa < qb;
-                        if (last_use[a] != last_use[b]) return last_use[a] < last_use[b];
-                        return a < b;
-                    };
-                    for (int v = 0; v < n_models; ++v) {
-                        if (state[v] != ST_RESIDENT || outstanding[v] != 0) continue;
-                        if (!queue[v].empty() && !head_less(m, v)) continue;   // older head: not a victim
-                        if (best < 0 || key_less(v, best)) best = v;
-                    }
-                    if (best >= 0) {
-                        const int sv = offload(best, out);
-                        load(m, sv, out);
-                    }
-                }
-                blocked[m] = 1;
-            }
-        }
-    }
-    // events ------------------------------------------------------------------------------
-    void arrival(int64_t rid, int m, double t, std::vector<Decision>& out) {
-        queue[m].push_back({rid, t});
-        schedule(t, out);
-    }
-    void ack(uint64_t e, int rank, double t, std::vector<Decision>& out) {
-        auto it = pending.find(e);
-        if (it == pending.end()) throw Error(MPSW_EINVARIANT, "ack for unknown entry");
-        if (it->second.mask & (1u << rank)) throw Error(MPSW_EINVARIANT, "duplicate ack");
-        it->second.mask |= 1u << rank;
-        if (--it->second.left == 0) {
-            state[it->second.model] = it->second.kind == E_LOAD ? ST_RESIDENT : ST_EVICTED;
-            pending.erase(it);
-        }
-        schedule(t, out);
-    }
-    void batch_done(uint64_t b, double t, std::vector<Decision>& out) {
-        auto it = batches.find(b);
-        if (it == batches.end()) throw Error(MPSW_EINVARIANT, "unknown batch");
-        Decision d{3, b, it->second.first};
-        d.rids = it->second.second;
-        --outstanding[it->second.first];
-        --inflight;
-        batches.erase(it);
-        out.push_back(std::move(d));
-        schedule(t, out);
-    }
-    void cmd_swap_in(int m, double t, std::vector<Decision>& out) {
-        const int st = state[m];
-        if (st == ST_RESIDENT || st == ST_LOADING) {
-            out.push_back(Decision{4, 0, m});
-        } else if (st == ST_OFFLOADING) {
-            Decision d{5, 0, m};
-            d.status = "EBUSY";
-            out.push_back(d);
-        } else {
-            const int s = free_slot();
-            if (s < 0) {
-                Decision d{5, 0, m};
-                d.status = "ENOMEM";
-                out.push_back(d);
-            } else {
-                load(m, s, out);
-            }
-        }
-        schedule(t, out);
-    }
-    void cmd_swap_out(int m, double t, std::vector<Decision>& out) {
-        const int st = state[m];
-        if (st == ST_EVICTED || st == ST_OFFLOADING) {
-            out.push_back(Decision{4, 0, m});
-        } else if (st == ST_LOADING || outstanding[m] > 0) {
-            Decision d{5, 0, m};
-            d.status = "EBUSY";
-            out.push_back(d);
-        } else {
-            offload(m, out);
-        }
-        schedule(t, out);
-    }
-    void check() const {
-        int owned = 0;
-        for (int s = 0; s < k; ++s)
-            if (owner[s] >= 0) ++owned;
-        if (owned > k) throw Error(MPSW_EINVARIANT, "more owned slots than k");
-        for (int m = 0; m < n_models; ++m) {
-            if (outstanding[m] > 0 && state[m] != ST_RESIDENT)
-                throw Error(MPSW_EINVARIANT, "in-flight batch on a non-resident model");
-            if ((state[m] == ST_LOADING || state[m] == ST_RESIDENT) && owner[slot_of[m]] != m)
-                throw Error(MPSW_EINVARIANT, "slot ownership");
-        }
-        if (inflight > D) throw Error(MPSW_EINVARIANT, "D exceeded");
-    }
-};
-
 // ----------------------------------------------------------------------------- per-rank state
 struct Slot {
     uint8_t* base = nullptr;
@@ -361,18 +227,17 @@ struct Slot {
 };
 
 struct Rank {
-    int index = 0, device = 0, numa = -1;
+    int index = 0, local = 0, device = 0, numa = -1;   // index = global TP rank
     cudaStream_t compute = nullptr, h2d = nullptr, d2h = nullptr, aux = nullptr;
     uint8_t* region = nullptr;             // param budget (one cudaMalloc)
     std::vector<Slot> slots;
     uint8_t* ws_base = nullptr;
     FwdWorkspace ws;
     std::vector<TensorPtrs> wptr;          // per slot
-    cudaEvent_t ev_point[2] = {nullptr, nullptr};
+    cudaEvent_t ev_point[2] = {nullptr, nullptr};   // partial-ready events (interprocess in mp mode)
     std::vector<cudaEvent_t> last_compute; // per model
     std::vector<char> last_compute_valid;
     unsigned long long* d_sum = nullptr;
-    // worker
     std::thread th;
     std::mutex mu;
     std::condition_variable cv;
@@ -381,7 +246,7 @@ struct Rank {
 
 struct Model {
     mpsw_opt_dims dims;
-    std::vector<PinnedBuf> arena;  // per rank
+    std::vector<PinnedBuf> arena;  // per LOCAL rank
 };
 
 struct Cmd {
@@ -399,8 +264,12 @@ struct mpsw_ctx {
     std::vector<int> device_ids;
     std::chrono::steady_clock::time_point t0;
     int tp = 1, D = 1;
+    bool mp = false;           // multi-process mode
+    bool leader = true;        // runs the engine (single-process mode: always)
+    int world_rank = 0;
     uint64_t chunk = 64ull << 20;
-    std::vector<std::unique_ptr<mpsw::Rank>> ranks;
+    std::vector<std::unique_ptr<mpsw::Rank>> ranks;     // LOCAL ranks
+    int local_of[mpsw::kMaxRanks];                        // global rank -> local index or -1
     std::vector<std::unique_ptr<mpsw::Model>> models;
     // geometry (fixed by the first registered model; homogeneous slots)
     bool geom = false;
@@ -410,10 +279,20 @@ struct mpsw_ctx {
     int k = 0, n_chunks = 0;
     mpsw::FwdShape fshape{};
     int max_rows = 0;
-    // logits / tokens staging ring (pinned), D + 1 entries
+    // TP peers (global rank -> partial buffers / partial-ready events)
+    float* peer_partial[mpsw::kMaxRanks][2] = {};
+    cudaEvent_t peer_ev[mpsw::kMaxRanks][2] = {};
+    std::vector<void*> ipc_mem_opened;
+    std::vector<cudaEvent_t> ipc_ev_opened;
+    // logits / tokens staging ring (pinned; shm in mp mode), D + 1 entries
     int ring_n = 2;
-    mpsw::PinnedBuf staging;
+    uint8_t* stg = nullptr;
+    mpsw::PinnedBuf stg_local;
+    size_t stg_map_bytes = 0;
     size_t ring_stride = 0, ring_tok_off = 0;
+    // multi-process control plane
+    std::string shm_name;
+    mpsw::ShmCtl* ctl = nullptr;
     // engine
     mpsw::StateMachine sm;
     std::mutex cmd_mu;
@@ -431,12 +310,16 @@ struct mpsw_ctx {
     std::atomic<int64_t> next_rid{0};
     int ring_next = 0;
     mpsw::SpinBarrier barrier;
-    std::mutex api_mu;  // serialises register / swap / request submission
+    std::mutex api_mu;
+    // follower-local view of residency (mp followers)
+    std::vector<int> f_slot_of;
+    std::vector<int> f_state;
+    std::mutex f_mu;
     // trace + stats
     bool trace = false;
     std::mutex trace_mu;
     std::vector<std::string> trace_lines;
-    std::mutex sm_mu;   // guards sm against readers (residency/checksum) and registration
+    std::mutex sm_mu;
     std::unordered_map<int64_t, std::shared_ptr<mpsw::ReqRec>> eng_reqs;   // engine-private
     std::atomic<uint64_t> launches{0}, h2d_bytes{0}, d2h_bytes{0}, swaps_in{0}, swaps_out{0}, n_batches{0},
         n_requests{0}, rejected{0};
@@ -453,26 +336,58 @@ std::string fmt_d(double v) {
 
 void poison(mpsw_ctx* c, const std::string& msg) {
     if (!c->poisoned.exchange(1)) c->poison_msg = msg;
-    std::fprintf(stderr, "[mpsw] ctx poisoned: %s\n", msg.c_str());
+    std::fprintf(stderr, "[mpsw] ctx poisoned (rank %d): %s\n", c->world_rank, msg.c_str());
+    if (c->ctl && !c->ctl->poisoned.exchange(1))
+        std::snprintf(c->ctl->poison_msg, sizeof(c->ctl->poison_msg), "rank %d: %s", c->world_rank, msg.c_str());
     c->done_cv.notify_all();
+}
+
+bool group_poisoned(mpsw_ctx* c) { return c->poisoned.load() || (c->ctl && c->ctl->poisoned.load()); }
+
+// Barrier of the t rank threads of a TP group (threads of one process, or one thread in each of
+// t processes through the shm segment). Bounded so a dead peer cannot hang the process forever.
+void group_barrier(mpsw_ctx* c) {
+    if (!c->mp) {
+        c->barrier.wait();
+        return;
+    }
+    ShmCtl* s = c->ctl;
+    const int g = s->bar_gen.load(std::memory_order_acquire);
+    if (s->bar_count.fetch_add(1, std::memory_order_acq_rel) + 1 == c->tp) {
+        s->bar_count.store(0, std::memory_order_relaxed);
+        s->bar_gen.fetch_add(1, std::memory_order_acq_rel);
+        return;
+    }
+    int spins = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    while (s->bar_gen.load(std::memory_order_acquire) == g) {
+        spin_pause(spins);
+        if ((spins & 4095) == 0) {
+            if (s->poisoned.load()) throw Error(MPSW_ECUDA, std::string("peer poisoned: ") + s->poison_msg);
+            if (now_s(t0) > 600) throw Error(MPSW_ETIMEDOUT, "group barrier timed out (peer process gone?)");
+        }
+    }
 }
 
 bool use_zero_copy(mpsw_ctx* c, uint64_t bytes) {
     if (c->cfg.swap_mode == MPSW_SWAP_ZERO_COPY) return true;
     if (c->cfg.swap_mode == MPSW_SWAP_COPY_ENGINE) return false;
-    return bytes <= (4ull << 20);   // AUTO: small shards skip DMA setup (measured crossover: bench cfg5)
+    return bytes <= (4ull << 20);   // AUTO: small shards skip DMA setup (measured crossover: DESIGN.md §8)
 }
 
 int zc_ctas(mpsw_ctx* c) { return c->cfg.zc_ctas > 0 ? c->cfg.zc_ctas : 32; }
 
+uint8_t* arena_of(mpsw_ctx* c, int model, const Rank& R) { return c->models[model]->arena[R.local].p; }
+
 // ----------------------------------------------------------------------------- worker issue
 void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
     Slot& sl = R.slots[e.slot];
-    const uint8_t* src = c->models[e.model]->arena[R.index].p;
+    const uint8_t* src = arena_of(c, e.model, R);
     const bool zc = use_zero_copy(c, c->S);
-    MPSW_CU(cudaEventCreate(&e.ev_start[R.index]));
-    MPSW_CU(cudaEventCreate(&e.ev_done[R.index]));
-    MPSW_CU(cudaEventRecord(e.ev_start[R.index], R.h2d));
+    const int r = R.index;
+    MPSW_CU(cudaEventCreate(&e.ev_start[r]));
+    MPSW_CU(cudaEventCreate(&e.ev_done[r]));
+    MPSW_CU(cudaEventRecord(e.ev_start[r], R.h2d));
     if (sl.whole_gate_valid) MPSW_CU(cudaStreamWaitEvent(R.h2d, sl.whole_gate, 0));
     if (!sl.chunk_gate_valid && zc) {
         launch_zero_copy(sl.base, src, c->S, zc_ctas(c), R.h2d);
@@ -491,19 +406,20 @@ void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
     }
     sl.chunk_gate_valid = false;
     sl.whole_gate_valid = false;
-    MPSW_CU(cudaEventRecord(e.ev_done[R.index], R.h2d));
+    MPSW_CU(cudaEventRecord(e.ev_done[r], R.h2d));
 }
 
 void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
     Slot& sl = R.slots[e.slot];
-    uint8_t* dst = c->models[e.model]->arena[R.index].p;
+    uint8_t* dst = arena_of(c, e.model, R);
     const bool zc = use_zero_copy(c, c->S);
-    MPSW_CU(cudaEventCreate(&e.ev_start[R.index]));
-    MPSW_CU(cudaEventCreate(&e.ev_done[R.index]));
+    const int r = R.index;
+    MPSW_CU(cudaEventCreate(&e.ev_start[r]));
+    MPSW_CU(cudaEventCreate(&e.ev_done[r]));
     // eviction never races an in-flight request: the D2H stream waits for the last forward
     // that read the victim (the engine also only evicts models with no in-flight batch)
     if (R.last_compute_valid[e.model]) MPSW_CU(cudaStreamWaitEvent(R.d2h, R.last_compute[e.model], 0));
-    MPSW_CU(cudaEventRecord(e.ev_start[R.index], R.d2h));
+    MPSW_CU(cudaEventRecord(e.ev_start[r], R.d2h));
     if (c->cfg.writeback) {
         for (int i = 0; i < c->n_chunks; ++i) {
             const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, c->S - off);
@@ -520,55 +436,55 @@ void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
         MPSW_CU(cudaEventRecord(sl.whole_gate, R.d2h));
         sl.whole_gate_valid = true;
     }
-    MPSW_CU(cudaEventRecord(e.ev_done[R.index], R.d2h));
+    MPSW_CU(cudaEventRecord(e.ev_done[r], R.d2h));
 }
 
 void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
     const FwdShape& s = c->fshape;
     FwdShape sr = s;
     sr.rank = R.index;
-    const int B = (int)e.reqs.size(), M = e.M;
+    const int B = e.B, M = e.M;
     const TensorPtrs& Wt = R.wptr[e.slot];
     cudaStream_t cs = R.compute;
     const int r = R.index, t = c->tp;
     MPSW_CU(cudaEventCreateWithFlags(&e.ev_done[r], cudaEventDisableTiming));
     // tokens + meta (packed by the engine into the pinned ring entry)
-    uint8_t* ring = c->staging.p + (size_t)e.ring * c->ring_stride;
+    uint8_t* ring = c->stg + (size_t)e.ring * c->ring_stride;
     const size_t meta_n = (size_t)(3 * B + 1 + M);
     MPSW_CU(cudaMemcpyAsync(R.ws.tokens, ring + c->ring_tok_off, (size_t)M * 4, cudaMemcpyHostToDevice, cs));
     MPSW_CU(cudaMemcpyAsync(R.ws.meta, ring + c->ring_tok_off + (size_t)c->max_rows * 4, meta_n * 4,
                             cudaMemcpyHostToDevice, cs));
     const int32_t* pos = R.ws.meta + 2 * B + 1;
     int nl = 0, point = 0;
-    // all-reduce point: record my partial, barrier with the other rank threads, then wait for
-    // every peer's partial on my stream and run the fused reduce+residual+bias+LN kernel.
-    auto allreduce_ln = [&](float* mine, const float* residual, const void* bias, const void* pos_table,
-                            const void* g, const void* b) {
+    // all-reduce point: record my partial, barrier with the other ranks of the group, wait for
+    // every peer's partial on my stream, then the fused reduce + bias + residual + LN kernel
+    // reads all t partials directly (peer / IPC mappings over NVLink).
+    auto allreduce_ln = [&](const float* residual, const void* bias, const void* pos_table, const void* g,
+                            const void* b) {
         const int pb = point & 1;
         const float* peers[kMaxRanks];
         if (t > 1) {
             MPSW_CU(cudaEventRecord(R.ev_point[pb], cs));
-            c->barrier.wait();
+            group_barrier(c);
             for (int p = 0; p < t; ++p)
-                if (p != r) MPSW_CU(cudaStreamWaitEvent(cs, c->ranks[p]->ev_point[pb], 0));
+                if (p != r) MPSW_CU(cudaStreamWaitEvent(cs, c->peer_ev[p][pb], 0));
         }
-        for (int p = 0; p < t; ++p) peers[p] = c->ranks[p]->ws.partial[pb];
-        (void)mine;
+        for (int p = 0; p < t; ++p) peers[p] = c->peer_partial[p][pb];
         nl += fwd_reduce_ln(sr, M, peers, t, residual, bias, pos_table, pos, g, b, R.ws.x, R.ws.a, cs);
         ++point;
     };
     nl += fwd_embed(sr, Wt, R.ws, M, R.ws.partial[point & 1], cs);
-    allreduce_ln(R.ws.partial[point & 1], nullptr, nullptr, Wt.embed_pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b);
+    allreduce_ln(nullptr, nullptr, Wt.embed_pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b);
     for (int l = 0; l < s.n_layers; ++l) {
         const auto& L = Wt.layers[l];
         nl += fwd_qkv(sr, L, R.ws, M, cs);
         nl += fwd_attention(sr, R.ws, B, cs);
         nl += fwd_out_proj(sr, L, R.ws, M, R.ws.partial[point & 1], cs);
-        allreduce_ln(R.ws.partial[point & 1], R.ws.x, L.o_b, nullptr, L.ln2_w, L.ln2_b);
+        allreduce_ln(R.ws.x, L.o_b, nullptr, L.ln2_w, L.ln2_b);
         nl += fwd_fc1(sr, L, R.ws, M, cs);
         nl += fwd_fc2(sr, L, R.ws, M, R.ws.partial[point & 1], cs);
         const bool last = l + 1 == s.n_layers;
-        allreduce_ln(R.ws.partial[point & 1], R.ws.x, L.fc2_b, nullptr, last ? Wt.lnf_w : Wt.layers[l + 1].ln1_w,
+        allreduce_ln(R.ws.x, L.fc2_b, nullptr, last ? Wt.lnf_w : Wt.layers[l + 1].ln1_w,
                      last ? Wt.lnf_b : Wt.layers[l + 1].ln1_b);
     }
     nl += fwd_lm_head(sr, Wt, R.ws, B, cs);
@@ -593,13 +509,11 @@ void worker_main(mpsw_ctx* c, Rank* R) {
             R->fifo.pop_front();
         }
         try {
-            if (!c->poisoned.load()) {
+            if (!group_poisoned(c)) {
                 if (e->kind == E_LOAD) issue_load(c, *R, *e);
                 else if (e->kind == E_OFFLOAD) issue_offload(c, *R, *e);
                 else issue_batch(c, *R, *e);
             }
-        } catch (const Error& err) {
-            poison(c, err.what());
         } catch (const std::exception& err) {
             poison(c, err.what());
         }
@@ -608,7 +522,15 @@ void worker_main(mpsw_ctx* c, Rank* R) {
     }
 }
 
-// ----------------------------------------------------------------------------- engine thread
+void push_to_workers(mpsw_ctx* c, const EntryP& e) {
+    for (auto& R : c->ranks) {
+        std::lock_guard<std::mutex> lk(R->mu);
+        R->fifo.push_back(e);
+        R->cv.notify_one();
+    }
+}
+
+// ----------------------------------------------------------------------------- engine (leader)
 void log_event(mpsw_ctx* c, const std::string& s) {
     if (!c->trace) return;
     std::lock_guard<std::mutex> lk(c->trace_mu);
@@ -639,6 +561,24 @@ void log_decisions(mpsw_ctx* c, const std::vector<Decision>& ds) {
     }
 }
 
+void publish(mpsw_ctx* c, const Entry& e) {
+    ShmCtl* s = c->ctl;
+    const uint64_t tail = s->log_tail.load(std::memory_order_relaxed);
+    // never overwrite a record a follower has not taken yet
+    int spins = 0;
+    for (int p = 1; p < c->tp; ++p)
+        while (tail - s->consumed[p].load(std::memory_order_acquire) >= kLogCap) spin_pause(spins);
+    ShmRec& rec = s->log[tail % kLogCap];
+    rec.id = e.id;
+    rec.kind = e.kind;
+    rec.model = e.model;
+    rec.slot = e.slot;
+    rec.ring = e.ring;
+    rec.B = e.B;
+    rec.M = e.M;
+    s->log_tail.store(tail + 1, std::memory_order_release);
+}
+
 void dispatch(mpsw_ctx* c, const std::vector<Decision>& ds, double now) {
     for (const auto& d : ds) {
         if (d.kind > 2) continue;
@@ -650,10 +590,10 @@ void dispatch(mpsw_ctx* c, const std::vector<Decision>& ds, double now) {
         e->t_submit = now;
         if (d.kind == E_BATCH) {
             e->slot = c->sm.slot_of[d.model];
-            // pack tokens + meta into the pinned ring entry
+            // pack tokens + meta into the pinned ring entry (shm in mp mode: every rank reads it)
             e->ring = c->ring_next;
             c->ring_next = (c->ring_next + 1) % c->ring_n;
-            uint8_t* ring = c->staging.p + (size_t)e->ring * c->ring_stride;
+            uint8_t* ring = c->stg + (size_t)e->ring * c->ring_stride;
             int32_t* tok = (int32_t*)(ring + c->ring_tok_off);
             int32_t* meta = tok + c->max_rows;
             const int B = (int)d.rids.size();
@@ -670,17 +610,15 @@ void dispatch(mpsw_ctx* c, const std::vector<Decision>& ds, double now) {
                 meta[B + 1 + b] = M - 1;                    // last row of request b (lm_head)
             }
             meta[B] = M;
+            e->B = B;
             e->M = M;
         } else {
             std::lock_guard<std::mutex> lk(c->done_mu);
             c->entries[e->id] = e;
         }
+        if (c->mp) publish(c, *e);
         c->inflight.push_back(e);
-        for (auto& R : c->ranks) {
-            std::lock_guard<std::mutex> lk(R->mu);
-            R->fifo.push_back(e);
-            R->cv.notify_one();
-        }
+        push_to_workers(c, e);
     }
 }
 
@@ -694,7 +632,7 @@ void step_and_dispatch(mpsw_ctx* c, const std::function<void(std::vector<Decisio
 }
 
 void complete_batch(mpsw_ctx* c, Entry& e, double now) {
-    const uint8_t* ring = c->staging.p + (size_t)e.ring * c->ring_stride;
+    const uint8_t* ring = c->stg + (size_t)e.ring * c->ring_stride;
     const int V = c->fshape.vocab;
     for (size_t b = 0; b < e.reqs.size(); ++b) {
         auto& rq = e.reqs[b];
@@ -711,16 +649,27 @@ void complete_batch(mpsw_ctx* c, Entry& e, double now) {
     c->done_cv.notify_all();
 }
 
+// 1 = rank r finished entry e, 0 = not yet. Local ranks: their CUDA event; remote ranks (mp):
+// the ack slot the follower wrote into the shm segment.
+int rank_done(mpsw_ctx* c, Entry& e, int r) {
+    if (c->local_of[r] >= 0) {
+        if (!e.issued[r].load(std::memory_order_acquire)) return 0;
+        if (!e.ev_done[r]) return 1;   // poisoned before issue
+        const cudaError_t q = cudaEventQuery(e.ev_done[r]);
+        if (q == cudaErrorNotReady) return 0;
+        if (q != cudaSuccess) throw Error(MPSW_ECUDA, std::string("copy/forward failed: ") + cudaGetErrorString(q));
+        return 1;
+    }
+    return c->ctl->ack[e.id % kAckCap][r].load(std::memory_order_acquire) == e.id + 1 ? 1 : 0;
+}
+
 bool poll_inflight(mpsw_ctx* c) {
     bool progressed = false;
     for (size_t i = 0; i < c->inflight.size();) {
         Entry& e = *c->inflight[i];
         bool finished = false;
         for (int r = 0; r < c->tp; ++r) {
-            if (e.acked[r] || !e.issued[r].load(std::memory_order_acquire)) continue;
-            cudaError_t q = e.ev_done[r] ? cudaEventQuery(e.ev_done[r]) : cudaSuccess;
-            if (q == cudaErrorNotReady) continue;
-            if (q != cudaSuccess) throw Error(MPSW_ECUDA, std::string("copy/forward failed: ") + cudaGetErrorString(q));
+            if (e.acked[r] || !rank_done(c, e, r)) continue;
             const double now = now_s(c->t0);
             e.acked[r] = 1;
             e.t_ack[r] = now;
@@ -772,7 +721,7 @@ void engine_main(mpsw_ctx* c) {
         }
         try {
             for (auto& cmd : batch) {
-                if (c->poisoned.load()) {
+                if (group_poisoned(c)) {
                     if (cmd.reply) cmd.reply->set_value({MPSW_ECUDA, 0});
                     continue;
                 }
@@ -781,8 +730,8 @@ void engine_main(mpsw_ctx* c) {
                     c->eng_reqs[rq->rid] = rq;
                     log_event(c, "{\"ev\":\"arrival\",\"t\":" + fmt_d(rq->t_arr) + ",\"rid\":" + std::to_string(rq->rid) +
                                      ",\"model\":" + std::to_string(rq->model) + "}");
-                    const double now = rq->t_arr;
-                    step_and_dispatch(c, [&](std::vector<Decision>& ds) { c->sm.arrival(rq->rid, rq->model, now, ds); },
+                    const double t = rq->t_arr;
+                    step_and_dispatch(c, [&](std::vector<Decision>& ds) { c->sm.arrival(rq->rid, rq->model, t, ds); },
                                       now_s(c->t0));
                 } else {
                     const double now = now_s(c->t0);
@@ -809,12 +758,96 @@ void engine_main(mpsw_ctx* c) {
                 if (prog) idle_spins = 0;
                 else if (++idle_spins > 64) std::this_thread::yield();
                 else _mm_pause();
+                if (c->ctl && c->ctl->poisoned.load() && !c->poisoned.load())
+                    poison(c, std::string("peer: ") + c->ctl->poison_msg);
             }
         } catch (const std::exception& err) {
             poison(c, err.what());
             for (auto& cmd : batch)
                 if (cmd.reply) try { cmd.reply->set_value({MPSW_EINVARIANT, 0}); } catch (...) {}
             c->inflight.clear();
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------- follower (mp)
+// Takes the leader's published entries in order, hands them to the local worker, and posts
+// this rank's acks (swap copy or batch forward finished on this GPU) into the shm segment.
+void follower_main(mpsw_ctx* c) {
+    Rank& R = *c->ranks[0];
+    cudaSetDevice(R.device);
+    ShmCtl* s = c->ctl;
+    uint64_t cur = 0;
+    int spins = 0;
+    while (true) {
+        bool progressed = false;
+        const uint64_t tail = s->log_tail.load(std::memory_order_acquire);
+        while (cur < tail) {
+            const ShmRec rec = s->log[cur % kLogCap];
+            ++cur;
+            s->consumed[c->world_rank].store(cur, std::memory_order_release);
+            auto e = std::make_shared<Entry>();
+            e->id = rec.id;
+            e->kind = rec.kind;
+            e->model = rec.model;
+            e->slot = rec.slot;
+            e->ring = rec.ring;
+            e->B = rec.B;
+            e->M = rec.M;
+            e->t_submit = now_s(c->t0);
+            if (e->kind != E_BATCH) {
+                std::lock_guard<std::mutex> lk(c->done_mu);
+                c->entries[e->id] = e;
+            }
+            {
+                std::lock_guard<std::mutex> lk(c->f_mu);
+                if (e->kind == E_LOAD) { c->f_slot_of[e->model] = e->slot; c->f_state[e->model] = ST_LOADING; }
+                if (e->kind == E_OFFLOAD) { c->f_slot_of[e->model] = -1; c->f_state[e->model] = ST_OFFLOADING; }
+            }
+            c->inflight.push_back(e);
+            push_to_workers(c, e);
+            progressed = true;
+        }
+        try {
+            const int r = R.index;
+            for (size_t i = 0; i < c->inflight.size();) {
+                Entry& e = *c->inflight[i];
+                if (!rank_done(c, e, r)) { ++i; continue; }
+                e.acked[r] = 1;
+                e.t_ack[r] = now_s(c->t0);
+                e.n_acked = 1;
+                s->ack[e.id % kAckCap][r].store(e.id + 1, std::memory_order_release);
+                {
+                    std::lock_guard<std::mutex> lk(c->f_mu);
+                    if (e.kind == E_LOAD && c->f_slot_of[e.model] == e.slot) c->f_state[e.model] = ST_RESIDENT;
+                    if (e.kind == E_OFFLOAD && c->f_state[e.model] == ST_OFFLOADING) c->f_state[e.model] = ST_EVICTED;
+                }
+                if (e.kind == E_BATCH) {
+                    if (e.ev_done[r]) cudaEventDestroy(e.ev_done[r]), e.ev_done[r] = nullptr;
+                    c->n_batches++;
+                } else {
+                    (e.kind == E_LOAD ? c->swaps_in : c->swaps_out)++;
+                    if (e.kind == E_LOAD) c->h2d_bytes += c->S;
+                    else if (c->cfg.writeback) c->d2h_bytes += c->S;
+                    std::lock_guard<std::mutex> lk(c->done_mu);
+                    e.complete.store(1, std::memory_order_release);
+                }
+                c->done_cv.notify_all();
+                c->inflight.erase(c->inflight.begin() + i);
+                progressed = true;
+            }
+        } catch (const std::exception& err) {
+            poison(c, err.what());
+            c->inflight.clear();
+        }
+        if (c->inflight.empty() && cur == s->log_tail.load(std::memory_order_acquire) &&
+            (s->stop.load(std::memory_order_acquire) || (c->stop.load() && group_poisoned(c))))
+            break;
+        if (progressed) spins = 0;
+        else if (c->inflight.empty()) {
+            if (++spins > 4096) std::this_thread::sleep_for(std::chrono::microseconds(50));
+        } else {
+            spin_pause(spins);
         }
     }
 }
@@ -839,7 +872,8 @@ TensorPtrs make_ptrs(const Layout& L, const uint8_t* base, int n_layers) {
 }
 
 // Fix the slot geometry at the first registration: k = floor(budget / S_r) slots per rank
-// carved from the region allocated at init; workspaces sized for max_batch * max_tokens rows.
+// carved from the region allocated at init; workspaces sized for max_batch * max_tokens rows;
+// TP peers wired (collective in multi-process mode: IPC handles exchanged through shm).
 void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& d) {
     Layout L;
     if (compute_layout(d, c->tp, 0, c->cfg.dtype, L) != MPSW_OK) throw Error(MPSW_EINVAL, tls_error());
@@ -864,6 +898,7 @@ void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& d) {
     f.dtype = c->cfg.dtype;
     c->max_rows = c->cfg.max_batch * c->cfg.max_tokens;
     const size_t wsb = workspace_bytes(f, c->max_rows, c->cfg.max_batch);
+    const unsigned ev_flags = c->mp ? (cudaEventInterprocess | cudaEventDisableTiming) : cudaEventDisableTiming;
     for (auto& Rp : c->ranks) {
         Rank& R = *Rp;
         MPSW_CU(cudaSetDevice(R.device));
@@ -879,14 +914,60 @@ void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& d) {
         MPSW_CU(cudaMalloc(&R.ws_base, wsb));
         MPSW_CU(cudaMemset(R.ws_base, 0, wsb));
         workspace_carve(R.ws, f, c->max_rows, c->cfg.max_batch, R.ws_base);
-        for (auto& ev : R.ev_point) MPSW_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        for (auto& ev : R.ev_point) MPSW_CU(cudaEventCreateWithFlags(&ev, ev_flags));
+        for (int pb = 0; pb < 2; ++pb) {
+            c->peer_partial[R.index][pb] = R.ws.partial[pb];
+            c->peer_ev[R.index][pb] = R.ev_point[pb];
+        }
     }
     // staging ring: per entry [max_batch * V] fp32 logits, then tokens [max_rows] + meta
     c->ring_n = c->D + 1;
     const size_t logits_b = ((size_t)c->cfg.max_batch * d.vocab * 4 + 255) & ~size_t(255);
     c->ring_tok_off = logits_b;
     c->ring_stride = (logits_b + (size_t)(c->max_rows * 2 + 3 * c->cfg.max_batch + 8) * 4 + 4095) & ~size_t(4095);
-    c->staging = pin_alloc(c->ring_stride * c->ring_n, c->ranks[0]->numa);
+    const size_t stg_bytes = c->ring_stride * c->ring_n;
+    if (!c->mp) {
+        c->stg_local = pin_alloc(stg_bytes, c->ranks[0]->numa);
+        c->stg = c->stg_local.p;
+    } else {
+        ShmCtl* s = c->ctl;
+        Rank& R = *c->ranks[0];
+        MPSW_CU(cudaSetDevice(R.device));
+        MPSW_CU(cudaIpcGetMemHandle(&s->ws_handle[R.index], R.ws_base));
+        for (int pb = 0; pb < 2; ++pb) {
+            s->partial_off[R.index][pb] = (uint64_t)((uint8_t*)R.ws.partial[pb] - R.ws_base);
+            MPSW_CU(cudaIpcGetEventHandle(&s->ev_handle[R.index][pb], R.ev_point[pb]));
+        }
+        const std::string stg_name = c->shm_name + "_stg";
+        if (c->leader) {
+            c->stg = (uint8_t*)shm_map(stg_name, stg_bytes, true);
+            s->stg_bytes = stg_bytes;
+            s->stg_ready.store(1, std::memory_order_release);
+        }
+        group_barrier(c);   // every rank published its handles; staging segment exists
+        if (!c->leader) {
+            if (s->stg_bytes != stg_bytes) throw Error(MPSW_EINVAL, "ranks disagree on the staging geometry");
+            c->stg = (uint8_t*)shm_map(stg_name, stg_bytes, false);
+            if (!c->stg) throw Error(MPSW_EINVAL, "cannot open the staging segment");
+        }
+        c->stg_map_bytes = stg_bytes;
+        MPSW_CU(cudaHostRegister(c->stg, stg_bytes, cudaHostRegisterPortable));
+        for (int p = 0; p < c->tp; ++p) {
+            if (p == R.index) continue;
+            void* base = nullptr;
+            MPSW_CU(cudaIpcOpenMemHandle(&base, s->ws_handle[p], cudaIpcMemLazyEnablePeerAccess));
+            c->ipc_mem_opened.push_back(base);
+            for (int pb = 0; pb < 2; ++pb) {
+                c->peer_partial[p][pb] = (float*)((uint8_t*)base + s->partial_off[p][pb]);
+                cudaEvent_t ev;
+                MPSW_CU(cudaIpcOpenEventHandle(&ev, s->ev_handle[p][pb]));
+                c->ipc_ev_opened.push_back(ev);
+                c->peer_ev[p][pb] = ev;
+            }
+        }
+        group_barrier(c);
+        if (c->leader) shm_unlink(stg_name.c_str());   // mapped everywhere; name no longer needed
+    }
     {
         std::lock_guard<std::mutex> lk(c->sm_mu);
         c->sm.k = k;
@@ -905,6 +986,16 @@ using namespace mpsw;
     }                                                                         \
     catch (const Error& e) { return set_error(e.status, e.what()); }         \
     catch (const std::exception& e) { return set_error(MPSW_EINVAL, e.what()); }
+
+static mpsw_status need_leader(mpsw_ctx* c) {
+    if (!c->leader) return set_error(MPSW_EINVAL, "multi-process mode: submit on rank 0 (the engine)");
+    return MPSW_OK;
+}
+
+static int local_index(mpsw_ctx* c, int rank) {
+    if (rank < 0 || rank >= c->tp) return -1;
+    return c->local_of[rank];
+}
 
 extern "C" {
 
@@ -928,38 +1019,58 @@ mpsw_status mpsw_shard_layout(const mpsw_opt_dims* dims, int tp, int rank, int d
 mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     API_BEGIN
     if (!cfg || !out) return set_error(MPSW_EINVAL, "NULL argument");
+    const bool mp = cfg->world_size > 1;
     if (cfg->n_gpus < 1 || cfg->n_gpus > kMaxRanks || !cfg->device_ids)
         return set_error(MPSW_EINVAL, "n_gpus must be 1..8 with device_ids");
-    if (cfg->tp != cfg->n_gpus) return set_error(MPSW_EINVAL, "tp must equal n_gpus (one TP group per ctx)");
+    if (mp) {
+        if (cfg->world_size > kMaxRanks) return set_error(MPSW_EINVAL, "world_size must be <= 8");
+        if (cfg->n_gpus != 1 || cfg->tp != cfg->world_size)
+            return set_error(MPSW_EINVAL, "multi-process mode: n_gpus = 1 and tp = world_size");
+        if (cfg->world_rank < 0 || cfg->world_rank >= cfg->world_size) return set_error(MPSW_EINVAL, "bad world_rank");
+        if (!cfg->shm_name || cfg->shm_name[0] != '/') return set_error(MPSW_EINVAL, "shm_name must start with '/'");
+    } else if (cfg->tp != cfg->n_gpus) {
+        return set_error(MPSW_EINVAL, "tp must equal n_gpus (one TP group per ctx)");
+    }
     if (cfg->max_batch < 1 || cfg->max_batch > 256) return set_error(MPSW_EINVAL, "max_batch must be 1..256");
     if (cfg->max_tokens < 1 || cfg->max_tokens > 128) return set_error(MPSW_EINVAL, "max_tokens must be 1..128");
     if (cfg->dtype != MPSW_BF16 && cfg->dtype != MPSW_FP32) return set_error(MPSW_EINVAL, "bad dtype");
     if (cfg->chunk_bytes % 4096) return set_error(MPSW_EINVAL, "chunk_bytes must be a multiple of 4096");
     if (cfg->swap_mode < 0 || cfg->swap_mode > 2) return set_error(MPSW_EINVAL, "bad swap_mode");
+    if (cfg->param_budget_bytes_per_gpu == 0) return set_error(MPSW_EINVAL, "param budget is 0");
     int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return set_error(MPSW_ECUDA, "no CUDA device");
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+        cudaGetLastError();
+        return set_error(MPSW_ECUDA, "no CUDA device");
+    }
     auto c = std::make_unique<mpsw_ctx>();
     c->cfg = *cfg;
+    c->cfg.shm_name = nullptr;
     c->t0 = std::chrono::steady_clock::now();
+    c->mp = mp;
+    c->world_rank = mp ? cfg->world_rank : 0;
+    c->leader = !mp || cfg->world_rank == 0;
     c->tp = cfg->tp;
     c->D = cfg->max_inflight_batches > 0 ? cfg->max_inflight_batches : 1;
     c->chunk = cfg->chunk_bytes ? cfg->chunk_bytes : (64ull << 20);
-    c->trace = cfg->trace != 0;
+    c->trace = cfg->trace != 0 && c->leader;
     c->device_ids.assign(cfg->device_ids, cfg->device_ids + cfg->n_gpus);
     c->sm.tp = c->tp;
     c->sm.max_batch = cfg->max_batch;
     c->sm.D = c->D;
-    c->barrier.n = c->tp;
+    c->barrier.n = mp ? 1 : c->tp;
     c->models.reserve(kMaxModels);
-    for (int r = 0; r < c->tp; ++r) {
-        const int dev = c->device_ids[r];
+    for (auto& x : c->local_of) x = -1;
+    for (int l = 0; l < cfg->n_gpus; ++l) {
+        const int dev = c->device_ids[l];
         if (dev < 0 || dev >= ndev) return set_error(MPSW_EINVAL, "device id out of range");
         auto R = std::make_unique<Rank>();
-        R->index = r;
+        R->index = mp ? cfg->world_rank : l;
+        R->local = l;
         R->device = dev;
         R->numa = gpu_numa_node(dev);
         R->last_compute.reserve(kMaxModels);
         R->last_compute_valid.reserve(kMaxModels);
+        c->local_of[R->index] = l;
         MPSW_CU(cudaSetDevice(dev));
         int hp = 0, lp = 0;
         MPSW_CU(cudaDeviceGetStreamPriorityRange(&lp, &hp));
@@ -967,7 +1078,6 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
         MPSW_CU(cudaStreamCreateWithFlags(&R->h2d, cudaStreamNonBlocking));
         MPSW_CU(cudaStreamCreateWithFlags(&R->d2h, cudaStreamNonBlocking));
         MPSW_CU(cudaStreamCreateWithFlags(&R->aux, cudaStreamNonBlocking));
-        if (cfg->param_budget_bytes_per_gpu == 0) return set_error(MPSW_EINVAL, "param budget is 0");
         cudaError_t e = cudaMalloc(&R->region, cfg->param_budget_bytes_per_gpu);
         if (e != cudaSuccess) {
             cudaGetLastError();
@@ -976,22 +1086,52 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
         MPSW_CU(cudaMalloc(&R->d_sum, sizeof(unsigned long long)));
         c->ranks.push_back(std::move(R));
     }
-    // peer access between distinct devices of the group (TP all-reduce reads peer partials)
-    for (int a = 0; a < c->tp; ++a)
-        for (int b = 0; b < c->tp; ++b) {
-            const int da = c->device_ids[a], db = c->device_ids[b];
-            if (da == db) continue;
-            int ok = 0;
-            cudaDeviceCanAccessPeer(&ok, da, db);
-            if (!ok) return set_error(MPSW_EINVAL, "GPUs of the TP group lack peer access");
-            cudaSetDevice(da);
-            cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
-            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) MPSW_CU(e);
-            cudaGetLastError();
+    if (!mp) {
+        // peer access between distinct devices of the group (TP all-reduce reads peer partials)
+        for (int a = 0; a < c->tp; ++a)
+            for (int b = 0; b < c->tp; ++b) {
+                const int da = c->device_ids[a], db = c->device_ids[b];
+                if (da == db) continue;
+                int ok = 0;
+                cudaDeviceCanAccessPeer(&ok, da, db);
+                if (!ok) return set_error(MPSW_EINVAL, "GPUs of the TP group lack peer access");
+                cudaSetDevice(da);
+                cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) MPSW_CU(e);
+                cudaGetLastError();
+            }
+    } else {
+        // shm control plane: the leader creates and initialises it; followers attach.
+        c->shm_name = cfg->shm_name;
+        ShmCtl* s = nullptr;
+        if (c->leader) {
+            s = (ShmCtl*)shm_map(c->shm_name, sizeof(ShmCtl), true);
+            if (!s) return set_error(MPSW_EINVAL, "cannot create shm segment " + c->shm_name);
+            std::memset((void*)s, 0, sizeof(ShmCtl));
+            s->world = c->tp;
+            s->magic.store(kShmMagic, std::memory_order_release);
+        } else {
+            const auto t0 = std::chrono::steady_clock::now();
+            while (true) {
+                s = (ShmCtl*)shm_map(c->shm_name, sizeof(ShmCtl), false);
+                if (s && s->magic.load(std::memory_order_acquire) == kShmMagic) break;
+                if (s) munmap((void*)s, sizeof(ShmCtl)), s = nullptr;
+                if (now_s(t0) > 120) return set_error(MPSW_ETIMEDOUT, "leader never created " + c->shm_name);
+                std::this_thread::sleep_for(std::chrono::milliseconds(20));
+            }
+            if (s->world != c->tp) return set_error(MPSW_EINVAL, "world_size differs from the leader's");
         }
+        c->ctl = s;
+        s->joined.fetch_add(1);
+        const auto t0 = std::chrono::steady_clock::now();
+        while (s->joined.load() < c->tp) {
+            if (now_s(t0) > 120) return set_error(MPSW_ETIMEDOUT, "peers did not join the control plane");
+            std::this_thread::sleep_for(std::chrono::milliseconds(5));
+        }
+    }
     mpsw_ctx* raw = c.release();
     for (auto& R : raw->ranks) R->th = std::thread(worker_main, raw, R.get());
-    raw->engine = std::thread(engine_main, raw);
+    raw->engine = std::thread(raw->leader ? engine_main : follower_main, raw);
     *out = raw;
     return MPSW_OK;
     API_END
@@ -999,22 +1139,32 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
 
 mpsw_status mpsw_shutdown(mpsw_ctx* c) {
     if (!c) return MPSW_OK;
+    if (c->mp && !c->leader) {
+        // a follower serves the leader's entries until the leader shuts down
+        const auto t0 = std::chrono::steady_clock::now();
+        while (!c->ctl->stop.load() && !group_poisoned(c) && now_s(t0) < 3600)
+            std::this_thread::sleep_for(std::chrono::milliseconds(2));
+    }
     {
         std::lock_guard<std::mutex> lk(c->cmd_mu);
         c->stop.store(true);
     }
     c->cmd_cv.notify_all();
     if (c->engine.joinable()) c->engine.join();
+    if (c->mp && c->leader) c->ctl->stop.store(1, std::memory_order_release);
     for (auto& R : c->ranks) {
-        {
-            std::lock_guard<std::mutex> lk(R->mu);
-        }
+        { std::lock_guard<std::mutex> lk(R->mu); }
         R->cv.notify_all();
         if (R->th.joinable()) R->th.join();
     }
     for (auto& R : c->ranks) {
         cudaSetDevice(R->device);
         cudaDeviceSynchronize();
+    }
+    for (auto p : c->ipc_mem_opened) cudaIpcCloseMemHandle(p);
+    for (auto ev : c->ipc_ev_opened) cudaEventDestroy(ev);
+    for (auto& R : c->ranks) {
+        cudaSetDevice(R->device);
         for (auto& sl : R->slots) {
             for (auto ev : sl.chunk_gate) cudaEventDestroy(ev);
             if (sl.whole_gate) cudaEventDestroy(sl.whole_gate);
@@ -1038,7 +1188,17 @@ mpsw_status mpsw_shutdown(mpsw_ctx* c) {
         }
     for (auto& m : c->models)
         for (auto& a : m->arena) pin_free(a);
-    pin_free(c->staging);
+    pin_free(c->stg_local);
+    if (c->mp) {
+        if (c->stg) {
+            cudaHostUnregister(c->stg);
+            munmap(c->stg, c->stg_map_bytes);
+        }
+        if (c->ctl) {
+            munmap((void*)c->ctl, sizeof(ShmCtl));
+            if (c->leader) shm_unlink(c->shm_name.c_str());
+        }
+    }
     delete c;
     return MPSW_OK;
 }
@@ -1047,28 +1207,28 @@ mpsw_status mpsw_register_model(mpsw_ctx* c, const mpsw_opt_dims* dims, int tp, 
                                 const uint64_t* shard_bytes, int* model_id) {
     API_BEGIN
     if (!c || !dims || !model_id) return set_error(MPSW_EINVAL, "NULL argument");
-    if (c->poisoned.load()) return set_error(MPSW_ECUDA, "ctx poisoned: " + c->poison_msg);
+    if (group_poisoned(c)) return set_error(MPSW_ECUDA, "ctx poisoned: " + c->poison_msg);
     if (tp != c->tp) return set_error(MPSW_EINVAL, "model tp must equal the ctx tp");
     std::lock_guard<std::mutex> api(c->api_mu);
     Layout L;
     mpsw_status s = compute_layout(*dims, tp, 0, c->cfg.dtype, L);
     if (s != MPSW_OK) return s;
     {
-        // the engine thread reads geometry; registration happens while it may be running
         std::lock_guard<std::mutex> lk(c->cmd_mu);
         if (!c->geom) setup_geometry(c, *dims);
         else if (std::memcmp(&c->dims, dims, sizeof(*dims)) != 0)
             return set_error(MPSW_EINVAL, "all models of a ctx must share dims (homogeneous slots, P:229)");
     }
     if (shards && shard_bytes)
-        for (int r = 0; r < tp; ++r)
-            if (shard_bytes[r] != c->S) return set_error(MPSW_EINVAL, "shard_bytes != S_r of the layout");
+        for (auto& R : c->ranks)
+            if (shards[R->index] && shard_bytes[R->index] != c->S)
+                return set_error(MPSW_EINVAL, "shard_bytes != S_r of the layout");
     auto m = std::make_unique<Model>();
     m->dims = *dims;
     try {
-        for (int r = 0; r < tp; ++r) {
-            m->arena.push_back(pin_alloc(c->S, c->ranks[r]->numa));
-            if (shards && shards[r]) parallel_memcpy(m->arena[r].p, (const uint8_t*)shards[r], c->S);
+        for (auto& R : c->ranks) {
+            m->arena.push_back(pin_alloc(c->S, R->numa));
+            if (shards && shards[R->index]) parallel_memcpy(m->arena.back().p, (const uint8_t*)shards[R->index], c->S);
         }
     } catch (...) {
         for (auto& a : m->arena) pin_free(a);
@@ -1078,18 +1238,19 @@ mpsw_status mpsw_register_model(mpsw_ctx* c, const mpsw_opt_dims* dims, int tp, 
         cudaSetDevice(R->device);
         cudaEvent_t ev;
         MPSW_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        // worker threads read last_compute[model] only for registered models; resize under the
-        // cmd lock so the engine never dispatches for a model whose vectors are not ready
         std::lock_guard<std::mutex> lk(R->mu);
-        R->last_compute.push_back(ev);
+        R->last_compute.push_back(ev);     // capacity reserved at init: no reallocation
         R->last_compute_valid.push_back(0);
     }
     {
         std::lock_guard<std::mutex> lk(c->cmd_mu);
         std::lock_guard<std::mutex> lk2(c->sm_mu);
+        std::lock_guard<std::mutex> lk3(c->f_mu);
         if (c->models.size() >= kMaxModels) return set_error(MPSW_ENOMEM, "too many models");
         c->models.push_back(std::move(m));   // capacity reserved at init: no reallocation
         c->sm.add_model();
+        c->f_slot_of.push_back(-1);
+        c->f_state.push_back(ST_EVICTED);
         *model_id = (int)c->models.size() - 1;
     }
     return MPSW_OK;
@@ -1100,8 +1261,9 @@ mpsw_status mpsw_model_arena(mpsw_ctx* c, int model_id, int rank, void** host, u
     API_BEGIN
     if (!c) return set_error(MPSW_EINVAL, "NULL ctx");
     if (model_id < 0 || model_id >= (int)c->models.size()) return set_error(MPSW_ENOENT, "unknown model");
-    if (rank < 0 || rank >= c->tp) return set_error(MPSW_EINVAL, "rank out of range");
-    if (host) *host = c->models[model_id]->arena[rank].p;
+    const int li = local_index(c, rank);
+    if (li < 0) return set_error(MPSW_EINVAL, "rank out of range or not driven by this process");
+    if (host) *host = c->models[model_id]->arena[li].p;
     if (bytes) *bytes = c->S;
     return MPSW_OK;
     API_END
@@ -1111,17 +1273,18 @@ mpsw_status mpsw_synth_fill(mpsw_ctx* c, int model_id, int rank, uint64_t seed, 
     API_BEGIN
     if (!c) return set_error(MPSW_EINVAL, "NULL ctx");
     if (model_id < 0 || model_id >= (int)c->models.size()) return set_error(MPSW_ENOENT, "unknown model");
-    if (rank < -1 || rank >= c->tp) return set_error(MPSW_EINVAL, "rank out of range");
-    for (int r = 0; r < c->tp; ++r)
-        if (rank < 0 || rank == r)
-            synth_fill_arena(c->dims, c->tp, r, c->cfg.dtype, seed, c->models[model_id]->arena[r].p, threads);
+    if (rank != -1 && local_index(c, rank) < 0) return set_error(MPSW_EINVAL, "rank out of range or not local");
+    for (auto& R : c->ranks)
+        if (rank < 0 || rank == R->index)
+            synth_fill_arena(c->dims, c->tp, R->index, c->cfg.dtype, seed, c->models[model_id]->arena[R->local].p, threads);
     return MPSW_OK;
     API_END
 }
 
 static mpsw_status submit_cmd(mpsw_ctx* c, int kind, int model_id, uint64_t* ticket) {
     if (!c) return set_error(MPSW_EINVAL, "NULL ctx");
-    if (c->poisoned.load()) return set_error(MPSW_ECUDA, "ctx poisoned: " + c->poison_msg);
+    if (need_leader(c) != MPSW_OK) return MPSW_EINVAL;
+    if (group_poisoned(c)) return set_error(MPSW_ECUDA, "ctx poisoned: " + c->poison_msg);
     if (model_id < 0 || model_id >= (int)c->models.size()) return set_error(MPSW_ENOENT, "unknown model");
     std::promise<std::pair<mpsw_status, uint64_t>> pr;
     auto fut = pr.get_future();
@@ -1159,14 +1322,20 @@ mpsw_status mpsw_wait(mpsw_ctx* c, uint64_t ticket, double timeout_s, double* t_
         return MPSW_OK;
     }
     EntryP e;
-    {
-        std::lock_guard<std::mutex> lk(c->done_mu);
-        auto it = c->entries.find(ticket);
-        if (it == c->entries.end()) return set_error(MPSW_ENOENT, "unknown ticket");
-        e = it->second;
+    const auto t0 = std::chrono::steady_clock::now();
+    while (true) {   // a follower may see the ticket shortly after the leader published it
+        {
+            std::lock_guard<std::mutex> lk(c->done_mu);
+            auto it = c->entries.find(ticket);
+            if (it != c->entries.end()) e = it->second;
+        }
+        if (e || c->leader) break;
+        if (timeout_s >= 0 && now_s(t0) > timeout_s) return set_error(MPSW_ETIMEDOUT, "ticket not seen yet");
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
     }
+    if (!e) return set_error(MPSW_ENOENT, "unknown ticket");
     std::unique_lock<std::mutex> lk(c->done_mu);
-    auto pred = [&] { return e->complete.load() || c->poisoned.load(); };
+    auto pred = [&] { return e->complete.load() || group_poisoned(c); };
     if (timeout_s < 0) c->done_cv.wait(lk, pred);
     else if (!c->done_cv.wait_for(lk, std::chrono::duration<double>(timeout_s), pred))
         return set_error(MPSW_ETIMEDOUT, "swap not complete");
@@ -1194,8 +1363,9 @@ mpsw_status mpsw_entry_gpu_ms(mpsw_ctx* c, uint64_t ticket, int* kind, int* mode
     if (gpu_ms)
         for (int r = 0; r < c->tp; ++r) {
             float ms = 0;
-            MPSW_CU(cudaEventElapsedTime(&ms, e->ev_start[r], e->ev_done[r]));
-            gpu_ms[r] = ms;
+            if (c->local_of[r] >= 0 && e->ev_start[r] && e->ev_done[r])
+                MPSW_CU(cudaEventElapsedTime(&ms, e->ev_start[r], e->ev_done[r]));
+            gpu_ms[r] = ms;   // 0 for ranks driven by other processes
         }
     return MPSW_OK;
     API_END
@@ -1205,7 +1375,8 @@ mpsw_status mpsw_request(mpsw_ctx* c, int model_id, const int32_t* tokens, int n
                          int64_t* request_id) {
     API_BEGIN
     if (!c || !logits_out || !request_id || !tokens) return set_error(MPSW_EINVAL, "NULL argument");
-    if (c->poisoned.load()) return set_error(MPSW_ECUDA, "ctx poisoned: " + c->poison_msg);
+    if (need_leader(c) != MPSW_OK) return MPSW_EINVAL;
+    if (group_poisoned(c)) return set_error(MPSW_ECUDA, "ctx poisoned: " + c->poison_msg);
     if (model_id < 0 || model_id >= (int)c->models.size()) {
         c->rejected++;
         return set_error(MPSW_ENOENT, "unknown model");
@@ -1243,7 +1414,7 @@ mpsw_status mpsw_poll(mpsw_ctx* c, int64_t rid, double* t_arrival, double* t_don
     auto rq = find_req(c, rid);
     if (!rq) return set_error(MPSW_ENOENT, "unknown request");
     if (!rq->done.load(std::memory_order_acquire)) {
-        if (c->poisoned.load()) return set_error(MPSW_ECUDA, "ctx poisoned: " + c->poison_msg);
+        if (group_poisoned(c)) return set_error(MPSW_ECUDA, "ctx poisoned: " + c->poison_msg);
         return set_error(MPSW_EAGAIN, "pending");
     }
     if (t_arrival) *t_arrival = rq->t_arr;
@@ -1258,7 +1429,7 @@ mpsw_status mpsw_wait_request(mpsw_ctx* c, int64_t rid, double timeout_s, double
     auto rq = find_req(c, rid);
     if (!rq) return set_error(MPSW_ENOENT, "unknown request");
     std::unique_lock<std::mutex> lk(c->done_mu);
-    auto pred = [&] { return rq->done.load() || c->poisoned.load(); };
+    auto pred = [&] { return rq->done.load() || group_poisoned(c); };
     if (timeout_s < 0) c->done_cv.wait(lk, pred);
     else if (!c->done_cv.wait_for(lk, std::chrono::duration<double>(timeout_s), pred))
         return set_error(MPSW_ETIMEDOUT, "request not complete");
@@ -1269,12 +1440,27 @@ mpsw_status mpsw_wait_request(mpsw_ctx* c, int64_t rid, double timeout_s, double
     API_END
 }
 
+// Slot of a model that is resident as seen by this process (-1 otherwise).
+static int resident_slot(mpsw_ctx* c, int model_id) {
+    if (c->leader) {
+        std::lock_guard<std::mutex> lk(c->sm_mu);
+        return c->sm.state[model_id] == ST_RESIDENT ? c->sm.slot_of[model_id] : -1;
+    }
+    std::lock_guard<std::mutex> lk(c->f_mu);
+    return c->f_state[model_id] == ST_RESIDENT ? c->f_slot_of[model_id] : -1;
+}
+
 mpsw_status mpsw_residency(mpsw_ctx* c, int model_id, int* state) {
     API_BEGIN
     if (!c || !state) return set_error(MPSW_EINVAL, "NULL argument");
-    std::lock_guard<std::mutex> lk(c->sm_mu);
-    if (model_id < 0 || model_id >= c->sm.n_models) return set_error(MPSW_ENOENT, "unknown model");
-    *state = c->sm.state[model_id];
+    if (model_id < 0 || model_id >= (int)c->models.size()) return set_error(MPSW_ENOENT, "unknown model");
+    if (c->leader) {
+        std::lock_guard<std::mutex> lk(c->sm_mu);
+        *state = c->sm.state[model_id];
+    } else {
+        std::lock_guard<std::mutex> lk(c->f_mu);
+        *state = c->f_state[model_id];
+    }
     return MPSW_OK;
     API_END
 }
@@ -1283,18 +1469,15 @@ mpsw_status mpsw_checksum(mpsw_ctx* c, int model_id, int rank, int on_device, ui
     API_BEGIN
     if (!c || !out) return set_error(MPSW_EINVAL, "NULL argument");
     if (model_id < 0 || model_id >= (int)c->models.size()) return set_error(MPSW_ENOENT, "unknown model");
-    if (rank < 0 || rank >= c->tp) return set_error(MPSW_EINVAL, "rank out of range");
+    const int li = local_index(c, rank);
+    if (li < 0) return set_error(MPSW_EINVAL, "rank out of range or not driven by this process");
     if (!on_device) {
-        *out = host_checksum(c->models[model_id]->arena[rank].p, c->S, 0);
+        *out = host_checksum(c->models[model_id]->arena[li].p, c->S, 0);
         return MPSW_OK;
     }
-    int slot = -1;
-    {
-        std::lock_guard<std::mutex> lk(c->sm_mu);
-        if (c->sm.state[model_id] != ST_RESIDENT) return set_error(MPSW_EINVAL, "model not RESIDENT");
-        slot = c->sm.slot_of[model_id];
-    }
-    Rank& R = *c->ranks[rank];
+    const int slot = resident_slot(c, model_id);
+    if (slot < 0) return set_error(MPSW_EINVAL, "model not RESIDENT");
+    Rank& R = *c->ranks[li];
     MPSW_CU(cudaSetDevice(R.device));
     MPSW_CU(cudaMemsetAsync(R.d_sum, 0, 8, R.aux));
     launch_checksum(R.slots[slot].base, c->S, R.d_sum, R.aux);
@@ -1311,14 +1494,11 @@ mpsw_status mpsw_peek(mpsw_ctx* c, int model_id, int rank, uint64_t offset, uint
     API_BEGIN
     if (!c || !dst) return set_error(MPSW_EINVAL, "NULL argument");
     if (model_id < 0 || model_id >= (int)c->models.size()) return set_error(MPSW_ENOENT, "unknown model");
-    if (rank < 0 || rank >= c->tp || offset + bytes > c->S) return set_error(MPSW_EINVAL, "range");
-    int slot = -1;
-    {
-        std::lock_guard<std::mutex> lk(c->sm_mu);
-        if (c->sm.state[model_id] != ST_RESIDENT) return set_error(MPSW_EINVAL, "model not RESIDENT");
-        slot = c->sm.slot_of[model_id];
-    }
-    Rank& R = *c->ranks[rank];
+    const int li = local_index(c, rank);
+    if (li < 0 || offset + bytes > c->S) return set_error(MPSW_EINVAL, "rank or range");
+    const int slot = resident_slot(c, model_id);
+    if (slot < 0) return set_error(MPSW_EINVAL, "model not RESIDENT");
+    Rank& R = *c->ranks[li];
     MPSW_CU(cudaSetDevice(R.device));
     MPSW_CU(cudaMemcpyAsync(dst, R.slots[slot].base + offset, bytes, cudaMemcpyDeviceToHost, R.aux));
     MPSW_CU(cudaStreamSynchronize(R.aux));
@@ -1329,6 +1509,7 @@ mpsw_status mpsw_peek(mpsw_ctx* c, int model_id, int rank, uint64_t offset, uint
 mpsw_status mpsw_trace_dump(mpsw_ctx* c, const char* path) {
     API_BEGIN
     if (!c || !path) return set_error(MPSW_EINVAL, "NULL argument");
+    if (need_leader(c) != MPSW_OK) return MPSW_EINVAL;
     if (!c->trace) return set_error(MPSW_EINVAL, "trace disabled (cfg.trace = 0)");
     std::lock_guard<std::mutex> lk(c->trace_mu);
     std::ofstream f(path);

@@ -30,7 +30,8 @@ class Config(C.Structure):
                 ("param_budget_bytes_per_gpu", C.c_uint64), ("workspace_bytes_per_gpu", C.c_uint64),
                 ("max_batch", C.c_int), ("max_tokens", C.c_int), ("dtype", C.c_int),
                 ("max_inflight_batches", C.c_int), ("swap_mode", C.c_int), ("chunk_bytes", C.c_uint64),
-                ("writeback", C.c_int), ("trace", C.c_int), ("zc_ctas", C.c_int)]
+                ("writeback", C.c_int), ("trace", C.c_int), ("zc_ctas", C.c_int),
+                ("world_size", C.c_int), ("world_rank", C.c_int), ("shm_name", C.c_char_p)]
 
 
 class OptDims(C.Structure):
@@ -118,11 +119,18 @@ class Ctx:
     """One TP group (see include/mpsw.h). Methods mirror the C-ABI names."""
 
     def __init__(self, device_ids=(0,), budget=1 << 30, max_batch=8, max_tokens=8, dtype=BF16,
-                 max_inflight=1, swap_mode=SWAP_AUTO, chunk_bytes=0, writeback=1, trace=0, zc_ctas=0):
+                 max_inflight=1, swap_mode=SWAP_AUTO, chunk_bytes=0, writeback=1, trace=0, zc_ctas=0,
+                 world_size=1, world_rank=0, shm_name=None):
+        """Single-process: one ctx over len(device_ids) ranks. Multi-process (world_size > 1):
+        device_ids = (this process's GPU,), rank world_rank of a TP group of world_size."""
         self._ids = (C.c_int * len(device_ids))(*device_ids)
-        self.tp = len(device_ids)
-        cfg = Config(len(device_ids), self._ids, len(device_ids), budget, 0, max_batch, max_tokens, dtype,
-                     max_inflight, swap_mode, chunk_bytes, writeback, trace, zc_ctas)
+        self.world_size, self.world_rank = world_size, world_rank
+        self.tp = world_size if world_size > 1 else len(device_ids)
+        self.local_ranks = [world_rank] if world_size > 1 else list(range(len(device_ids)))
+        self._shm = shm_name.encode() if shm_name else None
+        cfg = Config(len(device_ids), self._ids, self.tp, budget, 0, max_batch, max_tokens, dtype,
+                     max_inflight, swap_mode, chunk_bytes, writeback, trace, zc_ctas, world_size, world_rank,
+                     self._shm)
         h = _P()
         _check(lib().mpsw_init(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -141,14 +149,15 @@ class Ctx:
         self.close()
 
     def register_model(self, dims, shards=None):
+        """shards: list of tp per-rank blobs (entries of non-local ranks may be None)."""
         od = dims_of(dims)
         mid = C.c_int()
         if shards is None:
             _check(lib().mpsw_register_model(self.h, C.byref(od), self.tp, None, None, C.byref(mid)))
         else:
-            arrs = [np.ascontiguousarray(s) for s in shards]
-            ptrs = (_P * self.tp)(*[a.ctypes.data for a in arrs])
-            sizes = (C.c_uint64 * self.tp)(*[a.nbytes for a in arrs])
+            arrs = [None if s is None else np.ascontiguousarray(s) for s in shards]
+            ptrs = (_P * self.tp)(*[None if a is None else a.ctypes.data for a in arrs])
+            sizes = (C.c_uint64 * self.tp)(*[0 if a is None else a.nbytes for a in arrs])
             _check(lib().mpsw_register_model(self.h, C.byref(od), self.tp, ptrs, sizes, C.byref(mid)))
         self.vocab = dims.vocab
         return mid.value
@@ -174,6 +183,7 @@ class Ctx:
         return t.value
 
     def wait(self, ticket, timeout=-1.0):
+        """(t_submit, [t_ack per rank]); on a follower only its own rank's entry is meaningful."""
         ts = C.c_double()
         td = (C.c_double * self.tp)()
         _check(lib().mpsw_wait(self.h, ticket, timeout, C.byref(ts), td))
