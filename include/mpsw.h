@@ -75,6 +75,7 @@ typedef struct {
     int world_size;               /* processes in the TP group; 0/1 = single-process mode      */
     int world_rank;               /* this process's TP rank (0 = leader)                       */
     const char* shm_name;         /* POSIX shm name for the control plane, e.g. "/mpsw_1234"   */
+    int gemm_impl;                /* 0 auto (tcgen05/TMA for bf16, M <= 256), 1 SIMT, 2 tcgen05 */
 } mpsw_config;
 
 typedef struct { int n_layers, hidden, heads, ffn, vocab, max_pos; } mpsw_opt_dims;

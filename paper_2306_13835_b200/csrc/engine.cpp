@@ -450,7 +450,7 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
     MPSW_CU(cudaEventCreateWithFlags(&e.ev_done[r], cudaEventDisableTiming));
     // tokens + meta (packed by the engine into the pinned ring entry)
     uint8_t* ring = c->stg + (size_t)e.ring * c->ring_stride;
-    const size_t meta_n = (size_t)(3 * B + 1 + M);
+    const size_t meta_n = (size_t)(3 * B + 1 + 2 * M);
     MPSW_CU(cudaMemcpyAsync(R.ws.tokens, ring + c->ring_tok_off, (size_t)M * 4, cudaMemcpyHostToDevice, cs));
     MPSW_CU(cudaMemcpyAsync(R.ws.meta, ring + c->ring_tok_off + (size_t)c->max_rows * 4, meta_n * 4,
                             cudaMemcpyHostToDevice, cs));
@@ -487,7 +487,7 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
         allreduce_ln(R.ws.x, L.fc2_b, nullptr, last ? Wt.lnf_w : Wt.layers[l + 1].ln1_w,
                      last ? Wt.lnf_b : Wt.layers[l + 1].ln1_b);
     }
-    nl += fwd_lm_head(sr, Wt, R.ws, B, cs);
+    nl += fwd_lm_head(sr, Wt, R.ws, B, M, cs);
     float* logits_host = (float*)(ring) + (size_t)r * s.vocab_local;
     MPSW_CU(cudaMemcpy2DAsync(logits_host, (size_t)s.vocab * 4, R.ws.logits, (size_t)s.vocab_local * 4,
                               (size_t)s.vocab_local * 4, B, cudaMemcpyDeviceToHost, cs));
@@ -610,6 +610,9 @@ void dispatch(mpsw_ctx* c, const std::vector<Decision>& ds, double now) {
                 meta[B + 1 + b] = M - 1;                    // last row of request b (lm_head)
             }
             meta[B] = M;
+            int32_t* row_of_m = meta + 2 * B + 1 + M;      // lm_head: token row -> request (or -1)
+            for (int m = 0; m < M; ++m) row_of_m[m] = -1;
+            for (int b = 0; b < B; ++b) row_of_m[meta[B + 1 + b]] = b;
             e->B = B;
             e->M = M;
         } else {
@@ -897,6 +900,8 @@ void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& d) {
     f.ffn_local = d.ffn / c->tp; f.vocab_local = d.vocab / c->tp; f.vocab = d.vocab; f.tp = c->tp; f.rank = 0;
     f.dtype = c->cfg.dtype;
     c->max_rows = c->cfg.max_batch * c->cfg.max_tokens;
+    f.gemm_impl = c->cfg.gemm_impl;
+    f.max_rows = c->max_rows;
     const size_t wsb = workspace_bytes(f, c->max_rows, c->cfg.max_batch);
     const unsigned ev_flags = c->mp ? (cudaEventInterprocess | cudaEventDisableTiming) : cudaEventDisableTiming;
     for (auto& Rp : c->ranks) {
@@ -924,7 +929,7 @@ void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& d) {
     c->ring_n = c->D + 1;
     const size_t logits_b = ((size_t)c->cfg.max_batch * d.vocab * 4 + 255) & ~size_t(255);
     c->ring_tok_off = logits_b;
-    c->ring_stride = (logits_b + (size_t)(c->max_rows * 2 + 3 * c->cfg.max_batch + 8) * 4 + 4095) & ~size_t(4095);
+    c->ring_stride = (logits_b + (size_t)(c->max_rows * 3 + 3 * c->cfg.max_batch + 8) * 4 + 4095) & ~size_t(4095);
     const size_t stg_bytes = c->ring_stride * c->ring_n;
     if (!c->mp) {
         c->stg_local = pin_alloc(stg_bytes, c->ranks[0]->numa);
@@ -1037,6 +1042,7 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     if (cfg->chunk_bytes % 4096) return set_error(MPSW_EINVAL, "chunk_bytes must be a multiple of 4096");
     if (cfg->swap_mode < 0 || cfg->swap_mode > 2) return set_error(MPSW_EINVAL, "bad swap_mode");
     if (cfg->param_budget_bytes_per_gpu == 0) return set_error(MPSW_EINVAL, "param budget is 0");
+    if (cfg->gemm_impl < 0 || cfg->gemm_impl > 2) return set_error(MPSW_EINVAL, "bad gemm_impl");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
         cudaGetLastError();

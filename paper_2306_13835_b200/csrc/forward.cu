@@ -16,6 +16,10 @@
 
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
 namespace mpsw {
 
 namespace {
@@ -372,6 +376,32 @@ inline size_t esz(int dtype) { return dtype == MPSW_BF16 ? 2 : 4; }
 // ------------------------------------------------------------------ workspace
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// GEMM shapes of one rank's forward: (n_total, K)
+static void gemm_shapes(const FwdShape& s, int out[5][2]) {
+    const int hl = s.heads_local * s.head_dim;
+    const int sh[5][2] = {{3 * hl, s.hidden}, {s.hidden, hl}, {s.ffn_local, s.hidden}, {s.hidden, s.ffn_local},
+                          {s.vocab_local, s.hidden}};
+    for (int i = 0; i < 5; ++i) out[i][0] = sh[i][0], out[i][1] = sh[i][1];
+}
+
+static size_t tc_ws_floats(const FwdShape& s, int max_rows) {
+    if (s.dtype != MPSW_BF16) return 0;
+    int sh[5][2];
+    gemm_shapes(s, sh);
+    const int Mp = std::max(16, (std::min(max_rows, 256) + 15) / 16 * 16);
+    size_t m = 0;
+    for (auto& x : sh) m = std::max(m, tc_partial_floats(x[0], x[1], Mp));
+    return m;
+}
+
+static size_t tc_tiles_max(const FwdShape& s) {
+    int sh[5][2];
+    gemm_shapes(s, sh);
+    size_t m = 0;
+    for (auto& x : sh) m = std::max(m, (size_t)(x[0] + 127) / 128 + 3);
+    return m;
+}
+
 size_t workspace_bytes(const FwdShape& s, int max_rows, int max_batch) {
     const size_t e = esz(s.dtype), M = max_rows, h = s.hidden, hl = (size_t)s.heads_local * s.head_dim;
     size_t b = 0;
@@ -383,7 +413,9 @@ size_t workspace_bytes(const FwdShape& s, int max_rows, int max_batch) {
     b += 2 * align_up(M * h * 4);                // partials
     b += align_up((size_t)max_batch * s.vocab_local * 4);   // logits
     b += align_up(M * 4);                        // tokens
-    b += align_up((3 * (size_t)max_batch + 2 + M) * 4);     // meta
+    b += align_up((3 * (size_t)max_batch + 2 + 2 * M) * 4);     // meta
+    b += align_up(tc_ws_floats(s, max_rows) * 4);               // tcgen05 split-K partials
+    b += align_up(tc_tiles_max(s) * 4);                         // tile counters
     return b;
 }
 
@@ -401,7 +433,9 @@ void workspace_carve(FwdWorkspace& w, const FwdShape& s, int max_rows, int max_b
     w.partial[1] = (float*)take(M * h * 4);
     w.logits = (float*)take((size_t)max_batch * s.vocab_local * 4);
     w.tokens = (int32_t*)take(M * 4);
-    w.meta = (int32_t*)take((3 * (size_t)max_batch + 2 + M) * 4);
+    w.meta = (int32_t*)take((3 * (size_t)max_batch + 2 + 2 * M) * 4);
+    w.tc_partial = (float*)take(tc_ws_floats(s, max_rows) * 4);
+    w.tc_counters = (int*)take(tc_tiles_max(s) * 4);
     w.bytes = (size_t)(p - (char*)base);
 }
 
@@ -456,6 +490,31 @@ int fwd_reduce_ln(const FwdShape& s, int M, const float* const* peer_partials, i
     return 1;
 }
 
+// Route one GEMM to the tcgen05/TMA kernel (bf16, M <= 256) or the SIMT weight-streaming kernel
+// (fp32 parity mode: true fp32 FMA, no TF32).
+static bool use_tc(const FwdShape& s, int M, int K) {
+    if (s.dtype != MPSW_BF16 || s.gemm_impl == 1) return false;
+    return tc_supported(M, K);
+}
+
+static void run_gemm(const FwdShape& s, int epi, GemmArgs& g, const FwdWorkspace& ws, const int32_t* row_of_m,
+                     cudaStream_t st) {
+    if (use_tc(s, g.M, g.K) && !g.a_rows) {
+        const void* W[3];
+        const void* bias[3];
+        int N[3], col0[3];
+        float sc[3];
+        for (int i = 0; i < g.nseg; ++i) {
+            W[i] = g.seg[i].W; bias[i] = g.seg[i].bias; N[i] = g.seg[i].N; sc[i] = g.seg[i].scale;
+            col0[i] = g.seg[i].out_col0;
+        }
+        tc_gemm(W, bias, N, sc, col0, g.nseg, g.A, s.max_rows, g.M, g.K, epi, g.out, g.ldo, row_of_m, ws.tc_partial,
+                ws.tc_counters, st);
+        return;
+    }
+    launch_gemm(s.dtype, epi, g, st);
+}
+
 int fwd_qkv(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M, cudaStream_t st) {
     const int hl = s.heads_local * s.head_dim;
     GemmArgs g{};
@@ -465,7 +524,7 @@ int fwd_qkv(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& w
     g.seg[1] = {L.k_w, L.k_b, hl, 1.0f, hl};
     g.seg[2] = {L.v_w, L.v_b, hl, 1.0f, 2 * hl};
     g.nseg = 3; g.out = ws.qkv; g.ldo = 3 * hl;
-    launch_gemm(s.dtype, EPI_F32, g, st);
+    run_gemm(s, EPI_F32, g, ws, nullptr, st);
     return 1;
 }
 
@@ -488,7 +547,7 @@ int fwd_out_proj(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspa
     g.A = ws.o; g.M = M; g.K = hl; g.lda = hl;
     g.seg[0] = {L.o_w, nullptr, s.hidden, 1.0f, 0};   // bias added once after the all-reduce
     g.nseg = 1; g.out = partial; g.ldo = s.hidden;
-    launch_gemm(s.dtype, EPI_F32, g, st);
+    run_gemm(s, EPI_F32, g, ws, nullptr, st);
     return 1;
 }
 
@@ -497,7 +556,7 @@ int fwd_fc1(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& w
     g.A = ws.a; g.M = M; g.K = s.hidden; g.lda = s.hidden;
     g.seg[0] = {L.fc1_w, L.fc1_b, s.ffn_local, 1.0f, 0};
     g.nseg = 1; g.out = ws.r; g.ldo = s.ffn_local;
-    launch_gemm(s.dtype, EPI_RELU_T, g, st);
+    run_gemm(s, EPI_RELU_T, g, ws, nullptr, st);
     return 1;
 }
 
@@ -507,17 +566,89 @@ int fwd_fc2(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& w
     g.A = ws.r; g.M = M; g.K = s.ffn_local; g.lda = s.ffn_local;
     g.seg[0] = {L.fc2_w, nullptr, s.hidden, 1.0f, 0};
     g.nseg = 1; g.out = partial; g.ldo = s.hidden;
-    launch_gemm(s.dtype, EPI_F32, g, st);
+    run_gemm(s, EPI_F32, g, ws, nullptr, st);
     return 1;
 }
 
-int fwd_lm_head(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, int B, cudaStream_t st) {
+int fwd_lm_head(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, int B, int M, cudaStream_t st) {
     GemmArgs g{};
-    g.A = ws.a; g.a_rows = ws.meta + (B + 1); g.M = B; g.K = s.hidden; g.lda = s.hidden;
+    g.K = s.hidden; g.lda = s.hidden;
     g.seg[0] = {W.embed_tok, nullptr, s.vocab_local, 1.0f, 0};
     g.nseg = 1; g.out = ws.logits; g.ldo = s.vocab_local;
-    launch_gemm(s.dtype, EPI_F32, g, st);
+    g.A = ws.a;
+    if (use_tc(s, M, s.hidden)) {
+        // tensor-core path: compute every token row, keep the last row of each request
+        g.M = M;
+        g.n_total = s.vocab_local;
+        run_gemm(s, EPI_F32, g, ws, ws.meta + 2 * B + 1 + M, st);
+    } else {
+        g.a_rows = ws.meta + (B + 1); g.M = B;
+        launch_gemm(s.dtype, EPI_F32, g, st);
+    }
     return 1;
 }
 
 }  // namespace mpsw
+
+// ------------------------------------------------------------------ verification hook
+#include "../../include/mpsw_testing.h"
+
+extern "C" mpsw_status mpsw_test_gemm(int device, int dtype, int impl, const void* W, const void* X,
+                                      const void* bias, int M, int N, int K, int epi, float scale, float* out) {
+    using namespace mpsw;
+    try {
+        if (M < 1 || N < 1 || K < 8 || K % 8 || (impl != 1 && impl != 2) || (dtype != MPSW_BF16 && dtype != MPSW_FP32))
+            return set_error(MPSW_EINVAL, "bad shape / impl / dtype");
+        if (impl == 2 && (dtype != MPSW_BF16 || !tc_supported(M, K)))
+            return set_error(MPSW_EINVAL, "tcgen05 path needs bf16 and M <= 256");
+        MPSW_CU(cudaSetDevice(device));
+        const size_t es = dtype == MPSW_BF16 ? 2 : 4;
+        void *dW, *dX, *dB = nullptr, *dO;
+        int* dCnt;
+        float* dP;
+        const int Mp = std::max(16, (M + 15) / 16 * 16);
+        const size_t pf = std::max<size_t>(1, tc_partial_floats(N, K, Mp));
+        MPSW_CU(cudaMalloc(&dW, (size_t)N * K * es));
+        MPSW_CU(cudaMalloc(&dX, (size_t)M * K * es));
+        MPSW_CU(cudaMalloc(&dO, (size_t)M * N * 4));
+        MPSW_CU(cudaMalloc(&dP, pf * 4));
+        MPSW_CU(cudaMalloc(&dCnt, ((N + 127) / 128 + 4) * 4));
+        MPSW_CU(cudaMemset(dCnt, 0, ((N + 127) / 128 + 4) * 4));
+        MPSW_CU(cudaMemcpy(dW, W, (size_t)N * K * es, cudaMemcpyHostToDevice));
+        MPSW_CU(cudaMemcpy(dX, X, (size_t)M * K * es, cudaMemcpyHostToDevice));
+        if (bias) {
+            MPSW_CU(cudaMalloc(&dB, (size_t)N * es));
+            MPSW_CU(cudaMemcpy(dB, bias, (size_t)N * es, cudaMemcpyHostToDevice));
+        }
+        const int oes = epi == 0 ? 4 : (int)es;
+        if (impl == 2) {
+            const void* Wp[1] = {dW};
+            const void* Bp[1] = {dB};
+            int Np[1] = {N}, c0[1] = {0};
+            float sc[1] = {scale};
+            tc_gemm(Wp, Bp, Np, sc, c0, 1, dX, M, M, K, epi, dO, N, nullptr, dP, dCnt, 0);
+        } else {
+            GemmArgs g{};
+            g.A = dX; g.M = M; g.K = K; g.lda = K;
+            g.seg[0] = {dW, dB, N, scale, 0};
+            g.nseg = 1; g.out = dO; g.ldo = N;
+            launch_gemm(dtype, epi == 0 ? EPI_F32 : EPI_RELU_T, g, 0);
+        }
+        MPSW_CU(cudaDeviceSynchronize());
+        std::vector<uint8_t> h((size_t)M * N * oes);
+        MPSW_CU(cudaMemcpy(h.data(), dO, h.size(), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < (size_t)M * N; ++i) {
+            if (oes == 4) {
+                std::memcpy(&out[i], &h[4 * i], 4);
+            } else {
+                uint32_t b = (uint32_t)(h[2 * i] | (h[2 * i + 1] << 8)) << 16;
+                std::memcpy(&out[i], &b, 4);
+            }
+        }
+        cudaFree(dW); cudaFree(dX); cudaFree(dO); cudaFree(dP); cudaFree(dCnt);
+        if (dB) cudaFree(dB);
+        return MPSW_OK;
+    } catch (const Error& e) {
+        return set_error(e.status, e.what());
+    }
+}

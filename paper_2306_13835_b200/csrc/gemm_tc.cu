@@ -1,0 +1,410 @@
+// tcgen05 + TMA weight-streaming GEMM for sm_100a (bf16 in, fp32 accumulate in TMEM).
+//
+// out[m, n] = epilogue( sum_k X[m, k] * W[n, k] ),  W = [N, K] row-major weight (K contiguous),
+// X = [M, K] row-major activations, M = B*L tokens (<= 256).
+//
+// Swap-AB: the weight tile is the MMA's A operand (128 weight rows fill the 128-lane MMA M),
+// the few tokens are the B operand (MMA N = M rounded up to 16), so the tensor core is fed at
+// any batch size and the kernel is a pure HBM weight stream (arithmetic intensity ~M flop/B):
+//   * warp 0 (one elected thread): TMA producer, cp.async.bulk.tensor 2D loads of the W tile
+//     [128 x 64] and X tile [Mp x 64] (128B swizzle) into a kStages-deep smem ring;
+//   * warp 1 (one elected thread): tcgen05.mma.cta_group::1.kind::f16, 4 x (K=16) per stage,
+//     accumulator D[128 x Mp] fp32 in TMEM; tcgen05.commit frees the smem stage;
+//   * warp 2: TMEM allocator; warps 4..7: epilogue (tcgen05.ld 32x32b, lane = weight row).
+// Split-K over CTAs is chosen from (N, K) only — never from M — and the partial sums are
+// reduced by the last-arriving CTA of each tile in fixed split order, so results are
+// deterministic and bitwise batch-invariant.
+#include "internal.h"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <mutex>
+#include <unordered_map>
+
+namespace mpsw {
+
+namespace {
+
+constexpr int kBK = 64;             // K elements per stage (128 bytes of bf16 = one swizzle row)
+constexpr int kBN = 128;            // weight rows per tile (MMA M)
+constexpr int kMaxStages = 8;
+constexpr int kThreads = 256;
+constexpr uint32_t kTileABytes = kBN * kBK * 2;   // 16 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+// Bounded wait: a barrier that never completes (bad tensor map, lost arrive) traps the kernel
+// after ~2^26 polls instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done = 0;
+    for (uint32_t it = 0; !done; ++it) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (it > (1u << 26)) __trap();
+    }
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+// K-major, 128B-swizzled canonical UMMA layout: 8-row x 128 B atoms stacked along rows
+// (SBO = 1024 B), LBO unused (1), descriptor version 1 (sm_100), layout type 2 = SWIZZLE_128B.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                 // LBO (ignored for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+    d |= (uint64_t)1 << 46;                 // version
+    d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TcSeg {
+    int N;              // rows of this segment's weight
+    int tile0;          // first tile index of the segment
+    const __nv_bfloat16* bias;
+    float scale;
+    int out_col0;
+};
+
+struct TcArgs {
+    TcSeg seg[3];
+    int nseg, tiles, splits, kb_per_split, K, M, Mp, stages;
+    int epi;                     // 0: fp32 out (bias, scale); 1: bf16 out relu(acc + bias)
+    void* out;
+    int ldo;
+    const int32_t* row_of_m;     // optional: output row for token m (-1 = drop); lm_head
+    float* partial;              // [tiles][splits][128][Mp]
+    int* counters;               // [tiles]
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant__ CUtensorMap map_w1,
+               const __grid_constant__ CUtensorMap map_w2, const __grid_constant__ CUtensorMap map_x, TcArgs g) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-B alignment for the 128B swizzle atoms
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const uint32_t tile_b_bytes = (uint32_t)g.Mp * kBK * 2;
+    const int kStages = g.stages;
+    uint8_t* sa = smem;
+    uint8_t* sb = smem + kStages * kTileABytes;
+    uint64_t* full = (uint64_t*)(sb + kStages * tile_b_bytes);
+    uint64_t* empty = full + kMaxStages;
+    uint64_t* tmem_full = empty + kMaxStages;
+    uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
+    __shared__ int s_last;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.x, split = blockIdx.y;
+    int si = 0;
+    while (si + 1 < g.nseg && tile >= g.seg[si + 1].tile0) ++si;
+    const TcSeg seg = g.seg[si];
+    const int n0 = (tile - seg.tile0) * kBN;     // row offset inside the segment
+    const CUtensorMap* mw = si == 0 ? &map_w0 : (si == 1 ? &map_w1 : &map_w2);
+    const int kb0 = split * g.kb_per_split;
+    const int nkb = g.kb_per_split;
+    uint32_t ncols = 32;                          // TMEM columns: power of two >= max(32, Mp)
+    while ((int)ncols < g.Mp) ncols <<= 1;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(mw) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(ncols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem_d = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {                           // ---- TMA producer
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % kStages;
+                const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+                mbar_wait(&empty[s], ph ^ 1u);
+                mbar_expect_tx(&full[s], kTileABytes + tile_b_bytes);
+                const int kc = (kb0 + i) * kBK;
+                tma_load_2d(sa + s * kTileABytes, mw, &full[s], kc, n0);
+                tma_load_2d(sb + s * tile_b_bytes, &map_x, &full[s], kc, 0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {                           // ---- MMA issuer
+            // kind::f16: D fp32 (c_format 1), A = B = bf16 (format 1), both K-major,
+            // N = Mp (n_dim = N >> 3), M = 128 (m_dim = M >> 4)
+            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(g.Mp >> 3) << 17) |
+                                   ((uint32_t)(kBN >> 4) << 24);
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % kStages;
+                const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+                mbar_wait(&full[s], ph);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t a0 = smem_u32(sa + s * kTileABytes), b0 = smem_u32(sb + s * tile_b_bytes);
+#pragma unroll
+                for (int kk = 0; kk < kBK / 16; ++kk)
+                    umma_bf16(tmem_d, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, (i | kk) != 0);
+                umma_commit(&empty[s]);            // smem stage free once these MMAs have read it
+            }
+            umma_commit(tmem_full);                // accumulator complete
+        }
+    } else if (warp >= 4) {                        // ---- epilogue: TMEM lane = weight row
+        mbar_wait(tmem_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int q = warp - 4;                    // TMEM lane quarter of this warp
+        const int row = q * 32 + lane;             // row within the 128-row tile
+        const int n = n0 + row;                    // row within the segment
+        const bool nvalid = n < seg.N;
+        float* prow = g.partial + (((size_t)tile * g.splits + split) * kBN + row) * g.Mp;
+        float v[16];
+        for (int c = 0; c < g.Mp; c += 16) {
+            tmem_ld16(tmem_d + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+            if (g.splits > 1) {
+#pragma unroll
+                for (int j = 0; j < 16; j += 4)
+                    *reinterpret_cast<float4*>(prow + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else if (nvalid) {
+                for (int j = 0; j < 16 && c + j < g.M; ++j) {
+                    const int m = c + j;
+                    const int orow = g.row_of_m ? g.row_of_m[m] : m;
+                    if (orow < 0) continue;
+                    float x = v[j];
+                    if (seg.bias) x = x + __bfloat162float(seg.bias[n]);
+                    if (g.epi == 0)
+                        reinterpret_cast<float*>(g.out)[(size_t)orow * g.ldo + seg.out_col0 + n] = x * seg.scale;
+                    else
+                        reinterpret_cast<__nv_bfloat16*>(g.out)[(size_t)orow * g.ldo + seg.out_col0 + n] =
+                            __float2bfloat16_rn(fmaxf(x, 0.f));
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (g.splits > 1) {
+        // the last CTA of this tile reduces all splits in fixed order (deterministic)
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const int prev = atomicAdd(&g.counters[tile], 1);
+            s_last = prev == g.splits - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            if (warp >= 4) {
+                const int row = (warp - 4) * 32 + lane;
+                const int n = n0 + row;
+                if (n < seg.N) {
+                    const float* base = g.partial + ((size_t)tile * g.splits * kBN + row) * g.Mp;
+                    for (int m = 0; m < g.M; ++m) {
+                        float x = 0.f;
+                        for (int s = 0; s < g.splits; ++s) x += __ldcg(base + (size_t)s * kBN * g.Mp + m);
+                        const int orow = g.row_of_m ? g.row_of_m[m] : m;
+                        if (orow < 0) continue;
+                        if (seg.bias) x = x + __bfloat162float(seg.bias[n]);
+                        if (g.epi == 0)
+                            reinterpret_cast<float*>(g.out)[(size_t)orow * g.ldo + seg.out_col0 + n] = x * seg.scale;
+                        else
+                            reinterpret_cast<__nv_bfloat16*>(g.out)[(size_t)orow * g.ldo + seg.out_col0 + n] =
+                                __float2bfloat16_rn(fmaxf(x, 0.f));
+                    }
+                }
+            }
+            if (threadIdx.x == 0) g.counters[tile] = 0;   // ready for the next launch
+        }
+    }
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(ncols));
+}
+
+// ----------------------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    });
+    if (!fn) throw Error(MPSW_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2D bf16 tensor map over a row-major [rows, K] matrix, box [box_rows, 64] with 128B swizzle;
+// out-of-bounds rows / K are zero-filled by TMA (ragged N, K and the token padding).
+CUtensorMap make_map(const void* ptr, uint64_t rows, uint64_t K, uint32_t box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {K, rows};
+    const cuuint64_t strides[1] = {K * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(MPSW_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+struct MapKey {
+    const void* p;
+    uint64_t rows, K;
+    uint32_t box;
+    bool operator==(const MapKey& o) const { return p == o.p && rows == o.rows && K == o.K && box == o.box; }
+};
+struct MapKeyHash {
+    size_t operator()(const MapKey& k) const {
+        return std::hash<const void*>()(k.p) ^ (k.rows * 0x9E3779B97F4A7C15ull) ^ (k.K << 20) ^ k.box;
+    }
+};
+
+// per-thread cache: every rank's worker thread encodes its own maps once
+const CUtensorMap& cached_map(const void* p, uint64_t rows, uint64_t K, uint32_t box) {
+    thread_local std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+    const MapKey k{p, rows, K, box};
+    auto it = cache.find(k);
+    if (it != cache.end()) return it->second;
+    return cache.emplace(k, make_map(p, rows, K, box)).first->second;
+}
+
+}  // namespace
+
+int tc_split_k(int n_total, int K) {
+    // split-K from the weight shape only (batch invariance): aim for ~2 CTAs per SM,
+    // at least 4 k-blocks per split, and an exact division of the k-blocks
+    const int tiles = (n_total + kBN - 1) / kBN;
+    const int kb = (K + kBK - 1) / kBK;
+    int target = std::max(1, (2 * 148 + tiles - 1) / tiles);
+    target = std::min(target, std::max(1, kb / 4));
+    for (int s = target; s >= 1; --s)
+        if (kb % s == 0) return s;
+    return 1;
+}
+
+size_t tc_partial_floats(int n_total, int K, int Mp) {
+    const int tiles = (n_total + kBN - 1) / kBN;
+    const int s = tc_split_k(n_total, K);
+    return s > 1 ? (size_t)tiles * s * kBN * Mp : 0;
+}
+
+int tc_stages(int Mp) {
+    const size_t per = kTileABytes + (size_t)Mp * kBK * 2;
+    return (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, (200 * 1024) / per));
+}
+
+size_t tc_smem_bytes(int Mp) {
+    return 1024 + tc_stages(Mp) * (kTileABytes + (size_t)Mp * kBK * 2) + (2 * kMaxStages + 2) * 8 + 16;
+}
+
+bool tc_supported(int M, int K) { return M >= 1 && M <= 256 && K % 8 == 0; }
+
+// Launch: W segments (up to 3, each [N_i, K] bf16) times X [M, K] bf16 (rows of a buffer with
+// x_rows rows). epi 0: fp32 out = (acc + bias) * scale at out[(row) * ldo + out_col0 + n];
+// epi 1: bf16 out = relu(acc + bias).
+void tc_gemm(const void* const* W, const void* const* bias, const int* N, const float* scale, const int* out_col0,
+             int nseg, const void* X, int x_rows, int M, int K, int epi, void* out, int ldo, const int32_t* row_of_m,
+             float* partial, int* counters, cudaStream_t st) {
+    const int Mp = std::max(16, (M + 15) / 16 * 16);
+    TcArgs g{};
+    int tiles = 0, n_total = 0;
+    for (int i = 0; i < nseg; ++i) {
+        g.seg[i].N = N[i];
+        g.seg[i].tile0 = tiles;
+        g.seg[i].bias = (const __nv_bfloat16*)bias[i];
+        g.seg[i].scale = scale[i];
+        g.seg[i].out_col0 = out_col0[i];
+        tiles += (N[i] + kBN - 1) / kBN;
+        n_total += N[i];
+    }
+    g.nseg = nseg;
+    g.tiles = tiles;
+    g.splits = tc_split_k(n_total, K);
+    const int kb = (K + kBK - 1) / kBK;
+    g.kb_per_split = kb / g.splits;
+    g.K = K;
+    g.M = M;
+    g.Mp = Mp;
+    g.stages = tc_stages(Mp);
+    g.epi = epi;
+    g.out = out;
+    g.ldo = ldo;
+    g.row_of_m = row_of_m;
+    g.partial = partial;
+    g.counters = counters;
+    const CUtensorMap& m0 = cached_map(W[0], N[0], K, kBN);
+    const CUtensorMap& m1 = cached_map(W[nseg > 1 ? 1 : 0], N[nseg > 1 ? 1 : 0], K, kBN);
+    const CUtensorMap& m2 = cached_map(W[nseg > 2 ? 2 : 0], N[nseg > 2 ? 2 : 0], K, kBN);
+    const CUtensorMap& mx = cached_map(X, (uint64_t)x_rows, K, (uint32_t)Mp);
+    const size_t smem = tc_smem_bytes(Mp);
+    static thread_local bool attr_set = false;
+    if (!attr_set) {
+        MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_set = true;
+    }
+    dim3 grid(tiles, g.splits);
+    tc_gemm_kernel<<<grid, kThreads, smem, st>>>(m0, m1, m2, mx, g);
+    MPSW_CU(cudaGetLastError());
+}
+
+}  // namespace mpsw

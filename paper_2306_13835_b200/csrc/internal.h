@@ -71,6 +71,8 @@ struct TensorPtrs {          // device pointers of one rank's shard inside a slo
 struct FwdShape {
     int n_layers, hidden, heads_local, head_dim, ffn_local, vocab_local, vocab, tp, rank;
     int dtype;               // MPSW_BF16 / MPSW_FP32
+    int gemm_impl;           // 0 auto (tcgen05 for bf16), 1 SIMT, 2 tcgen05
+    int max_rows;            // rows of the activation buffers (max_batch * max_tokens)
 };
 
 struct FwdWorkspace {        // device buffers of one rank (sized for max_batch*max_tokens rows)
@@ -82,12 +84,22 @@ struct FwdWorkspace {        // device buffers of one rank (sized for max_batch*
     float* partial[2] = {nullptr, nullptr};   // row-parallel partials [M, h] fp32 (peers read)
     float* logits = nullptr;       // [B, V/t] fp32
     int32_t* tokens = nullptr;     // [M]
-    int32_t* meta = nullptr;       // [3*Bmax + M]: seq_start[B+1], last_row[B], pos[M]
+    int32_t* meta = nullptr;       // seq_start[B+1], last_row[B], pos[M], row_of_m[M]
+    float* tc_partial = nullptr;   // tcgen05 split-K partial sums
+    int* tc_counters = nullptr;    // per-tile arrival counters (self-resetting)
     void* base = nullptr;
     size_t bytes = 0;
 };
 size_t workspace_bytes(const FwdShape& s, int max_rows, int max_batch);
 void workspace_carve(FwdWorkspace& w, const FwdShape& s, int max_rows, int max_batch, void* base);
+
+// tcgen05/TMA weight-streaming GEMM (gemm_tc.cu)
+int tc_split_k(int n_total, int K);
+size_t tc_partial_floats(int n_total, int K, int Mp);
+bool tc_supported(int M, int K);
+void tc_gemm(const void* const* W, const void* const* bias, const int* N, const float* scale, const int* out_col0,
+             int nseg, const void* X, int x_rows, int M, int K, int epi, void* out, int ldo, const int32_t* row_of_m,
+             float* partial, int* counters, cudaStream_t st);
 
 // Kernel launchers (forward.cu). Each returns the number of kernels launched.
 int fwd_embed(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, int M, float* partial,
@@ -102,7 +114,7 @@ int fwd_out_proj(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspa
 int fwd_fc1(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M, cudaStream_t st);
 int fwd_fc2(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M, float* partial,
             cudaStream_t st);
-int fwd_lm_head(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, int B, cudaStream_t st);
+int fwd_lm_head(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, int B, int M, cudaStream_t st);
 
 inline double now_s(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

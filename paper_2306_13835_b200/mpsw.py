@@ -31,7 +31,8 @@ class Config(C.Structure):
                 ("max_batch", C.c_int), ("max_tokens", C.c_int), ("dtype", C.c_int),
                 ("max_inflight_batches", C.c_int), ("swap_mode", C.c_int), ("chunk_bytes", C.c_uint64),
                 ("writeback", C.c_int), ("trace", C.c_int), ("zc_ctas", C.c_int),
-                ("world_size", C.c_int), ("world_rank", C.c_int), ("shm_name", C.c_char_p)]
+                ("world_size", C.c_int), ("world_rank", C.c_int), ("shm_name", C.c_char_p),
+                ("gemm_impl", C.c_int)]
 
 
 class OptDims(C.Structure):
@@ -73,6 +74,8 @@ _SIGS = {
     "mpsw_residency": [_P, C.c_int, C.POINTER(C.c_int)],
     "mpsw_trace_dump": [_P, C.c_char_p],
     "mpsw_get_stats": [_P, C.POINTER(Stats)],
+    "mpsw_test_gemm": [C.c_int, C.c_int, C.c_int, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float,
+                       C.POINTER(C.c_float)],
 }
 
 _lib = None
@@ -101,6 +104,21 @@ def _check(st):
     return st
 
 
+def test_gemm(W, X, bias=None, impl=2, epi=0, scale=1.0, dtype=BF16, device=0):
+    """Verification hook (include/mpsw_testing.h): one library GEMM on host arrays.
+    W [N, K], X [M, K] as uint16 bf16 bits (dtype BF16) or float32; returns float32 [M, N]."""
+    W = np.ascontiguousarray(W)
+    X = np.ascontiguousarray(X)
+    N, K = W.shape
+    M = X.shape[0]
+    b = None if bias is None else np.ascontiguousarray(bias)
+    out = np.empty((M, N), np.float32)
+    _check(lib().mpsw_test_gemm(device, dtype, impl, W.ctypes.data, X.ctypes.data,
+                                None if b is None else b.ctypes.data, M, N, K, epi, scale,
+                                out.ctypes.data_as(C.POINTER(C.c_float))))
+    return out
+
+
 def dims_of(d):
     return OptDims(d.n_layers, d.hidden, d.heads, d.ffn, d.vocab, d.max_pos)
 
@@ -120,7 +138,7 @@ class Ctx:
 
     def __init__(self, device_ids=(0,), budget=1 << 30, max_batch=8, max_tokens=8, dtype=BF16,
                  max_inflight=1, swap_mode=SWAP_AUTO, chunk_bytes=0, writeback=1, trace=0, zc_ctas=0,
-                 world_size=1, world_rank=0, shm_name=None):
+                 world_size=1, world_rank=0, shm_name=None, gemm_impl=0):
         """Single-process: one ctx over len(device_ids) ranks. Multi-process (world_size > 1):
         device_ids = (this process's GPU,), rank world_rank of a TP group of world_size."""
         self._ids = (C.c_int * len(device_ids))(*device_ids)
@@ -130,7 +148,7 @@ class Ctx:
         self._shm = shm_name.encode() if shm_name else None
         cfg = Config(len(device_ids), self._ids, self.tp, budget, 0, max_batch, max_tokens, dtype,
                      max_inflight, swap_mode, chunk_bytes, writeback, trace, zc_ctas, world_size, world_rank,
-                     self._shm)
+                     self._shm, gemm_impl)
         h = _P()
         _check(lib().mpsw_init(C.byref(cfg), C.byref(h)))
         self.h = h
