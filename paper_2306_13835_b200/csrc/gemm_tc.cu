@@ -397,10 +397,10 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
     const CUtensorMap& m2 = cached_map(W[nseg > 2 ? 2 : 0], N[nseg > 2 ? 2 : 0], K, kBN);
     const CUtensorMap& mx = cached_map(X, (uint64_t)x_rows, K, (uint32_t)Mp);
     const size_t smem = tc_smem_bytes(Mp);
-    static thread_local bool attr_set = false;
-    if (!attr_set) {
-        MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_set = true;
+    static thread_local size_t attr_set = 0;
+    if (attr_set < smem) {
+        MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = smem;
     }
     dim3 grid(tiles, g.splits);
     tc_gemm_kernel<<<grid, kThreads, smem, st>>>(m0, m1, m2, mx, g);

@@ -30,8 +30,9 @@ def test_gemm_vs_fp64(impl, M, N, K):
     assert err < 2e-6, err
     relu = M_.test_gemm(W, X, b, impl=impl, epi=1)
     ref2 = bf16_bits_to_fp32(bf16_bits_from_fp32(np.maximum(Xf @ Wf.T + bf, 0).astype(np.float32)))
-    # bf16 output: equal up to one bf16 ulp where fp32 summation order flips the rounding
-    assert np.all(np.abs(relu - ref2) <= np.abs(ref2) * 2 ** -7 + 1e-30)
+    # bf16 output: equal up to one bf16 ulp where fp32 summation order flips the rounding (and
+    # pre-activations within fp32 rounding of 0 may land on either side of the ReLU)
+    assert np.all(np.abs(relu - ref2) <= np.abs(ref2) * 2 ** -7 + 1e-5 * np.abs(ref2).max())
 
 
 def test_fp32_simt_vs_fp64():

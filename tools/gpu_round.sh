@@ -1,11 +1,12 @@
 #!/bin/bash
-# One GPU round: build, GPU tests, smoke, bench N=1, N=2 code path on one GPU (numbers meaningless).
+# One GPU round: build, GPU tests, smoke, bench, ncu launch list + tcgen05 GEMM capture.
 set -x
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()"
-timeout 1500 python -m pytest tests -m gpu -q -rf --tb=short -k "not full_size" > gpurun_out/pytest_gpu.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -rf --tb=short > gpurun_out/pytest_gpu.txt 2>&1
 timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.txt 2>&1
-timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err
-MPSW_BENCH_DEVICE0=1 MPSW_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
-   --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 1 --model opt-1.3b \
-   > gpurun_out/bench_n2_dev0.json 2> gpurun_out/bench_n2_dev0.err
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv \
+    python bench.py --steps 2 --warmup 1 --no-cpu-baseline --n-models 2 > gpurun_out/bench_under_ncu.json 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 120 -c 4 -f -o gpurun_out/prof_tc \
+    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --n-models 2 > gpurun_out/prof_tc.log 2>&1
