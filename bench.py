@@ -34,6 +34,16 @@ import numpy as np
 PCIE_GEN5_X16_GBPS = 64.0        # nominal per direction per GPU (north star roofline)
 
 
+def _hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0                # B200_PROFILING.md fallback
+
+
+HBM_PEAK = _hbm_peak()
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -266,6 +276,7 @@ def run_ours(args, rank, world):
     return {
         "h2d_ms": h2d_ms, "swapin_lat_s": swapin_lat, "req_lat_s": lat, "dev_s": dev_s, "wall_s": wall,
         "launches": st1["kernel_launches"] - st0["kernel_launches"], "S_r": S_r, "tp": tp,
+        "fwd_ms": (st1["fwd_gpu_us_sum"] - st0["fwd_gpu_us_sum"]) / 1e3 / max(1, st1["fwd_gpu_n"] - st0["fwd_gpu_n"]),
         "ce_peak": ce_peak, "clocks": clk.summary(), "setup": {"register_pin_s": t_reg, "synth_fill_s": t_fill},
     }
 
@@ -338,6 +349,11 @@ def main():
                      "peak_source": "nominal PCIe Gen5 x16 per direction (north star); MEASURED_PEAKS.json has no PCIe entry",
                      "measured_ce_peak_GBps_per_gpu": r["ce_peak"], "frac_of_measured_ce_peak": achieved / (tp * r["ce_peak"]),
                      "kernel": "swap-in H2D (copy engine cudaMemcpyAsync chunks; not an SM kernel, so ncu dram traffic is n/a)"},
+        "forward": {"ms_per_batch_device": r["fwd_ms"], "weight_bytes_per_rank": r["S_r"],
+                    "achieved_hbm_GBps": r["S_r"] / (r["fwd_ms"] / 1e3) / 1e9 if r["fwd_ms"] > 0 else None,
+                    "peak_hbm_GBps": HBM_PEAK, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "frac": (r["S_r"] / (r["fwd_ms"] / 1e3) / 1e9) / HBM_PEAK if r["fwd_ms"] > 0 else None,
+                    "note": "TP forward of the swapped-in model (a6): weight-streaming, HBM-bound at M=B*L=2"},
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
         "setup_s": r["setup"],

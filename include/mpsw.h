@@ -194,6 +194,8 @@ typedef struct {
     uint64_t rejected;            /* requests rejected with ENOENT                          */
     int k_slots;                  /* slots per rank (0 before the first registration)       */
     uint64_t shard_bytes;         /* S_r                                                    */
+    uint64_t fwd_gpu_us_sum;      /* sum of per-batch forward device time (first local rank) */
+    uint64_t fwd_gpu_n;           /* batches in that sum                                    */
 } mpsw_stats;
 
 mpsw_status mpsw_get_stats(mpsw_ctx* ctx, mpsw_stats* out);

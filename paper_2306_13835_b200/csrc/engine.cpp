@@ -322,7 +322,7 @@ struct mpsw_ctx {
     std::mutex sm_mu;
     std::unordered_map<int64_t, std::shared_ptr<mpsw::ReqRec>> eng_reqs;   // engine-private
     std::atomic<uint64_t> launches{0}, h2d_bytes{0}, d2h_bytes{0}, swaps_in{0}, swaps_out{0}, n_batches{0},
-        n_requests{0}, rejected{0};
+        n_requests{0}, rejected{0}, fwd_us_sum{0}, fwd_n{0};
 };
 
 namespace mpsw {
@@ -447,7 +447,9 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
     const TensorPtrs& Wt = R.wptr[e.slot];
     cudaStream_t cs = R.compute;
     const int r = R.index, t = c->tp;
-    MPSW_CU(cudaEventCreateWithFlags(&e.ev_done[r], cudaEventDisableTiming));
+    MPSW_CU(cudaEventCreate(&e.ev_start[r]));
+    MPSW_CU(cudaEventCreate(&e.ev_done[r]));
+    MPSW_CU(cudaEventRecord(e.ev_start[r], cs));
     // tokens + meta (packed by the engine into the pinned ring entry)
     uint8_t* ring = c->stg + (size_t)e.ring * c->ring_stride;
     const size_t meta_n = (size_t)(3 * B + 1 + 2 * M);
@@ -652,6 +654,21 @@ void complete_batch(mpsw_ctx* c, Entry& e, double now) {
     c->done_cv.notify_all();
 }
 
+// Device time of a finished batch's forward on the first local rank (stats), then free its events.
+void record_fwd_time(mpsw_ctx* c, Entry& e) {
+    const int r0 = c->ranks[0]->index;
+    float ms = 0;
+    if (e.ev_start[r0] && e.ev_done[r0] && cudaEventElapsedTime(&ms, e.ev_start[r0], e.ev_done[r0]) == cudaSuccess) {
+        c->fwd_us_sum += (uint64_t)(ms * 1000.0f);
+        c->fwd_n++;
+    }
+    cudaGetLastError();
+    for (int r = 0; r < c->tp; ++r) {
+        if (e.ev_start[r]) cudaEventDestroy(e.ev_start[r]), e.ev_start[r] = nullptr;
+        if (e.ev_done[r]) cudaEventDestroy(e.ev_done[r]), e.ev_done[r] = nullptr;
+    }
+}
+
 // 1 = rank r finished entry e, 0 = not yet. Local ranks: their CUDA event; remote ranks (mp):
 // the ack slot the follower wrote into the shm segment.
 int rank_done(mpsw_ctx* c, Entry& e, int r) {
@@ -693,8 +710,7 @@ bool poll_inflight(mpsw_ctx* c) {
                 complete_batch(c, e, now);
                 log_event(c, "{\"ev\":\"batch_done\",\"t\":" + fmt_d(now) + ",\"batch\":" + std::to_string(e.id) + "}");
                 step_and_dispatch(c, [&](std::vector<Decision>& ds) { c->sm.batch_done(e.id, now, ds); }, now);
-                for (int r = 0; r < c->tp; ++r)
-                    if (e.ev_done[r]) cudaEventDestroy(e.ev_done[r]), e.ev_done[r] = nullptr;
+                record_fwd_time(c, e);
             } else {
                 (e.kind == E_LOAD ? c->swaps_in : c->swaps_out)++;
                 std::lock_guard<std::mutex> lk(c->done_mu);
@@ -826,7 +842,7 @@ void follower_main(mpsw_ctx* c) {
                     if (e.kind == E_OFFLOAD && c->f_state[e.model] == ST_OFFLOADING) c->f_state[e.model] = ST_EVICTED;
                 }
                 if (e.kind == E_BATCH) {
-                    if (e.ev_done[r]) cudaEventDestroy(e.ev_done[r]), e.ev_done[r] = nullptr;
+                    record_fwd_time(c, e);
                     c->n_batches++;
                 } else {
                     (e.kind == E_LOAD ? c->swaps_in : c->swaps_out)++;
@@ -1538,6 +1554,8 @@ mpsw_status mpsw_get_stats(mpsw_ctx* c, mpsw_stats* o) {
     o->rejected = c->rejected.load();
     o->k_slots = c->k;
     o->shard_bytes = c->S;
+    o->fwd_gpu_us_sum = c->fwd_us_sum.load();
+    o->fwd_gpu_n = c->fwd_n.load();
     return MPSW_OK;
     API_END
 }

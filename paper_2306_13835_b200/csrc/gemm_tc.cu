@@ -348,9 +348,11 @@ size_t tc_partial_floats(int n_total, int K, int Mp) {
     return s > 1 ? (size_t)tiles * s * kBN * Mp : 0;
 }
 
+// Stages sized so that two CTAs fit per SM (~96 KB each): one CTA's prologue/epilogue overlaps
+// the other's weight stream, and the split-K heuristic targets 2 CTAs per SM in one wave.
 int tc_stages(int Mp) {
     const size_t per = kTileABytes + (size_t)Mp * kBK * 2;
-    return (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, (200 * 1024) / per));
+    return (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, (96 * 1024) / per));
 }
 
 size_t tc_smem_bytes(int Mp) {

@@ -49,7 +49,7 @@ class Stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("swaps_in", C.c_uint64), ("swaps_out", C.c_uint64), ("batches", C.c_uint64),
                 ("requests", C.c_uint64), ("rejected", C.c_uint64), ("k_slots", C.c_int),
-                ("shard_bytes", C.c_uint64)]
+                ("shard_bytes", C.c_uint64), ("fwd_gpu_us_sum", C.c_uint64), ("fwd_gpu_n", C.c_uint64)]
 
 
 _P = C.c_void_p
