@@ -1,0 +1,125 @@
+"""Open-loop serving runs through the C-ABI (BASELINE cfg1/cfg2/cfg4-shaped traces on one GPU).
+
+For a named preset: registers the models, fills them with the C0 weights, injects a Gamma /
+Zipf / alternating trace at its arrival times (real time), and reports nearest-rank p50/p99/mean
+request latency, swap counts and swap-in GB/s; then replays the engine's recorded event
+log through the oracle scheduler (decisions must be identical) and checks the logits of sampled
+requests against the oracle forward when the model is small enough for the oracle.
+
+usage: python tools/serve_trace.py PRESET [--cv 4] [--seed 0] [--out results.json]
+presets: cfg1 | cfg2 | cfg2-t1 | cfg4-analog
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2306_13835_b200 import mpsw as M
+from synth import opt_dims, gamma_trace, alternating_blocking, zipf_rates
+from oracle import layout, forward, metrics, scheduler as S
+
+PRESETS = {
+    # 2 x OPT-125M, TP1, budget 1 model, 20 alternating blocking requests, L=2
+    "cfg1": dict(model="opt-125m", n=2, tp=1, k=1, max_batch=1, L=2, kind="alternating", n_req=20),
+    # 4 x OPT-1.3B, TP2 (two virtual ranks on one GPU: they share ONE PCIe link), budget 2 models,
+    # uniform rates 2 req/s, Gamma CV=1, 30 s, L=8, max batch 8
+    "cfg2": dict(model="opt-1.3b", n=4, tp=2, k=2, max_batch=8, L=8, kind="gamma", rates=[2.0] * 4, duration=30.0),
+    "cfg2-t1": dict(model="opt-1.3b", n=4, tp=1, k=2, max_batch=8, L=8, kind="gamma", rates=[2.0] * 4, duration=30.0),
+    # cfg4's trace shape (6 models, 4 resident, Zipf lambda_i = 10/i, CV=4, max batch 32, L=8) on
+    # OPT-1.3B-shaped models at TP1 (one GPU / 196 GB host cannot hold 6 x OPT-30B)
+    "cfg4-analog": dict(model="opt-1.3b", n=6, tp=1, k=4, max_batch=32, L=8, kind="gamma",
+                        rates=zipf_rates(6, 10.0, 1.0), duration=30.0),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("preset")
+    ap.add_argument("--cv", type=float, default=None)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--out", default="")
+    ap.add_argument("--check-logits", type=int, default=-1, help="requests to check vs the oracle (-1 = auto)")
+    args = ap.parse_args()
+    P = dict(PRESETS[args.preset])
+    d = opt_dims(P["model"])
+    tp = P["tp"]
+    S_r = layout.shard_bytes(d, tp)
+    cv = args.cv if args.cv is not None else (4.0 if "cfg4" in args.preset else 1.0)
+    if P["kind"] == "alternating":
+        trace = alternating_blocking(P["n_req"], args.seed, P["L"], d.vocab)
+    else:
+        trace = gamma_trace(P["rates"], cv, P["duration"], args.seed, P["L"], d.vocab)
+    budget = P["k"] * ((S_r + 4095) // 4096 * 4096)
+    res = {"preset": args.preset, "model": P["model"], "tp": tp, "k": P["k"], "cv": cv, "seed": args.seed,
+           "requests": len(trace), "shard_bytes": S_r}
+    t_setup = time.perf_counter()
+    with M.Ctx(device_ids=(0,) * tp, budget=budget, max_batch=P["max_batch"], max_tokens=P["L"], trace=1,
+               writeback=0) as ctx:
+        ids = [ctx.register_model(d) for _ in range(P["n"])]
+        for m in ids:
+            ctx.synth_fill(m, 7000 + m)
+        res["setup_s"] = time.perf_counter() - t_setup
+        outs = []
+        t0 = time.perf_counter()
+        for r in trace:
+            if P["kind"] == "gamma" and not r.warmup:
+                dt = r.t_arr - (time.perf_counter() - t0)
+                if dt > 0:
+                    time.sleep(dt)
+            rid, out = ctx.request(ids[r.model], r.tokens)
+            outs.append((rid, r, out))
+            if r.warmup or P["kind"] == "alternating":
+                ctx.wait_request(rid, 600)
+        lat = []
+        for rid, r, out in outs:
+            ta, td = ctx.wait_request(rid, 600)
+            if not r.warmup:
+                lat.append(td - ta)
+        tpath = "/tmp/serve_trace.ndjson"
+        ctx.trace_dump(tpath)
+        st = ctx.stats()
+        loads = [json.loads(l) for l in open(tpath) if '"dec":"load"' in l]
+        h2d = []
+        for ld in loads:
+            _, _, ms = ctx.entry_gpu_ms(ld["id"])
+            h2d.append(max(ms))
+    if P["kind"] == "alternating":
+        lat = lat[1:]                       # cold first load reported separately
+    res["latency_s"] = metrics.summary(lat)
+    res["swaps_in"] = st["swaps_in"]
+    res["swap_in_GBps_median"] = float(np.median([tp * S_r / (ms / 1e3) / 1e9 for ms in h2d])) if h2d else None
+    res["batches"] = st["batches"]
+    res["fwd_ms_mean"] = st["fwd_gpu_us_sum"] / 1e3 / max(1, st["fwd_gpu_n"])
+    # replay parity of the engine's decisions (oracle C1)
+    evs, decs = [], []
+    for line in open(tpath):
+        o = json.loads(line)
+        (evs if "ev" in o else decs).append(o)
+    rdecs, _ = S.replay(S.EngineConfig(P["n"], st["k_slots"], tp, P["max_batch"], 1), evs)
+    res["replay_identical"] = rdecs == decs
+    # logits parity on sampled requests (oracle C5, bf16-emulating) where the oracle is fast enough
+    n_check = args.check_logits if args.check_logits >= 0 else (len(outs) if P["model"] == "opt-125m" else 0)
+    if n_check:
+        errs = []
+        Ws = {}
+        for rid, r, out in outs[:: max(1, len(outs) // n_check)][:n_check]:
+            if r.model not in Ws:
+                Ws[r.model] = layout.full_tensors(d, 7000 + r.model)
+            ref = forward.forward_bf16_emulated(d, Ws[r.model], r.tokens[None])[0]
+            errs.append(forward.rel_l2(out, ref))
+        res["logits_checked"] = len(errs)
+        res["logits_max_rel_l2"] = max(errs)
+    print(json.dumps(res), flush=True)
+    if args.out:
+        with open(args.out, "a") as f:
+            f.write(json.dumps(res) + "\n")
+
+
+if __name__ == "__main__":
+    main()
