@@ -380,6 +380,14 @@ int zc_ctas(mpsw_ctx* c) { return c->cfg.zc_ctas > 0 ? c->cfg.zc_ctas : 32; }
 uint8_t* arena_of(mpsw_ctx* c, int model, const Rank& R) { return c->models[model]->arena[R.local].p; }
 
 // ----------------------------------------------------------------------------- worker issue
+bool event_done(cudaEvent_t ev) {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) return true;
+    if (q == cudaErrorNotReady) return false;
+    MPSW_CU(q);
+    return false;
+}
+
 void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
     Slot& sl = R.slots[e.slot];
     const uint8_t* src = arena_of(c, e.model, R);
@@ -388,14 +396,17 @@ void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
     MPSW_CU(cudaEventCreate(&e.ev_start[r]));
     MPSW_CU(cudaEventCreate(&e.ev_done[r]));
     MPSW_CU(cudaEventRecord(e.ev_start[r], R.h2d));
-    if (sl.whole_gate_valid) MPSW_CU(cudaStreamWaitEvent(R.h2d, sl.whole_gate, 0));
+    // gates that already completed are skipped (a stream wait on another stream's event costs
+    // tens of microseconds, which dominates small-shard swaps: DESIGN.md §8 cfg5)
+    if (sl.whole_gate_valid && !event_done(sl.whole_gate)) MPSW_CU(cudaStreamWaitEvent(R.h2d, sl.whole_gate, 0));
     if (!sl.chunk_gate_valid && zc) {
         launch_zero_copy(sl.base, src, c->S, zc_ctas(c), R.h2d);
         c->launches++;
     } else {
         for (int i = 0; i < c->n_chunks; ++i) {
             const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, c->S - off);
-            if (sl.chunk_gate_valid) MPSW_CU(cudaStreamWaitEvent(R.h2d, sl.chunk_gate[i], 0));
+            if (sl.chunk_gate_valid && !event_done(sl.chunk_gate[i]))
+                MPSW_CU(cudaStreamWaitEvent(R.h2d, sl.chunk_gate[i], 0));
             if (zc) {
                 launch_zero_copy(sl.base + off, src + off, n, zc_ctas(c), R.h2d);
                 c->launches++;
@@ -418,7 +429,8 @@ void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
     MPSW_CU(cudaEventCreate(&e.ev_done[r]));
     // eviction never races an in-flight request: the D2H stream waits for the last forward
     // that read the victim (the engine also only evicts models with no in-flight batch)
-    if (R.last_compute_valid[e.model]) MPSW_CU(cudaStreamWaitEvent(R.d2h, R.last_compute[e.model], 0));
+    if (R.last_compute_valid[e.model] && !event_done(R.last_compute[e.model]))
+        MPSW_CU(cudaStreamWaitEvent(R.d2h, R.last_compute[e.model], 0));
     MPSW_CU(cudaEventRecord(e.ev_start[r], R.d2h));
     if (c->cfg.writeback) {
         for (int i = 0; i < c->n_chunks; ++i) {

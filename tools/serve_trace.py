@@ -85,10 +85,10 @@ def main():
         ctx.trace_dump(tpath)
         st = ctx.stats()
         loads = [json.loads(l) for l in open(tpath) if '"dec":"load"' in l]
-        h2d = []
-        for ld in loads:
-            _, _, ms = ctx.entry_gpu_ms(ld["id"])
-            h2d.append(max(ms))
+        h2d = []   # host-observed swap-in latency (submit -> last rank's ack), ms: virtual ranks share
+        for ld in loads:  # one GPU and one link, so per-rank device spans would overlap-count
+            ts, td = ctx.wait(ld["id"])
+            h2d.append((max(td) - ts) * 1e3)
     if P["kind"] == "alternating":
         lat = lat[1:]                       # cold first load reported separately
     res["latency_s"] = metrics.summary(lat)
