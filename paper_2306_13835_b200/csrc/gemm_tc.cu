@@ -121,14 +121,42 @@ struct TcSeg {
 
 struct TcArgs {
     TcSeg seg[3];
-    int nseg, tiles, splits, kb_per_split, K, M, Mp, stages;
+    int nseg, tiles, kb, K, M, Mp, stages, G;
+    uint64_t units;              // tiles * kb
     int epi;                     // 0: fp32 out (bias, scale); 1: bf16 out relu(acc + bias)
     void* out;
     int ldo;
     const int32_t* row_of_m;     // optional: output row for token m (-1 = drop); lm_head
-    float* partial;              // [tiles][splits][128][Mp]
-    int* counters;               // [tiles]
+    float* partial;              // [G][2][128][Mp]: a CTA's first / last partial run
+    int* counters;               // [tiles], self-resetting
 };
+
+// Stream-K work split: CTA c owns units [ubeg(c), ubeg(c+1)) of the linearised (tile, k-block)
+// space. Depends only on (tiles, kb, G) — never on M — so it is batch-invariant.
+__device__ __forceinline__ uint64_t ubeg(const TcArgs& g, int c) { return (uint64_t)c * g.units / (uint64_t)g.G; }
+
+__device__ __forceinline__ int cta_of(const TcArgs& g, uint64_t u) {
+    int c = (int)(u * (uint64_t)g.G / g.units);
+    while (c + 1 < g.G && ubeg(g, c + 1) <= u) ++c;
+    while (c > 0 && ubeg(g, c) > u) --c;
+    return c;
+}
+
+__device__ __forceinline__ void epi_store(const TcArgs& g, const TcSeg& seg, int n, int m, float x) {
+    const int orow = g.row_of_m ? g.row_of_m[m] : m;
+    if (orow < 0) return;
+    if (seg.bias) x = x + __bfloat162float(seg.bias[n]);
+    if (g.epi == 0)
+        reinterpret_cast<float*>(g.out)[(size_t)orow * g.ldo + seg.out_col0 + n] = x * seg.scale;
+    else
+        reinterpret_cast<__nv_bfloat16*>(g.out)[(size_t)orow * g.ldo + seg.out_col0 + n] = __float2bfloat16_rn(fmaxf(x, 0.f));
+}
+
+__device__ __forceinline__ int seg_of(const TcArgs& g, int tile) {
+    int si = 0;
+    while (si + 1 < g.nseg && tile >= g.seg[si + 1].tile0) ++si;
+    return si;
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant__ CUtensorMap map_w1,
@@ -142,30 +170,32 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
     uint8_t* sb = smem + kStages * kTileABytes;
     uint64_t* full = (uint64_t*)(sb + kStages * tile_b_bytes);
     uint64_t* empty = full + kMaxStages;
-    uint64_t* tmem_full = empty + kMaxStages;
-    uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
+    uint64_t* tmem_full = empty + kMaxStages;      // [2] accumulator ready
+    uint64_t* tmem_empty = tmem_full + 2;          // [2] accumulator drained
+    uint32_t* tmem_slot = (uint32_t*)(tmem_empty + 2);
     __shared__ int s_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x, split = blockIdx.y;
-    int si = 0;
-    while (si + 1 < g.nseg && tile >= g.seg[si + 1].tile0) ++si;
-    const TcSeg seg = g.seg[si];
-    const int n0 = (tile - seg.tile0) * kBN;     // row offset inside the segment
-    const CUtensorMap* mw = si == 0 ? &map_w0 : (si == 1 ? &map_w1 : &map_w2);
-    const int kb0 = split * g.kb_per_split;
-    const int nkb = g.kb_per_split;
-    uint32_t ncols = 32;                          // TMEM columns: power of two >= max(32, Mp)
-    while ((int)ncols < g.Mp) ncols <<= 1;
+    const int c = blockIdx.x;
+    const uint64_t u0 = ubeg(g, c), u1 = ubeg(g, c + 1);
+    if (u0 >= u1) return;                          // uniform for the whole CTA
+    uint32_t nbuf = 32;                            // TMEM columns per accumulator: pow2 >= max(32, Mp)
+    while ((int)nbuf < g.Mp) nbuf <<= 1;
+    const uint32_t ncols = 2 * nbuf;               // double-buffered accumulator
 
     if (warp == 0 && lane == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(mw) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w0) : "memory");
+        if (g.nseg > 1) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w1) : "memory");
+        if (g.nseg > 2) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w2) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tmem_full[b], 1);
+            mbar_init(&tmem_empty[b], 4);          // one arrive per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -176,18 +206,21 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem_d = *tmem_slot;
+    const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {                           // ---- TMA producer
-            for (int i = 0; i < nkb; ++i) {
+        if (lane == 0) {                           // ---- TMA producer: continuous across tiles
+            for (uint64_t u = u0; u < u1; ++u) {
+                const int i = (int)(u - u0);
                 const int s = i % kStages;
                 const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+                const int tile = (int)(u / g.kb), kbi = (int)(u % g.kb);
+                const int si = seg_of(g, tile);
+                const CUtensorMap* mw = si == 0 ? &map_w0 : (si == 1 ? &map_w1 : &map_w2);
                 mbar_wait(&empty[s], ph ^ 1u);
                 mbar_expect_tx(&full[s], kTileABytes + tile_b_bytes);
-                const int kc = (kb0 + i) * kBK;
-                tma_load_2d(sa + s * kTileABytes, mw, &full[s], kc, n0);
-                tma_load_2d(sb + s * tile_b_bytes, &map_x, &full[s], kc, 0);
+                tma_load_2d(sa + s * kTileABytes, mw, &full[s], kbi * kBK, (tile - g.seg[si].tile0) * kBN);
+                tma_load_2d(sb + s * tile_b_bytes, &map_x, &full[s], kbi * kBK, 0);
             }
         }
     } else if (warp == 1) {
@@ -196,85 +229,96 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             // N = Mp (n_dim = N >> 3), M = 128 (m_dim = M >> 4)
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(g.Mp >> 3) << 17) |
                                    ((uint32_t)(kBN >> 4) << 24);
-            for (int i = 0; i < nkb; ++i) {
+            int run = 0;
+            uint32_t tmem_d = tmem_base;
+            for (uint64_t u = u0; u < u1; ++u) {
+                const int i = (int)(u - u0);
                 const int s = i % kStages;
                 const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+                const bool first = u == u0 || u % g.kb == 0;
+                const bool last = u + 1 == u1 || u % g.kb == (uint64_t)g.kb - 1;
+                if (first) {
+                    const int b = run & 1;
+                    mbar_wait(&tmem_empty[b], (((uint32_t)run >> 1) & 1u) ^ 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    tmem_d = tmem_base + (uint32_t)b * nbuf;
+                }
                 mbar_wait(&full[s], ph);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t a0 = smem_u32(sa + s * kTileABytes), b0 = smem_u32(sb + s * tile_b_bytes);
 #pragma unroll
                 for (int kk = 0; kk < kBK / 16; ++kk)
-                    umma_bf16(tmem_d, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, (i | kk) != 0);
+                    umma_bf16(tmem_d, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, (!first || kk) ? 1u : 0u);
                 umma_commit(&empty[s]);            // smem stage free once these MMAs have read it
-            }
-            umma_commit(tmem_full);                // accumulator complete
-        }
-    } else if (warp >= 4) {                        // ---- epilogue: TMEM lane = weight row
-        mbar_wait(tmem_full, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int q = warp - 4;                    // TMEM lane quarter of this warp
-        const int row = q * 32 + lane;             // row within the 128-row tile
-        const int n = n0 + row;                    // row within the segment
-        const bool nvalid = n < seg.N;
-        float* prow = g.partial + (((size_t)tile * g.splits + split) * kBN + row) * g.Mp;
-        float v[16];
-        for (int c = 0; c < g.Mp; c += 16) {
-            tmem_ld16(tmem_d + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
-            if (g.splits > 1) {
-#pragma unroll
-                for (int j = 0; j < 16; j += 4)
-                    *reinterpret_cast<float4*>(prow + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            } else if (nvalid) {
-                for (int j = 0; j < 16 && c + j < g.M; ++j) {
-                    const int m = c + j;
-                    const int orow = g.row_of_m ? g.row_of_m[m] : m;
-                    if (orow < 0) continue;
-                    float x = v[j];
-                    if (seg.bias) x = x + __bfloat162float(seg.bias[n]);
-                    if (g.epi == 0)
-                        reinterpret_cast<float*>(g.out)[(size_t)orow * g.ldo + seg.out_col0 + n] = x * seg.scale;
-                    else
-                        reinterpret_cast<__nv_bfloat16*>(g.out)[(size_t)orow * g.ldo + seg.out_col0 + n] =
-                            __float2bfloat16_rn(fmaxf(x, 0.f));
+                if (last) {
+                    umma_commit(&tmem_full[run & 1]);   // accumulator of this run complete
+                    ++run;
                 }
             }
+        }
+    } else if (warp >= 4) {                        // ---- epilogue: TMEM lane = weight row
+        const int q = warp - 4;                    // TMEM lane quarter of this warp
+        const int row = q * 32 + lane;             // row within the 128-row tile
+        const int cfirst_run_tile = (int)(u0 / g.kb);
+        int run = 0;
+        for (uint64_t u = u0; u < u1; ++run) {
+            const int tile = (int)(u / g.kb);
+            const uint64_t tend = (uint64_t)(tile + 1) * g.kb;
+            const uint64_t rend = u1 < tend ? u1 : tend;
+            const int si = seg_of(g, tile);
+            const TcSeg& seg = g.seg[si];
+            const int n = (tile - seg.tile0) * kBN + row;
+            const bool nvalid = n < seg.N;
+            const int c_first = cta_of(g, (uint64_t)tile * g.kb), c_last = cta_of(g, tend - 1);
+            const bool whole = c_first == c_last;
+            const int which = tile == cfirst_run_tile ? 0 : 1;
+            float* prow = g.partial + (((size_t)c * 2 + which) * kBN + row) * g.Mp;
+            const int b = run & 1;
+            mbar_wait(&tmem_full[b], ((uint32_t)run >> 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            float v[16];
+            for (int col = 0; col < g.Mp; col += 16) {
+                tmem_ld16(tmem_base + (uint32_t)b * nbuf + ((uint32_t)(q * 32) << 16) + (uint32_t)col, v);
+                if (!whole) {
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        *reinterpret_cast<float4*>(prow + col + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                } else if (nvalid) {
+                    for (int j = 0; j < 16 && col + j < g.M; ++j) epi_store(g, seg, n, col + j, v[j]);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[b])) : "memory");
+            if (!whole) {
+                // fix-up: the last CTA to finish a run of this tile sums all runs in k order
+                __threadfence();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (row == 0) s_last = atomicAdd(&g.counters[tile], 1) == c_last - c_first;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (s_last) {
+                    __threadfence();
+                    if (nvalid) {
+                        const int first_tile_of_cf = (int)(ubeg(g, c_first) / g.kb);
+                        for (int m = 0; m < g.M; ++m) {
+                            float x = 0.f;
+                            for (int cc = c_first; cc <= c_last; ++cc) {
+                                const int wh = (cc == c_first && first_tile_of_cf != tile) ? 1 : 0;
+                                x += __ldcg(g.partial + (((size_t)cc * 2 + wh) * kBN + row) * g.Mp + m);
+                            }
+                            epi_store(g, seg, n, m, x);
+                        }
+                    }
+                    if (row == 0) g.counters[tile] = 0;   // ready for the next launch
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+            }
+            u = rend;
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (g.splits > 1) {
-        // the last CTA of this tile reduces all splits in fixed order (deterministic)
-        if (threadIdx.x == 0) {
-            __threadfence();
-            const int prev = atomicAdd(&g.counters[tile], 1);
-            s_last = prev == g.splits - 1;
-        }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            if (warp >= 4) {
-                const int row = (warp - 4) * 32 + lane;
-                const int n = n0 + row;
-                if (n < seg.N) {
-                    const float* base = g.partial + ((size_t)tile * g.splits * kBN + row) * g.Mp;
-                    for (int m = 0; m < g.M; ++m) {
-                        float x = 0.f;
-                        for (int s = 0; s < g.splits; ++s) x += __ldcg(base + (size_t)s * kBN * g.Mp + m);
-                        const int orow = g.row_of_m ? g.row_of_m[m] : m;
-                        if (orow < 0) continue;
-                        if (seg.bias) x = x + __bfloat162float(seg.bias[n]);
-                        if (g.epi == 0)
-                            reinterpret_cast<float*>(g.out)[(size_t)orow * g.ldo + seg.out_col0 + n] = x * seg.scale;
-                        else
-                            reinterpret_cast<__nv_bfloat16*>(g.out)[(size_t)orow * g.ldo + seg.out_col0 + n] =
-                                __float2bfloat16_rn(fmaxf(x, 0.f));
-                    }
-                }
-            }
-            if (threadIdx.x == 0) g.counters[tile] = 0;   // ready for the next launch
-        }
-    }
-    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(ncols));
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
 }
 
 // ----------------------------------------------------------------------------- host side
@@ -330,33 +374,37 @@ const CUtensorMap& cached_map(const void* p, uint64_t rows, uint64_t K, uint32_t
 
 }  // namespace
 
-int tc_split_k(int n_total, int K) {
-    // split-K from the weight shape only (batch invariance): aim for ~2 CTAs per SM,
-    // at least 4 k-blocks per split, and an exact division of the k-blocks
-    const int tiles = (n_total + kBN - 1) / kBN;
-    const int kb = (K + kBK - 1) / kBK;
-    int target = std::max(1, (2 * 148 + tiles - 1) / tiles);
-    target = std::min(target, std::max(1, kb / 4));
-    for (int s = target; s >= 1; --s)
-        if (kb % s == 0) return s;
-    return 1;
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
 }
+
+// Persistent grid: two CTAs per SM (fixed, so the stream-K split never depends on M).
+static int tc_grid(int tiles, int K) {
+    const uint64_t units = (uint64_t)tiles * ((K + kBK - 1) / kBK);
+    return (int)std::min<uint64_t>(units, 2 * (uint64_t)sm_count());
+}
+
+int tc_split_k(int n_total, int K) { return tc_grid((n_total + kBN - 1) / kBN, K); }
 
 size_t tc_partial_floats(int n_total, int K, int Mp) {
-    const int tiles = (n_total + kBN - 1) / kBN;
-    const int s = tc_split_k(n_total, K);
-    return s > 1 ? (size_t)tiles * s * kBN * Mp : 0;
+    return (size_t)tc_grid((n_total + kBN - 1) / kBN, K) * 2 * kBN * Mp;
 }
 
-// Stages sized so that two CTAs fit per SM (~96 KB each): one CTA's prologue/epilogue overlaps
-// the other's weight stream, and the split-K heuristic targets 2 CTAs per SM in one wave.
+// Stages sized so that two CTAs fit per SM (<= ~110 KB each).
 int tc_stages(int Mp) {
     const size_t per = kTileABytes + (size_t)Mp * kBK * 2;
-    return (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, (96 * 1024) / per));
+    return (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, (104 * 1024) / per));
 }
 
 size_t tc_smem_bytes(int Mp) {
-    return 1024 + tc_stages(Mp) * (kTileABytes + (size_t)Mp * kBK * 2) + (2 * kMaxStages + 2) * 8 + 16;
+    return 1024 + tc_stages(Mp) * (kTileABytes + (size_t)Mp * kBK * 2) + (2 * kMaxStages + 4) * 8 + 16;
 }
 
 bool tc_supported(int M, int K) { return M >= 1 && M <= 256 && K % 8 == 0; }
@@ -381,9 +429,9 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
     }
     g.nseg = nseg;
     g.tiles = tiles;
-    g.splits = tc_split_k(n_total, K);
-    const int kb = (K + kBK - 1) / kBK;
-    g.kb_per_split = kb / g.splits;
+    g.kb = (K + kBK - 1) / kBK;
+    g.units = (uint64_t)tiles * g.kb;
+    g.G = tc_grid(tiles, K);
     g.K = K;
     g.M = M;
     g.Mp = Mp;
@@ -404,8 +452,7 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
         MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = smem;
     }
-    dim3 grid(tiles, g.splits);
-    tc_gemm_kernel<<<grid, kThreads, smem, st>>>(m0, m1, m2, mx, g);
+    tc_gemm_kernel<<<g.G, kThreads, smem, st>>>(m0, m1, m2, mx, g);
     MPSW_CU(cudaGetLastError());
 }
 
