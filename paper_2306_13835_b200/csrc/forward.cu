@@ -87,6 +87,8 @@ template <typename T, int MT, int EPI>
 __global__ void __launch_bounds__(kGemmWarps * 32) gemm_rows_kernel(GemmArgs g) {
     constexpr int V = Vec<T>::N;
     __shared__ float red[kGemmWarps][kGemmR * MT];
+    pdl_trigger();
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int n0 = blockIdx.x * kGemmR;
@@ -195,10 +197,10 @@ template <typename T, int EPI>
 void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
     const int grid = (g.n_total + kGemmR - 1) / kGemmR;
     const int threads = kGemmWarps * 32;
-    if (g.M <= 1) gemm_rows_kernel<T, 1, EPI><<<grid, threads, 0, st>>>(g);
-    else if (g.M <= 2) gemm_rows_kernel<T, 2, EPI><<<grid, threads, 0, st>>>(g);
-    else if (g.M <= 4) gemm_rows_kernel<T, 4, EPI><<<grid, threads, 0, st>>>(g);
-    else gemm_rows_kernel<T, 8, EPI><<<grid, threads, 0, st>>>(g);
+    if (g.M <= 1) launch_pdl(gemm_rows_kernel<T, 1, EPI>, grid, threads, 0, st, g);
+    else if (g.M <= 2) launch_pdl(gemm_rows_kernel<T, 2, EPI>, grid, threads, 0, st, g);
+    else if (g.M <= 4) launch_pdl(gemm_rows_kernel<T, 4, EPI>, grid, threads, 0, st, g);
+    else launch_pdl(gemm_rows_kernel<T, 8, EPI>, grid, threads, 0, st, g);
     MPSW_CU(cudaGetLastError());
 }
 
@@ -218,6 +220,8 @@ void launch_gemm(int dtype, int epi, GemmArgs& g, cudaStream_t st) {
 template <typename T>
 __global__ void embed_kernel(const int32_t* __restrict__ tokens, const T* __restrict__ E, int lo, int Vl,
                              int h, float* __restrict__ partial) {
+    pdl_trigger();
+    pdl_wait();
     const int m = blockIdx.x;
     const int tok = tokens[m];
     const bool in = tok >= lo && tok < lo + Vl;
@@ -265,6 +269,8 @@ __global__ void __launch_bounds__(kLnThreads) reduce_ln_kernel(Peers peers, cons
                                                               const T* __restrict__ beta, float* __restrict__ x_out,
                                                               T* __restrict__ ln_out, int h) {
     __shared__ float red[32];
+    pdl_trigger();
+    pdl_wait();
     const int m = blockIdx.x;
     const size_t row = (size_t)m * h;
     const int h4 = h / 4;
@@ -324,6 +330,8 @@ template <typename T>
 __global__ void __launch_bounds__(128) attention_kernel(const float* __restrict__ qkv, const int32_t* __restrict__ seq_start,
                                                         T* __restrict__ o, int hl, int hd) {
     __shared__ float sc[4][128];
+    pdl_trigger();
+    pdl_wait();
     const int b = blockIdx.x, head = blockIdx.y;
     const int s0 = seq_start[b], L = seq_start[b + 1] - s0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -444,9 +452,11 @@ int fwd_embed(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, in
               cudaStream_t st) {
     const int lo = s.rank * s.vocab_local;
     if (s.dtype == MPSW_BF16)
-        embed_kernel<bf16><<<M, 256, 0, st>>>(ws.tokens, (const bf16*)W.embed_tok, lo, s.vocab_local, s.hidden, partial);
+        launch_pdl(embed_kernel<bf16>, M, 256, 0, st, (const int32_t*)ws.tokens, (const bf16*)W.embed_tok, lo, s.vocab_local,
+                   s.hidden, partial);
     else
-        embed_kernel<float><<<M, 256, 0, st>>>(ws.tokens, (const float*)W.embed_tok, lo, s.vocab_local, s.hidden, partial);
+        launch_pdl(embed_kernel<float>, M, 256, 0, st, (const int32_t*)ws.tokens, (const float*)W.embed_tok, lo,
+                   s.vocab_local, s.hidden, partial);
     MPSW_CU(cudaGetLastError());
     return 1;
 }
@@ -455,8 +465,8 @@ template <typename T, int VPT>
 static void launch_ln(int M, const Peers& P, const float* residual, const void* bias, const void* pos_table,
                       const int32_t* pos, const void* gamma, const void* beta, float* x_out, void* ln_out, int h,
                       cudaStream_t st) {
-    reduce_ln_kernel<T, VPT><<<M, kLnThreads, 0, st>>>(P, residual, (const T*)bias, (const T*)pos_table, pos,
-                                                       (const T*)gamma, (const T*)beta, x_out, (T*)ln_out, h);
+    launch_pdl(reduce_ln_kernel<T, VPT>, M, kLnThreads, 0, st, P, residual, (const T*)bias, (const T*)pos_table, pos,
+               (const T*)gamma, (const T*)beta, x_out, (T*)ln_out, h);
 }
 
 template <typename T>
@@ -533,9 +543,10 @@ int fwd_attention(const FwdShape& s, const FwdWorkspace& ws, int B, cudaStream_t
     dim3 grid(B, s.heads_local);
     const int32_t* seq_start = ws.meta;
     if (s.dtype == MPSW_BF16)
-        attention_kernel<bf16><<<grid, 128, 0, st>>>(ws.qkv, seq_start, (bf16*)ws.o, hl, s.head_dim);
+        launch_pdl(attention_kernel<bf16>, grid, 128, 0, st, (const float*)ws.qkv, seq_start, (bf16*)ws.o, hl, s.head_dim);
     else
-        attention_kernel<float><<<grid, 128, 0, st>>>(ws.qkv, seq_start, (float*)ws.o, hl, s.head_dim);
+        launch_pdl(attention_kernel<float>, grid, 128, 0, st, (const float*)ws.qkv, seq_start, (float*)ws.o, hl,
+                   s.head_dim);
     MPSW_CU(cudaGetLastError());
     return 1;
 }

@@ -178,6 +178,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x;
     const uint64_t u0 = ubeg(g, c), u1 = ubeg(g, c + 1);
+    pdl_trigger();                                 // let the next kernel's CTAs get scheduled
     if (u0 >= u1) return;                          // uniform for the whole CTA
     uint32_t nbuf = 32;                            // TMEM columns per accumulator: pow2 >= max(32, Mp)
     while ((int)nbuf < g.Mp) nbuf <<= 1;
@@ -210,7 +211,21 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
 
     if (warp == 0) {
         if (lane == 0) {                           // ---- TMA producer: continuous across tiles
-            for (uint64_t u = u0; u < u1; ++u) {
+            // Weights do not depend on the previous kernel: the first kStages weight tiles are in
+            // flight before griddepcontrol.wait, overlapping the previous kernel's tail (PDL).
+            const int pre = (int)(u1 - u0 < (uint64_t)kStages ? u1 - u0 : (uint64_t)kStages);
+            for (int i = 0; i < pre; ++i) {
+                const uint64_t u = u0 + i;
+                const int tile = (int)(u / g.kb), kbi = (int)(u % g.kb);
+                const int si = seg_of(g, tile);
+                const CUtensorMap* mw = si == 0 ? &map_w0 : (si == 1 ? &map_w1 : &map_w2);
+                mbar_expect_tx(&full[i], kTileABytes + tile_b_bytes);
+                tma_load_2d(sa + i * kTileABytes, mw, &full[i], kbi * kBK, (tile - g.seg[si].tile0) * kBN);
+            }
+            pdl_wait();
+            for (int i = 0; i < pre; ++i)
+                tma_load_2d(sb + i * tile_b_bytes, &map_x, &full[i], (int)((u0 + i) % g.kb) * kBK, 0);
+            for (uint64_t u = u0 + pre; u < u1; ++u) {
                 const int i = (int)(u - u0);
                 const int s = i % kStages;
                 const uint32_t ph = (uint32_t)(i / kStages) & 1u;
@@ -257,6 +272,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             }
         }
     } else if (warp >= 4) {                        // ---- epilogue: TMEM lane = weight row
+        pdl_wait();                                // outputs / partials written only after it
         const int q = warp - 4;                    // TMEM lane quarter of this warp
         const int row = q * 32 + lane;             // row within the 128-row tile
         const int cfirst_run_tile = (int)(u0 / g.kb);
@@ -452,7 +468,7 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
         MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = smem;
     }
-    tc_gemm_kernel<<<g.G, kThreads, smem, st>>>(m0, m1, m2, mx, g);
+    launch_pdl(tc_gemm_kernel, g.G, kThreads, smem, st, m0, m1, m2, mx, g);
     MPSW_CU(cudaGetLastError());
 }
 

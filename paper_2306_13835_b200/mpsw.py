@@ -154,11 +154,13 @@ class Ctx:
         self.h = h
         self.dtype = dtype
         self.vocab = None
+        self._live = {}          # request id -> output array the library writes into (kept alive)
 
     def close(self):
         if self.h:
-            lib().mpsw_shutdown(self.h)
+            lib().mpsw_shutdown(self.h)   # waits for in-flight work before buffers are released
             self.h = None
+            self._live.clear()
 
     def __enter__(self):
         return self
@@ -218,8 +220,11 @@ class Ctx:
         if out is None:
             out = np.empty(self.vocab, np.float32)
         rid = C.c_int64()
+        if out.dtype != np.float32 or out.size < self.vocab or not out.flags.c_contiguous:
+            raise ValueError("out must be a contiguous float32 array of at least vocab elements")
         _check(lib().mpsw_request(self.h, model_id, tok.ctypes.data_as(C.POINTER(C.c_int32)), tok.size,
                                   out.ctypes.data_as(C.POINTER(C.c_float)), C.byref(rid)))
+        self._live[rid.value] = out    # the library writes here until the request completes
         return rid.value, out
 
     def poll(self, rid):
@@ -228,11 +233,13 @@ class Ctx:
         if st == EAGAIN:
             return None
         _check(st)
+        self._live.pop(rid, None)
         return a.value, d.value
 
     def wait_request(self, rid, timeout=-1.0):
         a, d = C.c_double(), C.c_double()
         _check(lib().mpsw_wait_request(self.h, rid, timeout, C.byref(a), C.byref(d)))
+        self._live.pop(rid, None)
         return a.value, d.value
 
     def checksum(self, model_id, rank, on_device=True):
