@@ -182,7 +182,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
     if (u0 >= u1) return;                          // uniform for the whole CTA
     uint32_t nbuf = 32;                            // TMEM columns per accumulator: pow2 >= max(32, Mp)
     while ((int)nbuf < g.Mp) nbuf <<= 1;
-    const uint32_t ncols = 2 * nbuf;               // double-buffered accumulator
+    // double-buffered accumulator while two CTAs per SM still fit in the 512 TMEM columns
+    const int nacc = nbuf <= 128 ? 2 : 1;
+    const uint32_t ncols = (uint32_t)nacc * nbuf;
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w0) : "memory");
@@ -253,8 +255,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                 const bool first = u == u0 || u % g.kb == 0;
                 const bool last = u + 1 == u1 || u % g.kb == (uint64_t)g.kb - 1;
                 if (first) {
-                    const int b = run & 1;
-                    mbar_wait(&tmem_empty[b], (((uint32_t)run >> 1) & 1u) ^ 1u);
+                    const int b = nacc == 2 ? (run & 1) : 0;
+                    const int use = nacc == 2 ? (run >> 1) : run;       // previous uses of buffer b
+                    mbar_wait(&tmem_empty[b], ((uint32_t)use & 1u) ^ 1u);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     tmem_d = tmem_base + (uint32_t)b * nbuf;
                 }
@@ -266,7 +269,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                     umma_bf16(tmem_d, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, (!first || kk) ? 1u : 0u);
                 umma_commit(&empty[s]);            // smem stage free once these MMAs have read it
                 if (last) {
-                    umma_commit(&tmem_full[run & 1]);   // accumulator of this run complete
+                    umma_commit(&tmem_full[nacc == 2 ? (run & 1) : 0]);   // accumulator of this run complete
                     ++run;
                 }
             }
@@ -289,8 +292,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             const bool whole = c_first == c_last;
             const int which = tile == cfirst_run_tile ? 0 : 1;
             float* prow = g.partial + (((size_t)c * 2 + which) * kBN + row) * g.Mp;
-            const int b = run & 1;
-            mbar_wait(&tmem_full[b], ((uint32_t)run >> 1) & 1u);
+            const int b = nacc == 2 ? (run & 1) : 0;
+            const int use = nacc == 2 ? (run >> 1) : run;
+            mbar_wait(&tmem_full[b], (uint32_t)use & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             float v[16];
             for (int col = 0; col < g.Mp; col += 16) {
