@@ -142,10 +142,10 @@ __device__ __forceinline__ int cta_of(const TcArgs& g, uint64_t u) {
     return c;
 }
 
-__device__ __forceinline__ void epi_store(const TcArgs& g, const TcSeg& seg, int n, int m, float x) {
+__device__ __forceinline__ void epi_store(const TcArgs& g, const TcSeg& seg, int n, int m, float x, float bias_n) {
     const int orow = g.row_of_m ? g.row_of_m[m] : m;
     if (orow < 0) return;
-    if (seg.bias) x = x + __bfloat162float(seg.bias[n]);
+    if (seg.bias) x = x + bias_n;
     if (g.epi == 0)
         reinterpret_cast<float*>(g.out)[(size_t)orow * g.ldo + seg.out_col0 + n] = x * seg.scale;
     else
@@ -288,6 +288,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             const TcSeg& seg = g.seg[si];
             const int n = (tile - seg.tile0) * kBN + row;
             const bool nvalid = n < seg.N;
+            const float bias_n = (seg.bias && nvalid) ? __bfloat162float(seg.bias[n]) : 0.f;
             const int c_first = cta_of(g, (uint64_t)tile * g.kb), c_last = cta_of(g, tend - 1);
             const bool whole = c_first == c_last;
             const int which = tile == cfirst_run_tile ? 0 : 1;
@@ -304,7 +305,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                     for (int j = 0; j < 16; j += 4)
                         *reinterpret_cast<float4*>(prow + col + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                 } else if (nvalid) {
-                    for (int j = 0; j < 16 && col + j < g.M; ++j) epi_store(g, seg, n, col + j, v[j]);
+                    for (int j = 0; j < 16 && col + j < g.M; ++j) epi_store(g, seg, n, col + j, v[j], bias_n);
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -320,13 +321,25 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                     __threadfence();
                     if (nvalid) {
                         const int first_tile_of_cf = (int)(ubeg(g, c_first) / g.kb);
-                        for (int m = 0; m < g.M; ++m) {
-                            float x = 0.f;
+                        for (int m0 = 0; m0 < g.M; m0 += 16) {
+                            // 16 outputs at a time: all runs' float4 loads in flight, then the
+                            // sums in fixed run (k) order
+                            float x[16];
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) x[j] = 0.f;
                             for (int cc = c_first; cc <= c_last; ++cc) {
                                 const int wh = (cc == c_first && first_tile_of_cf != tile) ? 1 : 0;
-                                x += __ldcg(g.partial + (((size_t)cc * 2 + wh) * kBN + row) * g.Mp + m);
+                                const float4* p = reinterpret_cast<const float4*>(
+                                    g.partial + (((size_t)cc * 2 + wh) * kBN + row) * g.Mp + m0);
+                                float4 q[4];
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) q[j] = __ldcg(p + j);
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    x[4 * j] += q[j].x; x[4 * j + 1] += q[j].y; x[4 * j + 2] += q[j].z; x[4 * j + 3] += q[j].w;
+                                }
                             }
-                            epi_store(g, seg, n, m, x);
+                            for (int j = 0; j < 16 && m0 + j < g.M; ++j) epi_store(g, seg, n, m0 + j, x[j], bias_n);
                         }
                     }
                     if (row == 0) g.counters[tile] = 0;   // ready for the next launch
