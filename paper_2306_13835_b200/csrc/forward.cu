@@ -270,10 +270,22 @@ __global__ void __launch_bounds__(kLnThreads) reduce_ln_kernel(Peers peers, cons
                                                               T* __restrict__ ln_out, int h) {
     __shared__ float red[32];
     pdl_trigger();
-    pdl_wait();
     const int m = blockIdx.x;
     const size_t row = (size_t)m * h;
     const int h4 = h / 4;
+    // parameters (bias, gamma, beta) do not depend on the previous kernel: load them while it
+    // drains (PDL), then wait for the partials / residual
+    float4 bi[VPT], ga[VPT], be[VPT];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int j4 = threadIdx.x + i * kLnThreads;
+        if (j4 < h4) {
+            bi[i] = bias ? ld4<T>(bias + 4 * j4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            ga[i] = ld4<T>(gamma + 4 * j4);
+            be[i] = ld4<T>(beta + 4 * j4);
+        }
+    }
+    pdl_wait();
     float4 x[VPT];
     float lsum = 0.f;
     const T* prow = pos_table ? pos_table + (size_t)pos[m] * h : nullptr;
@@ -290,7 +302,7 @@ __global__ void __launch_bounds__(kLnThreads) reduce_ln_kernel(Peers peers, cons
                 s.x += q.x; s.y += q.y; s.z += q.z; s.w += q.w;
             }
         }
-        if (bias) { const float4 b = ld4<T>(bias + j); s.x = s.x + b.x; s.y = s.y + b.y; s.z = s.z + b.z; s.w = s.w + b.w; }
+        if (bias) { s.x = s.x + bi[i].x; s.y = s.y + bi[i].y; s.z = s.z + bi[i].z; s.w = s.w + bi[i].w; }
         if (prow) { const float4 p = ld4<T>(prow + j); s.x = s.x + p.x; s.y = s.y + p.y; s.z = s.z + p.z; s.w = s.w + p.w; }
         if (residual) {
             const float4 q = *reinterpret_cast<const float4*>(residual + row + j);
@@ -315,13 +327,11 @@ __global__ void __launch_bounds__(kLnThreads) reduce_ln_kernel(Peers peers, cons
     for (int i = 0; i < VPT; ++i) {
         const int j4 = threadIdx.x + i * kLnThreads;
         if (j4 >= h4) break;
-        const int j = 4 * j4;
-        const float4 g4 = ld4<T>(gamma + j), b4 = ld4<T>(beta + j);
-        T* o = ln_out + row + j;
-        o[0] = from_f<T>(((x[i].x - mean) / den) * g4.x + b4.x);
-        o[1] = from_f<T>(((x[i].y - mean) / den) * g4.y + b4.y);
-        o[2] = from_f<T>(((x[i].z - mean) / den) * g4.z + b4.z);
-        o[3] = from_f<T>(((x[i].w - mean) / den) * g4.w + b4.w);
+        T* o = ln_out + row + 4 * j4;
+        o[0] = from_f<T>(((x[i].x - mean) / den) * ga[i].x + be[i].x);
+        o[1] = from_f<T>(((x[i].y - mean) / den) * ga[i].y + be[i].y);
+        o[2] = from_f<T>(((x[i].z - mean) / den) * ga[i].z + be[i].z);
+        o[3] = from_f<T>(((x[i].w - mean) / den) * ga[i].w + be[i].w);
     }
 }
 
