@@ -321,25 +321,19 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                     __threadfence();
                     if (nvalid) {
                         const int first_tile_of_cf = (int)(ubeg(g, c_first) / g.kb);
-                        for (int m0 = 0; m0 < g.M; m0 += 16) {
-                            // 16 outputs at a time: all runs' float4 loads in flight, then the
-                            // sums in fixed run (k) order
-                            float x[16];
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) x[j] = 0.f;
+                        for (int m0 = 0; m0 < g.M; m0 += 4) {
+                            // 4 outputs per step, register resident; runs summed in fixed k order
+                            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
                             for (int cc = c_first; cc <= c_last; ++cc) {
                                 const int wh = (cc == c_first && first_tile_of_cf != tile) ? 1 : 0;
-                                const float4* p = reinterpret_cast<const float4*>(
-                                    g.partial + (((size_t)cc * 2 + wh) * kBN + row) * g.Mp + m0);
-                                float4 q[4];
-#pragma unroll
-                                for (int j = 0; j < 4; ++j) q[j] = __ldcg(p + j);
-#pragma unroll
-                                for (int j = 0; j < 4; ++j) {
-                                    x[4 * j] += q[j].x; x[4 * j + 1] += q[j].y; x[4 * j + 2] += q[j].z; x[4 * j + 3] += q[j].w;
-                                }
+                                const float4 q = __ldcg(reinterpret_cast<const float4*>(
+                                    g.partial + (((size_t)cc * 2 + wh) * kBN + row) * g.Mp + m0));
+                                x.x += q.x; x.y += q.y; x.z += q.z; x.w += q.w;
                             }
-                            for (int j = 0; j < 16 && m0 + j < g.M; ++j) epi_store(g, seg, n, m0 + j, x[j], bias_n);
+                            epi_store(g, seg, n, m0, x.x, bias_n);
+                            if (m0 + 1 < g.M) epi_store(g, seg, n, m0 + 1, x.y, bias_n);
+                            if (m0 + 2 < g.M) epi_store(g, seg, n, m0 + 2, x.z, bias_n);
+                            if (m0 + 3 < g.M) epi_store(g, seg, n, m0 + 3, x.w, bias_n);
                         }
                     }
                     if (row == 0) g.counters[tile] = 0;   // ready for the next launch
