@@ -160,3 +160,23 @@ def element_at(d, tp: int, rank: int, model_seed: int, byte_offset: int, dtype: 
             idx = shard_flat_indices(p.spec, tp, rank)[k:k + 1]
             return weights.tensor_values(model_seed, p.spec.tid, idx, p.spec.ln_gamma, dtype)[0]
     return None
+
+
+class LazyFull:
+    """Read-only mapping name -> FULL (unsharded) tensor values, generated on demand by the C
+    transcription of C0 (oracle/c/c0gen.c) and never cached, so an OPT-13B/30B forward can be
+    computed layer by layer in O(layer) memory (test infrastructure for full-size parity)."""
+
+    def __init__(self, d, model_seed: int, dtype: str = "bf16"):
+        self.specs = {s.name: s for s in canonical_tensors(d)}
+        self.seed = model_seed
+        self.bf16 = dtype == "bf16"
+
+    def __getitem__(self, name):
+        from . import cgen
+        s = self.specs[name]
+        n = int(np.prod(s.shape))
+        return cgen.values(self.seed, s.tid, 0, n, s.ln_gamma, self.bf16).reshape(s.shape)
+
+    def keys(self):
+        return self.specs.keys()

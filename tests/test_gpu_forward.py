@@ -73,3 +73,34 @@ def test_mid_model_tp2_parity():
     W = layout.full_tensors(d, 23, "bf16")
     for t, y in zip(toks, outs):
         assert forward.rel_l2(y, forward.forward_bf16_emulated(d, W, t[None])[0]) < 1e-2
+
+
+@pytest.mark.slow
+def test_full_size_opt13b_logits_parity():
+    """cfg3 at full size (OPT-13B, TP1, the bench's launch configuration): request logits vs the
+    oracle's bf16-emulating forward computed layer by layer from the C0 spec."""
+    M = need_gpu()
+    d = opt_dims("opt-13b")
+    toks = [request_tokens(9, 0, i, 2, d.vocab) for i in range(2)]
+    outs, st = run_requests(M, d, 1, M.BF16, 1000, toks, max_batch=1)
+    W = layout.LazyFull(d, 1000)
+    for t, y in zip(toks, outs):
+        ref = forward.forward_bf16_emulated(d, W, t[None])[0]
+        err = forward.rel_l2(y, ref)
+        assert err < 1e-2, err
+        assert int(np.argmax(y)) == int(np.argmax(ref))
+
+
+@pytest.mark.slow
+def test_full_size_opt13b_tp2_batch_invariance():
+    """Property at full size: OPT-13B TP2 (virtual ranks) is bitwise batch-invariant and agrees
+    with TP1 within the bf16 tolerance."""
+    M = need_gpu()
+    d = opt_dims("opt-13b")
+    toks = [request_tokens(8, 0, i, 2, d.vocab) for i in range(3)]
+    tp2_batched, _ = run_requests(M, d, 2, M.BF16, 1001, toks, max_batch=4)
+    tp2_alone, _ = run_requests(M, d, 2, M.BF16, 1001, toks[1:2], max_batch=1)
+    assert np.array_equal(tp2_alone[0], tp2_batched[1])
+    tp1, _ = run_requests(M, d, 1, M.BF16, 1001, toks, max_batch=4)
+    for a, b in zip(tp1, tp2_batched):
+        assert forward.rel_l2(b, a) < 1e-2
