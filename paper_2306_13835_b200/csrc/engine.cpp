@@ -372,7 +372,7 @@ void group_barrier(mpsw_ctx* c) {
 bool use_zero_copy(mpsw_ctx* c, uint64_t bytes) {
     if (c->cfg.swap_mode == MPSW_SWAP_ZERO_COPY) return true;
     if (c->cfg.swap_mode == MPSW_SWAP_COPY_ENGINE) return false;
-    return bytes <= (4ull << 20);   // AUTO: small shards skip DMA setup (measured crossover: DESIGN.md §8)
+    return bytes <= (8ull << 20);   // AUTO: zero-copy for shards <= 8 MiB (cfg5 sweep crossover)
 }
 
 int zc_ctas(mpsw_ctx* c) { return c->cfg.zc_ctas > 0 ? c->cfg.zc_ctas : 32; }
