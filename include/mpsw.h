@@ -58,9 +58,9 @@ enum { MPSW_EVICTED = 0, MPSW_LOADING = 1, MPSW_RESIDENT = 2, MPSW_OFFLOADING = 
 typedef struct mpsw_ctx mpsw_ctx;   /* opaque; owns arenas, slots, streams, threads */
 
 typedef struct {
-    int n_gpus;                   /* ranks driven by THIS process (t, or 1 in multi-process)   */
+    int n_gpus;                   /* ranks driven by THIS process (tp*pp, or 1 in multi-process) */
     const int* device_ids;        /* n_gpus CUDA ordinals (caller-owned, read during init)     */
-    int tp;                       /* TP degree t: == n_gpus (single-process) or == world_size  */
+    int tp;                       /* TP degree t: tp * pp == n_gpus, or tp == world_size       */
     uint64_t param_budget_bytes_per_gpu;  /* parameter slots per rank (the swapping budget)    */
     uint64_t workspace_bytes_per_gpu;     /* 0 = auto (activations, partials, logits staging)  */
     int max_batch;                /* requests per batch entry, 1..256 (P:168 uses 8, P:196 32) */
@@ -76,6 +76,8 @@ typedef struct {
     int world_rank;               /* this process's TP rank (0 = leader)                       */
     const char* shm_name;         /* POSIX shm name for the control plane, e.g. "/mpsw_1234"   */
     int gemm_impl;                /* 0 auto (tcgen05/TMA for bf16, M <= 256), 1 SIMT, 2 tcgen05 */
+    int pp;                       /* pipeline stages (0/1 = none); ranks = tp * pp, global rank  */
+                                  /* g = stage * tp + tp_rank; single-process only; needs D = 1  */
 } mpsw_config;
 
 typedef struct { int n_layers, hidden, heads, ffn, vocab, max_pos; } mpsw_opt_dims;
@@ -86,6 +88,7 @@ typedef struct {
     int rows, cols;               /* shard shape (cols == 1 for vectors)                      */
     int split;                    /* 0 replicated, 1 row-block (column-parallel / vocab),     */
                                   /* 2 column-block (row-parallel), reading #12 */
+    int tensor_id;                /* index in the full model's canonical tensor list (C0 key) */
 } mpsw_tensor_desc;
 
 /* Create a ctx. Allocates each rank's parameter region (one cudaMalloc of the budget) and
@@ -97,12 +100,14 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out);
 /* Wait for all in-flight work, stop threads, free every arena, slot, stream. NULL is OK. */
 mpsw_status mpsw_shutdown(mpsw_ctx* ctx);
 
-/* Pure function (no ctx, no GPU): the per-rank arena layout of an OPT model at TP degree
- * `tp` (P:138 every shard keeps all T = 16*L+4 tensors). Writes up to
- * `cap` descriptors to `out` (may be NULL), the tensor count to *n and the arena size to
- * *shard_bytes. `dtype` MPSW_BF16 (2-byte elements) or MPSW_FP32. EINVAL if tp does not
- * divide heads, vocab, ffn and hidden. */
-mpsw_status mpsw_shard_layout(const mpsw_opt_dims* dims, int tp, int rank, int dtype,
+/* Pure function (no ctx, no GPU): the arena layout of TP rank `rank` of pipeline stage `stage`
+ * of an OPT model at TP degree `tp` and PP degree `pp` (P:138 every TP shard
+ * keeps all tensors of its stage; stage s holds layers [s*L/pp, (s+1)*L/pp), stage 0 the
+ * embeddings, the last stage the final LayerNorm and a copy of embed_tokens for the tied
+ * lm_head). Writes up to `cap` descriptors to `out` (may be NULL), the tensor count to *n and
+ * the arena size to *shard_bytes. `dtype` MPSW_BF16 (2-byte elements) or MPSW_FP32.
+ * EINVAL if tp does not divide heads, vocab, ffn and hidden, or pp does not divide n_layers. */
+mpsw_status mpsw_shard_layout(const mpsw_opt_dims* dims, int tp, int pp, int stage, int rank, int dtype,
                               mpsw_tensor_desc* out, int cap, int* n, uint64_t* shard_bytes);
 
 /* Register a model (P:72 co-located instances). `tp` must equal the ctx's. `shards` is an

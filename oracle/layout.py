@@ -95,15 +95,35 @@ class Placed:
     nbytes: int
 
 
-def arena_layout(d, tp: int, rank: int, dtype: str = "bf16"):
-    """Returns (list[Placed], shard_bytes).  Rank-independent in sizes (every rank has the
-    same shard shapes); `rank` kept for the API's symmetry."""
+def stage_holds(d, spec: TensorSpec, pp: int, stage: int) -> bool:
+    """Pipeline split (reading #27; P:72 TP and PP dimensions): stage s holds layers
+    [s*L/pp, (s+1)*L/pp); stage 0 also the embeddings; the last stage the final LayerNorm and
+    (for pp > 1) a copy of embed_tokens for the tied lm_head."""
+    name = spec.name
+    if name.startswith("decoder.layers."):
+        i = int(name.split(".")[2])
+        per = d.n_layers // pp
+        return stage * per <= i < (stage + 1) * per
+    if name == "decoder.embed_tokens.weight":
+        return stage == 0 or stage == pp - 1
+    if name == "decoder.embed_positions.weight":
+        return stage == 0
+    return stage == pp - 1                       # final_layer_norm
+
+
+def arena_layout(d, tp: int, rank: int, dtype: str = "bf16", pp: int = 1, stage: int = 0):
+    """Returns (list[Placed], shard_bytes) of TP rank `rank` of pipeline stage `stage`.  Sizes
+    do not depend on `rank` (every TP rank has the same shard shapes)."""
     check_tp(d, tp)
     if not 0 <= rank < tp:
         raise ValueError("rank out of range")
+    if pp < 1 or d.n_layers % pp or not 0 <= stage < pp:
+        raise ValueError("pp must divide n_layers and 0 <= stage < pp")
     es = 2 if dtype == "bf16" else 4
     off, out = 0, []
     for spec in canonical_tensors(d):
+        if not stage_holds(d, spec, pp, stage):
+            continue
         shp = shard_shape(spec, tp)
         nb = int(np.prod(shp)) * es
         out.append(Placed(spec, shp, off, nb))
@@ -111,8 +131,8 @@ def arena_layout(d, tp: int, rank: int, dtype: str = "bf16"):
     return out, off
 
 
-def shard_bytes(d, tp: int, dtype: str = "bf16") -> int:
-    return arena_layout(d, tp, 0, dtype)[1]
+def shard_bytes(d, tp: int, dtype: str = "bf16", pp: int = 1, stage: int = 0) -> int:
+    return arena_layout(d, tp, 0, dtype, pp, stage)[1]
 
 
 def replicated_bytes(d, dtype: str = "bf16") -> int:
@@ -122,9 +142,10 @@ def replicated_bytes(d, dtype: str = "bf16") -> int:
                if p.spec.split == REPL)
 
 
-def shard_image(d, tp: int, rank: int, model_seed: int, dtype: str = "bf16") -> np.ndarray:
-    """The exact bytes of rank `rank`'s arena (uint8 array of shard_bytes)."""
-    placed, total = arena_layout(d, tp, rank, dtype)
+def shard_image(d, tp: int, rank: int, model_seed: int, dtype: str = "bf16", pp: int = 1,
+                stage: int = 0) -> np.ndarray:
+    """The exact bytes of (stage, TP rank)'s arena (uint8 array of shard_bytes)."""
+    placed, total = arena_layout(d, tp, rank, dtype, pp, stage)
     img = np.zeros(total, dtype=np.uint8)
     for p in placed:
         idx = shard_flat_indices(p.spec, tp, rank)

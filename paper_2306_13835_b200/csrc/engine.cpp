@@ -227,7 +227,14 @@ struct Slot {
 };
 
 struct Rank {
-    int index = 0, local = 0, device = 0, numa = -1;   // index = global TP rank
+    int index = 0, local = 0, device = 0, numa = -1;   // index = global rank = stage * tp + trank
+    int stage = 0, trank = 0;              // pipeline stage, TP rank inside the stage
+    Layout layout;                         // this rank's arena layout (stage-dependent)
+    uint64_t S = 0, stride = 0;            // arena bytes, slot stride
+    int n_chunks = 0;
+    FwdShape fs{};                         // forward shape of this rank (its stage's layers)
+    cudaEvent_t ev_stage = nullptr;        // PP: residual stream of this stage is ready
+    std::atomic<uint64_t> stage_out{0};    // PP: id+1 of the last batch whose ev_stage is recorded
     cudaStream_t compute = nullptr, h2d = nullptr, d2h = nullptr, aux = nullptr;
     uint8_t* region = nullptr;             // param budget (one cudaMalloc)
     std::vector<Slot> slots;
@@ -264,6 +271,8 @@ struct mpsw_ctx {
     std::vector<int> device_ids;
     std::chrono::steady_clock::time_point t0;
     int tp = 1, D = 1;
+    int pp = 1, nr = 1;        // pipeline stages; ranks = tp * pp (workers, acks per entry)
+    mpsw::SpinBarrier stage_barrier[mpsw::kMaxRanks];   // TP barrier of each stage (single process)
     bool mp = false;           // multi-process mode
     bool leader = true;        // runs the engine (single-process mode: always)
     int world_rank = 0;
@@ -274,10 +283,9 @@ struct mpsw_ctx {
     // geometry (fixed by the first registered model; homogeneous slots)
     bool geom = false;
     mpsw_opt_dims dims{};
-    mpsw::Layout layout;
-    uint64_t S = 0, slot_stride = 0;
-    int k = 0, n_chunks = 0;
-    mpsw::FwdShape fshape{};
+    int k = 0;
+    uint64_t rank_S[mpsw::kMaxRanks] = {};   // arena bytes per global rank
+    int vocab = 0;
     int max_rows = 0;
     // TP peers (global rank -> partial buffers / partial-ready events)
     float* peer_partial[mpsw::kMaxRanks][2] = {};
@@ -346,9 +354,9 @@ bool group_poisoned(mpsw_ctx* c) { return c->poisoned.load() || (c->ctl && c->ct
 
 // Barrier of the t rank threads of a TP group (threads of one process, or one thread in each of
 // t processes through the shm segment). Bounded so a dead peer cannot hang the process forever.
-void group_barrier(mpsw_ctx* c) {
+void group_barrier(mpsw_ctx* c, int stage = 0) {
     if (!c->mp) {
-        c->barrier.wait();
+        c->stage_barrier[stage].wait();
         return;
     }
     ShmCtl* s = c->ctl;
@@ -391,7 +399,7 @@ bool event_done(cudaEvent_t ev) {
 void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
     Slot& sl = R.slots[e.slot];
     const uint8_t* src = arena_of(c, e.model, R);
-    const bool zc = use_zero_copy(c, c->S);
+    const bool zc = use_zero_copy(c, R.S);
     const int r = R.index;
     MPSW_CU(cudaEventCreate(&e.ev_start[r]));
     MPSW_CU(cudaEventCreate(&e.ev_done[r]));
@@ -400,11 +408,11 @@ void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
     // tens of microseconds, which dominates small-shard swaps: DESIGN.md §8 cfg5)
     if (sl.whole_gate_valid && !event_done(sl.whole_gate)) MPSW_CU(cudaStreamWaitEvent(R.h2d, sl.whole_gate, 0));
     if (!sl.chunk_gate_valid && zc) {
-        launch_zero_copy(sl.base, src, c->S, zc_ctas(c), R.h2d);
+        launch_zero_copy(sl.base, src, R.S, zc_ctas(c), R.h2d);
         c->launches++;
     } else {
-        for (int i = 0; i < c->n_chunks; ++i) {
-            const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, c->S - off);
+        for (int i = 0; i < R.n_chunks; ++i) {
+            const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, R.S - off);
             if (sl.chunk_gate_valid && !event_done(sl.chunk_gate[i]))
                 MPSW_CU(cudaStreamWaitEvent(R.h2d, sl.chunk_gate[i], 0));
             if (zc) {
@@ -423,7 +431,7 @@ void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
 void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
     Slot& sl = R.slots[e.slot];
     uint8_t* dst = arena_of(c, e.model, R);
-    const bool zc = use_zero_copy(c, c->S);
+    const bool zc = use_zero_copy(c, R.S);
     const int r = R.index;
     MPSW_CU(cudaEventCreate(&e.ev_start[r]));
     MPSW_CU(cudaEventCreate(&e.ev_done[r]));
@@ -433,8 +441,8 @@ void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
         MPSW_CU(cudaStreamWaitEvent(R.d2h, R.last_compute[e.model], 0));
     MPSW_CU(cudaEventRecord(e.ev_start[r], R.d2h));
     if (c->cfg.writeback) {
-        for (int i = 0; i < c->n_chunks; ++i) {
-            const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, c->S - off);
+        for (int i = 0; i < R.n_chunks; ++i) {
+            const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, R.S - off);
             if (zc) {
                 launch_zero_copy(dst + off, sl.base + off, n, zc_ctas(c), R.d2h);
                 c->launches++;
@@ -452,13 +460,13 @@ void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
 }
 
 void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
-    const FwdShape& s = c->fshape;
-    FwdShape sr = s;
-    sr.rank = R.index;
+    const FwdShape& s = R.fs;
     const int B = e.B, M = e.M;
     const TensorPtrs& Wt = R.wptr[e.slot];
     cudaStream_t cs = R.compute;
     const int r = R.index, t = c->tp;
+    const int g0 = R.stage * t;                    // first global rank of my stage
+    const bool first = R.stage == 0, last = R.stage == c->pp - 1;
     MPSW_CU(cudaEventCreate(&e.ev_start[r]));
     MPSW_CU(cudaEventCreate(&e.ev_done[r]));
     MPSW_CU(cudaEventRecord(e.ev_start[r], cs));
@@ -470,7 +478,7 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
                             cudaMemcpyHostToDevice, cs));
     const int32_t* pos = R.ws.meta + 2 * B + 1;
     int nl = 0, point = 0;
-    // all-reduce point: record my partial, barrier with the other ranks of the group, wait for
+    // all-reduce point: record my partial, barrier with the other TP ranks of my stage, wait for
     // every peer's partial on my stream, then the fused reduce + bias + residual + LN kernel
     // reads all t partials directly (peer / IPC mappings over NVLink).
     auto allreduce_ln = [&](const float* residual, const void* bias, const void* pos_table, const void* g,
@@ -479,32 +487,58 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
         const float* peers[kMaxRanks];
         if (t > 1) {
             MPSW_CU(cudaEventRecord(R.ev_point[pb], cs));
-            group_barrier(c);
+            group_barrier(c, R.stage);
             for (int p = 0; p < t; ++p)
-                if (p != r) MPSW_CU(cudaStreamWaitEvent(cs, c->peer_ev[p][pb], 0));
+                if (g0 + p != r) MPSW_CU(cudaStreamWaitEvent(cs, c->peer_ev[g0 + p][pb], 0));
         }
-        for (int p = 0; p < t; ++p) peers[p] = c->peer_partial[p][pb];
-        nl += fwd_reduce_ln(sr, M, peers, t, residual, bias, pos_table, pos, g, b, R.ws.x, R.ws.a, cs);
+        for (int p = 0; p < t; ++p) peers[p] = c->peer_partial[g0 + p][pb];
+        nl += fwd_reduce_ln(s, M, peers, t, residual, bias, pos_table, pos, g, b, R.ws.x, R.ws.a, cs);
         ++point;
     };
-    nl += fwd_embed(sr, Wt, R.ws, M, R.ws.partial[point & 1], cs);
-    allreduce_ln(nullptr, nullptr, Wt.embed_pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b);
+    if (first) {
+        nl += fwd_embed(s, Wt, R.ws, M, R.ws.partial[point & 1], cs);
+        allreduce_ln(nullptr, nullptr, Wt.embed_pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b);
+    } else {
+        // PP hop ("PP communication occurs through FIFO pipes"): take the residual stream
+        // of the same TP rank of the previous stage (peer copy over NVLink), then LN1 of my
+        // first layer. D = 1 for pp > 1, so batches never overlap on a stage boundary.
+        Rank& P = *c->ranks[c->local_of[r - t]];
+        int spins = 0;
+        while (P.stage_out.load(std::memory_order_acquire) < e.id + 1) {
+            if (group_poisoned(c)) throw Error(MPSW_ECUDA, "peer failed");
+            spin_pause(spins);
+        }
+        MPSW_CU(cudaStreamWaitEvent(cs, P.ev_stage, 0));
+        MPSW_CU(cudaMemcpyAsync(R.ws.partial[0], P.ws.x, (size_t)M * s.hidden * 4, cudaMemcpyDeviceToDevice, cs));
+        const float* self[1] = {R.ws.partial[0]};
+        nl += fwd_reduce_ln(s, M, self, 1, nullptr, nullptr, nullptr, pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b,
+                            R.ws.x, R.ws.a, cs);
+        point = 1;
+    }
     for (int l = 0; l < s.n_layers; ++l) {
         const auto& L = Wt.layers[l];
-        nl += fwd_qkv(sr, L, R.ws, M, cs);
-        nl += fwd_attention(sr, R.ws, B, cs);
-        nl += fwd_out_proj(sr, L, R.ws, M, R.ws.partial[point & 1], cs);
+        nl += fwd_qkv(s, L, R.ws, M, cs);
+        nl += fwd_attention(s, R.ws, B, cs);
+        nl += fwd_out_proj(s, L, R.ws, M, R.ws.partial[point & 1], cs);
         allreduce_ln(R.ws.x, L.o_b, nullptr, L.ln2_w, L.ln2_b);
-        nl += fwd_fc1(sr, L, R.ws, M, cs);
-        nl += fwd_fc2(sr, L, R.ws, M, R.ws.partial[point & 1], cs);
-        const bool last = l + 1 == s.n_layers;
-        allreduce_ln(R.ws.x, L.fc2_b, nullptr, last ? Wt.lnf_w : Wt.layers[l + 1].ln1_w,
-                     last ? Wt.lnf_b : Wt.layers[l + 1].ln1_b);
+        nl += fwd_fc1(s, L, R.ws, M, cs);
+        nl += fwd_fc2(s, L, R.ws, M, R.ws.partial[point & 1], cs);
+        const bool lastl = l + 1 == s.n_layers;
+        // after a non-final stage's last layer only the residual stream matters; the LN output
+        // (computed with this layer's LN2 parameters) is unused
+        const void* ng = lastl ? (last ? Wt.lnf_w : L.ln2_w) : Wt.layers[l + 1].ln1_w;
+        const void* nb = lastl ? (last ? Wt.lnf_b : L.ln2_b) : Wt.layers[l + 1].ln1_b;
+        allreduce_ln(R.ws.x, L.fc2_b, nullptr, ng, nb);
     }
-    nl += fwd_lm_head(sr, Wt, R.ws, B, M, cs);
-    float* logits_host = (float*)(ring) + (size_t)r * s.vocab_local;
-    MPSW_CU(cudaMemcpy2DAsync(logits_host, (size_t)s.vocab * 4, R.ws.logits, (size_t)s.vocab_local * 4,
-                              (size_t)s.vocab_local * 4, B, cudaMemcpyDeviceToHost, cs));
+    if (last) {
+        nl += fwd_lm_head(s, Wt, R.ws, B, M, cs);
+        float* logits_host = (float*)(ring) + (size_t)R.trank * s.vocab_local;
+        MPSW_CU(cudaMemcpy2DAsync(logits_host, (size_t)s.vocab * 4, R.ws.logits, (size_t)s.vocab_local * 4,
+                                  (size_t)s.vocab_local * 4, B, cudaMemcpyDeviceToHost, cs));
+    } else {
+        MPSW_CU(cudaEventRecord(R.ev_stage, cs));
+        R.stage_out.store(e.id + 1, std::memory_order_release);
+    }
     MPSW_CU(cudaEventRecord(e.ev_done[r], cs));
     MPSW_CU(cudaEventRecord(R.last_compute[e.model], cs));
     R.last_compute_valid[e.model] = 1;
@@ -580,7 +614,7 @@ void publish(mpsw_ctx* c, const Entry& e) {
     const uint64_t tail = s->log_tail.load(std::memory_order_relaxed);
     // never overwrite a record a follower has not taken yet
     int spins = 0;
-    for (int p = 1; p < c->tp; ++p)
+    for (int p = 1; p < c->nr; ++p)
         while (tail - s->consumed[p].load(std::memory_order_acquire) >= kLogCap) spin_pause(spins);
     ShmRec& rec = s->log[tail % kLogCap];
     rec.id = e.id;
@@ -650,7 +684,7 @@ void step_and_dispatch(mpsw_ctx* c, const std::function<void(std::vector<Decisio
 
 void complete_batch(mpsw_ctx* c, Entry& e, double now) {
     const uint8_t* ring = c->stg + (size_t)e.ring * c->ring_stride;
-    const int V = c->fshape.vocab;
+    const int V = c->vocab;
     for (size_t b = 0; b < e.reqs.size(); ++b) {
         auto& rq = e.reqs[b];
         std::memcpy(rq->out, (const float*)ring + b * (size_t)V, (size_t)V * 4);
@@ -675,7 +709,7 @@ void record_fwd_time(mpsw_ctx* c, Entry& e) {
         c->fwd_n++;
     }
     cudaGetLastError();
-    for (int r = 0; r < c->tp; ++r) {
+    for (int r = 0; r < c->nr; ++r) {
         if (e.ev_start[r]) cudaEventDestroy(e.ev_start[r]), e.ev_start[r] = nullptr;
         if (e.ev_done[r]) cudaEventDestroy(e.ev_done[r]), e.ev_done[r] = nullptr;
     }
@@ -700,7 +734,7 @@ bool poll_inflight(mpsw_ctx* c) {
     for (size_t i = 0; i < c->inflight.size();) {
         Entry& e = *c->inflight[i];
         bool finished = false;
-        for (int r = 0; r < c->tp; ++r) {
+        for (int r = 0; r < c->nr; ++r) {
             if (e.acked[r] || !rank_done(c, e, r)) continue;
             const double now = now_s(c->t0);
             e.acked[r] = 1;
@@ -712,11 +746,11 @@ bool poll_inflight(mpsw_ctx* c) {
                 log_event(c, "{\"ev\":\"ack\",\"t\":" + fmt_d(now) + ",\"entry\":" + std::to_string(e.id) +
                                  ",\"rank\":" + std::to_string(r) + "}");
                 step_and_dispatch(c, [&](std::vector<Decision>& ds) { c->sm.ack(e.id, r, now, ds); }, now);
-                if (e.kind == E_LOAD) c->h2d_bytes += c->S;
-                else if (c->cfg.writeback) c->d2h_bytes += c->S;
+                if (e.kind == E_LOAD) c->h2d_bytes += c->rank_S[r];
+                else if (c->cfg.writeback) c->d2h_bytes += c->rank_S[r];
             }
         }
-        if (e.n_acked == c->tp) {
+        if (e.n_acked == c->nr) {
             const double now = now_s(c->t0);
             if (e.kind == E_BATCH) {
                 complete_batch(c, e, now);
@@ -858,8 +892,8 @@ void follower_main(mpsw_ctx* c) {
                     c->n_batches++;
                 } else {
                     (e.kind == E_LOAD ? c->swaps_in : c->swaps_out)++;
-                    if (e.kind == E_LOAD) c->h2d_bytes += c->S;
-                    else if (c->cfg.writeback) c->d2h_bytes += c->S;
+                    if (e.kind == E_LOAD) c->h2d_bytes += R.S;
+                    else if (c->cfg.writeback) c->d2h_bytes += R.S;
                     std::lock_guard<std::mutex> lk(c->done_mu);
                     e.complete.store(1, std::memory_order_release);
                 }
@@ -883,20 +917,31 @@ void follower_main(mpsw_ctx* c) {
     }
 }
 
-TensorPtrs make_ptrs(const Layout& L, const uint8_t* base, int n_layers) {
+// Weight pointers of one rank's slot, looked up by HF name in that rank's layout (stage-local
+// layers only; embeddings / final LN only where the stage holds them).
+TensorPtrs make_ptrs(const Layout& L, const uint8_t* base, int layer0, int n_layers) {
+    std::unordered_map<std::string, const void*> by;
+    for (const auto& t : L.t) by[t.name] = base + t.offset;
+    auto p = [&](const std::string& n) -> const void* {
+        auto it = by.find(n);
+        return it == by.end() ? nullptr : it->second;
+    };
     TensorPtrs w;
-    auto p = [&](int i) { return (const void*)(base + L.t[i].offset); };
-    w.embed_tok = p(0);
-    w.embed_pos = p(1);
-    w.lnf_w = p(2);
-    w.lnf_b = p(3);
-    for (int l = 0; l < n_layers; ++l) {
-        const int b = 4 + 16 * l;
+    w.embed_tok = p("decoder.embed_tokens.weight");
+    w.embed_pos = p("decoder.embed_positions.weight");
+    w.lnf_w = p("decoder.final_layer_norm.weight");
+    w.lnf_b = p("decoder.final_layer_norm.bias");
+    for (int l = layer0; l < layer0 + n_layers; ++l) {
+        const std::string q = "decoder.layers." + std::to_string(l) + ".";
         TensorPtrs::Layer x;
-        x.k_w = p(b + 0); x.k_b = p(b + 1); x.v_w = p(b + 2); x.v_b = p(b + 3);
-        x.q_w = p(b + 4); x.q_b = p(b + 5); x.o_w = p(b + 6); x.o_b = p(b + 7);
-        x.ln1_w = p(b + 8); x.ln1_b = p(b + 9); x.fc1_w = p(b + 10); x.fc1_b = p(b + 11);
-        x.fc2_w = p(b + 12); x.fc2_b = p(b + 13); x.ln2_w = p(b + 14); x.ln2_b = p(b + 15);
+        x.k_w = p(q + "self_attn.k_proj.weight"); x.k_b = p(q + "self_attn.k_proj.bias");
+        x.v_w = p(q + "self_attn.v_proj.weight"); x.v_b = p(q + "self_attn.v_proj.bias");
+        x.q_w = p(q + "self_attn.q_proj.weight"); x.q_b = p(q + "self_attn.q_proj.bias");
+        x.o_w = p(q + "self_attn.out_proj.weight"); x.o_b = p(q + "self_attn.out_proj.bias");
+        x.ln1_w = p(q + "self_attn_layer_norm.weight"); x.ln1_b = p(q + "self_attn_layer_norm.bias");
+        x.fc1_w = p(q + "fc1.weight"); x.fc1_b = p(q + "fc1.bias");
+        x.fc2_w = p(q + "fc2.weight"); x.fc2_b = p(q + "fc2.bias");
+        x.ln2_w = p(q + "final_layer_norm.weight"); x.ln2_b = p(q + "final_layer_norm.bias");
         w.layers.push_back(x);
     }
     return w;
@@ -906,48 +951,59 @@ TensorPtrs make_ptrs(const Layout& L, const uint8_t* base, int n_layers) {
 // carved from the region allocated at init; workspaces sized for max_batch * max_tokens rows;
 // TP peers wired (collective in multi-process mode: IPC handles exchanged through shm).
 void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& d) {
-    Layout L;
-    if (compute_layout(d, c->tp, 0, c->cfg.dtype, L) != MPSW_OK) throw Error(MPSW_EINVAL, tls_error());
     const int hd = d.hidden / d.heads;
     if (hd % 8 || hd > 128) throw Error(MPSW_EINVAL, "head_dim must be a multiple of 8 and <= 128");
     if ((d.hidden / c->tp) % 8 || (d.ffn / c->tp) % 8 || d.hidden % 8)
         throw Error(MPSW_EINVAL, "hidden/tp, ffn/tp and hidden must be multiples of 8");
     if (d.hidden > 12288) throw Error(MPSW_EINVAL, "hidden too large for the LN kernel");
-    const uint64_t S = L.bytes;
-    const uint64_t stride = (S + kSlotAlign - 1) / kSlotAlign * kSlotAlign;
-    const int k = (int)std::min<uint64_t>(c->cfg.param_budget_bytes_per_gpu / stride, 1024);
-    if (k < 1) throw Error(MPSW_ENOMEM, "param budget cannot hold one shard (S_r = " + std::to_string(S) + ")");
+    // every global rank's arena size (stage-dependent) and the slot count k, the same on all
+    // ranks (a model occupies one slot on every worker): k = min_r floor(budget / stride_r)
+    int k = 1024;
+    for (int g = 0; g < c->nr; ++g) {
+        Layout L;
+        if (compute_layout(d, c->tp, c->pp, g / c->tp, g % c->tp, c->cfg.dtype, L) != MPSW_OK)
+            throw Error(MPSW_EINVAL, tls_error());
+        c->rank_S[g] = L.bytes;
+        const uint64_t stride = (L.bytes + kSlotAlign - 1) / kSlotAlign * kSlotAlign;
+        k = (int)std::min<uint64_t>((uint64_t)k, c->cfg.param_budget_bytes_per_gpu / stride);
+    }
+    if (k < 1)
+        throw Error(MPSW_ENOMEM, "param budget cannot hold one shard (S_r = " + std::to_string(c->rank_S[0]) + ")");
     c->dims = d;
-    c->layout = L;
-    c->S = S;
-    c->slot_stride = stride;
+    c->vocab = d.vocab;
     c->k = k;
-    c->n_chunks = (int)((S + c->chunk - 1) / c->chunk);
-    FwdShape& f = c->fshape;
-    f.n_layers = d.n_layers; f.hidden = d.hidden; f.heads_local = d.heads / c->tp; f.head_dim = hd;
-    f.ffn_local = d.ffn / c->tp; f.vocab_local = d.vocab / c->tp; f.vocab = d.vocab; f.tp = c->tp; f.rank = 0;
-    f.dtype = c->cfg.dtype;
     c->max_rows = c->cfg.max_batch * c->cfg.max_tokens;
-    f.gemm_impl = c->cfg.gemm_impl;
-    f.max_rows = c->max_rows;
-    const size_t wsb = workspace_bytes(f, c->max_rows, c->cfg.max_batch);
     const unsigned ev_flags = c->mp ? (cudaEventInterprocess | cudaEventDisableTiming) : cudaEventDisableTiming;
     for (auto& Rp : c->ranks) {
         Rank& R = *Rp;
         MPSW_CU(cudaSetDevice(R.device));
+        if (compute_layout(d, c->tp, c->pp, R.stage, R.trank, c->cfg.dtype, R.layout) != MPSW_OK)
+            throw Error(MPSW_EINVAL, tls_error());
+        R.S = R.layout.bytes;
+        R.stride = (R.S + kSlotAlign - 1) / kSlotAlign * kSlotAlign;
+        R.n_chunks = (int)((R.S + c->chunk - 1) / c->chunk);
+        FwdShape& f = R.fs;
+        f.n_layers = d.n_layers / c->pp; f.hidden = d.hidden; f.heads_local = d.heads / c->tp; f.head_dim = hd;
+        f.ffn_local = d.ffn / c->tp; f.vocab_local = d.vocab / c->tp; f.vocab = d.vocab; f.tp = c->tp;
+        f.rank = R.trank;
+        f.dtype = c->cfg.dtype;
+        f.gemm_impl = c->cfg.gemm_impl;
+        f.max_rows = c->max_rows;
+        const size_t wsb = workspace_bytes(f, c->max_rows, c->cfg.max_batch);
         R.slots.resize(k);
         for (int s = 0; s < k; ++s) {
             Slot& sl = R.slots[s];
-            sl.base = R.region + (uint64_t)s * stride;
-            sl.chunk_gate.resize(c->n_chunks);
+            sl.base = R.region + (uint64_t)s * R.stride;
+            sl.chunk_gate.resize(R.n_chunks);
             for (auto& ev : sl.chunk_gate) MPSW_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
             MPSW_CU(cudaEventCreateWithFlags(&sl.whole_gate, cudaEventDisableTiming));
-            R.wptr.push_back(make_ptrs(L, sl.base, d.n_layers));
+            R.wptr.push_back(make_ptrs(R.layout, sl.base, R.stage * f.n_layers, f.n_layers));
         }
         MPSW_CU(cudaMalloc(&R.ws_base, wsb));
         MPSW_CU(cudaMemset(R.ws_base, 0, wsb));
         workspace_carve(R.ws, f, c->max_rows, c->cfg.max_batch, R.ws_base);
         for (auto& ev : R.ev_point) MPSW_CU(cudaEventCreateWithFlags(&ev, ev_flags));
+        MPSW_CU(cudaEventCreateWithFlags(&R.ev_stage, cudaEventDisableTiming));
         for (int pb = 0; pb < 2; ++pb) {
             c->peer_partial[R.index][pb] = R.ws.partial[pb];
             c->peer_ev[R.index][pb] = R.ev_point[pb];
@@ -1026,7 +1082,7 @@ static mpsw_status need_leader(mpsw_ctx* c) {
 }
 
 static int local_index(mpsw_ctx* c, int rank) {
-    if (rank < 0 || rank >= c->tp) return -1;
+    if (rank < 0 || rank >= c->nr) return -1;
     return c->local_of[rank];
 }
 
@@ -1034,12 +1090,12 @@ extern "C" {
 
 const char* mpsw_last_error(void) { return tls_error().c_str(); }
 
-mpsw_status mpsw_shard_layout(const mpsw_opt_dims* dims, int tp, int rank, int dtype, mpsw_tensor_desc* out,
-                              int cap, int* n, uint64_t* shard_bytes) {
+mpsw_status mpsw_shard_layout(const mpsw_opt_dims* dims, int tp, int pp, int stage, int rank, int dtype,
+                              mpsw_tensor_desc* out, int cap, int* n, uint64_t* shard_bytes) {
     API_BEGIN
     if (!dims) return set_error(MPSW_EINVAL, "dims is NULL");
     Layout L;
-    mpsw_status s = compute_layout(*dims, tp, rank, dtype, L);
+    mpsw_status s = compute_layout(*dims, tp, pp, stage, rank, dtype, L);
     if (s != MPSW_OK) return s;
     if (n) *n = (int)L.t.size();
     if (shard_bytes) *shard_bytes = L.bytes;
@@ -1053,17 +1109,21 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     API_BEGIN
     if (!cfg || !out) return set_error(MPSW_EINVAL, "NULL argument");
     const bool mp = cfg->world_size > 1;
+    const int pp = cfg->pp > 0 ? cfg->pp : 1;
     if (cfg->n_gpus < 1 || cfg->n_gpus > kMaxRanks || !cfg->device_ids)
         return set_error(MPSW_EINVAL, "n_gpus must be 1..8 with device_ids");
     if (mp) {
         if (cfg->world_size > kMaxRanks) return set_error(MPSW_EINVAL, "world_size must be <= 8");
         if (cfg->n_gpus != 1 || cfg->tp != cfg->world_size)
             return set_error(MPSW_EINVAL, "multi-process mode: n_gpus = 1 and tp = world_size");
+        if (pp != 1) return set_error(MPSW_EINVAL, "pipeline parallelism is single-process only");
         if (cfg->world_rank < 0 || cfg->world_rank >= cfg->world_size) return set_error(MPSW_EINVAL, "bad world_rank");
         if (!cfg->shm_name || cfg->shm_name[0] != '/') return set_error(MPSW_EINVAL, "shm_name must start with '/'");
-    } else if (cfg->tp != cfg->n_gpus) {
-        return set_error(MPSW_EINVAL, "tp must equal n_gpus (one TP group per ctx)");
+    } else if (cfg->tp < 1 || cfg->tp * pp != cfg->n_gpus) {
+        return set_error(MPSW_EINVAL, "tp * pp must equal n_gpus (one TP x PP group per ctx)");
     }
+    if (pp > 1 && cfg->max_inflight_batches > 1)
+        return set_error(MPSW_EINVAL, "pp > 1 requires max_inflight_batches = 1");
     if (cfg->max_batch < 1 || cfg->max_batch > 256) return set_error(MPSW_EINVAL, "max_batch must be 1..256");
     if (cfg->max_tokens < 1 || cfg->max_tokens > 128) return set_error(MPSW_EINVAL, "max_tokens must be 1..128");
     if (cfg->dtype != MPSW_BF16 && cfg->dtype != MPSW_FP32) return set_error(MPSW_EINVAL, "bad dtype");
@@ -1084,14 +1144,17 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     c->world_rank = mp ? cfg->world_rank : 0;
     c->leader = !mp || cfg->world_rank == 0;
     c->tp = cfg->tp;
+    c->pp = pp;
+    c->nr = mp ? cfg->world_size : cfg->n_gpus;
     c->D = cfg->max_inflight_batches > 0 ? cfg->max_inflight_batches : 1;
     c->chunk = cfg->chunk_bytes ? cfg->chunk_bytes : (64ull << 20);
     c->trace = cfg->trace != 0 && c->leader;
     c->device_ids.assign(cfg->device_ids, cfg->device_ids + cfg->n_gpus);
-    c->sm.tp = c->tp;
+    c->sm.tp = c->nr;              // acks per entry: one per worker
     c->sm.max_batch = cfg->max_batch;
     c->sm.D = c->D;
     c->barrier.n = mp ? 1 : c->tp;
+    for (auto& b : c->stage_barrier) b.n = mp ? 1 : c->tp;
     c->models.reserve(kMaxModels);
     for (auto& x : c->local_of) x = -1;
     for (int l = 0; l < cfg->n_gpus; ++l) {
@@ -1099,6 +1162,8 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
         if (dev < 0 || dev >= ndev) return set_error(MPSW_EINVAL, "device id out of range");
         auto R = std::make_unique<Rank>();
         R->index = mp ? cfg->world_rank : l;
+        R->stage = R->index / cfg->tp;
+        R->trank = R->index % cfg->tp;
         R->local = l;
         R->device = dev;
         R->numa = gpu_numa_node(dev);
@@ -1122,8 +1187,8 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     }
     if (!mp) {
         // peer access between distinct devices of the group (TP all-reduce reads peer partials)
-        for (int a = 0; a < c->tp; ++a)
-            for (int b = 0; b < c->tp; ++b) {
+        for (int a = 0; a < c->nr; ++a)
+            for (int b = 0; b < c->nr; ++b) {
                 const int da = c->device_ids[a], db = c->device_ids[b];
                 if (da == db) continue;
                 int ok = 0;
@@ -1205,6 +1270,7 @@ mpsw_status mpsw_shutdown(mpsw_ctx* c) {
         }
         for (auto ev : R->ev_point)
             if (ev) cudaEventDestroy(ev);
+        if (R->ev_stage) cudaEventDestroy(R->ev_stage);
         for (auto ev : R->last_compute)
             if (ev) cudaEventDestroy(ev);
         cudaFree(R->region);
@@ -1216,7 +1282,7 @@ mpsw_status mpsw_shutdown(mpsw_ctx* c) {
         cudaStreamDestroy(R->aux);
     }
     for (auto& kv : c->entries)
-        for (int r = 0; r < c->tp; ++r) {
+        for (int r = 0; r < c->nr; ++r) {
             if (kv.second->ev_start[r]) cudaEventDestroy(kv.second->ev_start[r]);
             if (kv.second->ev_done[r]) cudaEventDestroy(kv.second->ev_done[r]);
         }
@@ -1245,7 +1311,7 @@ mpsw_status mpsw_register_model(mpsw_ctx* c, const mpsw_opt_dims* dims, int tp, 
     if (tp != c->tp) return set_error(MPSW_EINVAL, "model tp must equal the ctx tp");
     std::lock_guard<std::mutex> api(c->api_mu);
     Layout L;
-    mpsw_status s = compute_layout(*dims, tp, 0, c->cfg.dtype, L);
+    mpsw_status s = compute_layout(*dims, tp, c->pp, 0, 0, c->cfg.dtype, L);
     if (s != MPSW_OK) return s;
     {
         std::lock_guard<std::mutex> lk(c->cmd_mu);
@@ -1255,14 +1321,14 @@ mpsw_status mpsw_register_model(mpsw_ctx* c, const mpsw_opt_dims* dims, int tp, 
     }
     if (shards && shard_bytes)
         for (auto& R : c->ranks)
-            if (shards[R->index] && shard_bytes[R->index] != c->S)
+            if (shards[R->index] && shard_bytes[R->index] != R->S)
                 return set_error(MPSW_EINVAL, "shard_bytes != S_r of the layout");
     auto m = std::make_unique<Model>();
     m->dims = *dims;
     try {
         for (auto& R : c->ranks) {
-            m->arena.push_back(pin_alloc(c->S, R->numa));
-            if (shards && shards[R->index]) parallel_memcpy(m->arena.back().p, (const uint8_t*)shards[R->index], c->S);
+            m->arena.push_back(pin_alloc(R->S, R->numa));
+            if (shards && shards[R->index]) parallel_memcpy(m->arena.back().p, (const uint8_t*)shards[R->index], R->S);
         }
     } catch (...) {
         for (auto& a : m->arena) pin_free(a);
@@ -1298,7 +1364,7 @@ mpsw_status mpsw_model_arena(mpsw_ctx* c, int model_id, int rank, void** host, u
     const int li = local_index(c, rank);
     if (li < 0) return set_error(MPSW_EINVAL, "rank out of range or not driven by this process");
     if (host) *host = c->models[model_id]->arena[li].p;
-    if (bytes) *bytes = c->S;
+    if (bytes) *bytes = c->ranks[li]->S;
     return MPSW_OK;
     API_END
 }
@@ -1310,7 +1376,8 @@ mpsw_status mpsw_synth_fill(mpsw_ctx* c, int model_id, int rank, uint64_t seed, 
     if (rank != -1 && local_index(c, rank) < 0) return set_error(MPSW_EINVAL, "rank out of range or not local");
     for (auto& R : c->ranks)
         if (rank < 0 || rank == R->index)
-            synth_fill_arena(c->dims, c->tp, R->index, c->cfg.dtype, seed, c->models[model_id]->arena[R->local].p, threads);
+            synth_fill_arena(c->dims, c->tp, c->pp, R->stage, R->trank, c->cfg.dtype, seed,
+                             c->models[model_id]->arena[R->local].p, threads);
     return MPSW_OK;
     API_END
 }
@@ -1376,7 +1443,7 @@ mpsw_status mpsw_wait(mpsw_ctx* c, uint64_t ticket, double timeout_s, double* t_
     if (!e->complete.load()) return set_error(MPSW_ECUDA, "ctx poisoned: " + c->poison_msg);
     if (t_submit) *t_submit = e->t_submit;
     if (t_done_per_rank)
-        for (int r = 0; r < c->tp; ++r) t_done_per_rank[r] = e->t_ack[r];
+        for (int r = 0; r < c->nr; ++r) t_done_per_rank[r] = e->t_ack[r];
     return MPSW_OK;
     API_END
 }
@@ -1395,7 +1462,7 @@ mpsw_status mpsw_entry_gpu_ms(mpsw_ctx* c, uint64_t ticket, int* kind, int* mode
     if (kind) *kind = e->kind;
     if (model_id) *model_id = e->model;
     if (gpu_ms)
-        for (int r = 0; r < c->tp; ++r) {
+        for (int r = 0; r < c->nr; ++r) {
             float ms = 0;
             if (c->local_of[r] >= 0 && e->ev_start[r] && e->ev_done[r])
                 MPSW_CU(cudaEventElapsedTime(&ms, e->ev_start[r], e->ev_done[r]));
@@ -1506,7 +1573,7 @@ mpsw_status mpsw_checksum(mpsw_ctx* c, int model_id, int rank, int on_device, ui
     const int li = local_index(c, rank);
     if (li < 0) return set_error(MPSW_EINVAL, "rank out of range or not driven by this process");
     if (!on_device) {
-        *out = host_checksum(c->models[model_id]->arena[li].p, c->S, 0);
+        *out = host_checksum(c->models[model_id]->arena[li].p, c->ranks[li]->S, 0);
         return MPSW_OK;
     }
     const int slot = resident_slot(c, model_id);
@@ -1514,7 +1581,7 @@ mpsw_status mpsw_checksum(mpsw_ctx* c, int model_id, int rank, int on_device, ui
     Rank& R = *c->ranks[li];
     MPSW_CU(cudaSetDevice(R.device));
     MPSW_CU(cudaMemsetAsync(R.d_sum, 0, 8, R.aux));
-    launch_checksum(R.slots[slot].base, c->S, R.d_sum, R.aux);
+    launch_checksum(R.slots[slot].base, R.S, R.d_sum, R.aux);
     c->launches += 2;
     unsigned long long h = 0;
     MPSW_CU(cudaMemcpyAsync(&h, R.d_sum, 8, cudaMemcpyDeviceToHost, R.aux));
@@ -1529,7 +1596,7 @@ mpsw_status mpsw_peek(mpsw_ctx* c, int model_id, int rank, uint64_t offset, uint
     if (!c || !dst) return set_error(MPSW_EINVAL, "NULL argument");
     if (model_id < 0 || model_id >= (int)c->models.size()) return set_error(MPSW_ENOENT, "unknown model");
     const int li = local_index(c, rank);
-    if (li < 0 || offset + bytes > c->S) return set_error(MPSW_EINVAL, "rank or range");
+    if (li < 0 || offset + bytes > c->ranks[li]->S) return set_error(MPSW_EINVAL, "rank or range");
     const int slot = resident_slot(c, model_id);
     if (slot < 0) return set_error(MPSW_EINVAL, "model not RESIDENT");
     Rank& R = *c->ranks[li];
@@ -1565,7 +1632,7 @@ mpsw_status mpsw_get_stats(mpsw_ctx* c, mpsw_stats* o) {
     o->requests = c->n_requests.load();
     o->rejected = c->rejected.load();
     o->k_slots = c->k;
-    o->shard_bytes = c->S;
+    o->shard_bytes = c->rank_S[0];
     o->fwd_gpu_us_sum = c->fwd_us_sum.load();
     o->fwd_gpu_n = c->fwd_n.load();
     return MPSW_OK;

@@ -42,10 +42,10 @@ struct Layout {
     std::vector<mpsw_tensor_desc> t;
     uint64_t bytes = 0;
 };
-mpsw_status compute_layout(const mpsw_opt_dims& d, int tp, int rank, int dtype, Layout& out);
+mpsw_status compute_layout(const mpsw_opt_dims& d, int tp, int pp, int stage, int rank, int dtype, Layout& out);
 
 // ---------------------------------------------------------------- synthetic fill (C0, product side)
-void synth_fill_arena(const mpsw_opt_dims& d, int tp, int rank, int dtype, uint64_t seed,
+void synth_fill_arena(const mpsw_opt_dims& d, int tp, int pp, int stage, int rank, int dtype, uint64_t seed,
                       uint8_t* dst, int threads);
 uint64_t host_checksum(const uint8_t* p, uint64_t bytes, int threads);
 

@@ -59,10 +59,10 @@ static void run_rows(const Job& j, int es, int r0, int r1) {
     }
 }
 
-void synth_fill_arena(const mpsw_opt_dims& d, int tp, int rank, int dtype, uint64_t seed,
+void synth_fill_arena(const mpsw_opt_dims& d, int tp, int pp, int stage, int rank, int dtype, uint64_t seed,
                       uint8_t* dst, int threads) {
     Layout L;
-    if (compute_layout(d, tp, rank, dtype, L) != MPSW_OK) throw Error(MPSW_EINVAL, tls_error());
+    if (compute_layout(d, tp, pp, stage, rank, dtype, L) != MPSW_OK) throw Error(MPSW_EINVAL, tls_error());
     const int es = dtype == MPSW_BF16 ? 2 : 4;
     std::memset(dst, 0, L.bytes);  // padding is zero (C2)
     // Split every tensor into row blocks; hand blocks to threads round-robin.
@@ -71,7 +71,7 @@ void synth_fill_arena(const mpsw_opt_dims& d, int tp, int rank, int dtype, uint6
     for (size_t tid = 0; tid < L.t.size(); ++tid) {
         const auto& t = L.t[tid];
         Job j{};
-        j.key = seed ^ ((uint64_t)tid << 40);
+        j.key = seed ^ ((uint64_t)t.tensor_id << 40);   // C0 key: id in the full canonical list
         const std::string name(t.name);
         j.gamma = name.find("layer_norm.weight") != std::string::npos;
         j.split = t.split;

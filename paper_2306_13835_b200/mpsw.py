@@ -32,7 +32,7 @@ class Config(C.Structure):
                 ("max_inflight_batches", C.c_int), ("swap_mode", C.c_int), ("chunk_bytes", C.c_uint64),
                 ("writeback", C.c_int), ("trace", C.c_int), ("zc_ctas", C.c_int),
                 ("world_size", C.c_int), ("world_rank", C.c_int), ("shm_name", C.c_char_p),
-                ("gemm_impl", C.c_int)]
+                ("gemm_impl", C.c_int), ("pp", C.c_int)]
 
 
 class OptDims(C.Structure):
@@ -42,7 +42,7 @@ class OptDims(C.Structure):
 
 class TensorDesc(C.Structure):
     _fields_ = [("name", C.c_char * 64), ("offset", C.c_uint64), ("bytes", C.c_uint64), ("rows", C.c_int),
-                ("cols", C.c_int), ("split", C.c_int)]
+                ("cols", C.c_int), ("split", C.c_int), ("tensor_id", C.c_int)]
 
 
 class Stats(C.Structure):
@@ -56,8 +56,8 @@ _P = C.c_void_p
 _SIGS = {
     "mpsw_init": [C.POINTER(Config), C.POINTER(_P)],
     "mpsw_shutdown": [_P],
-    "mpsw_shard_layout": [C.POINTER(OptDims), C.c_int, C.c_int, C.c_int, C.POINTER(TensorDesc), C.c_int,
-                          C.POINTER(C.c_int), C.POINTER(C.c_uint64)],
+    "mpsw_shard_layout": [C.POINTER(OptDims), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(TensorDesc),
+                          C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_uint64)],
     "mpsw_register_model": [_P, C.POINTER(OptDims), C.c_int, C.POINTER(_P), C.POINTER(C.c_uint64),
                             C.POINTER(C.c_int)],
     "mpsw_model_arena": [_P, C.c_int, C.c_int, C.POINTER(_P), C.POINTER(C.c_uint64)],
@@ -123,14 +123,15 @@ def dims_of(d):
     return OptDims(d.n_layers, d.hidden, d.heads, d.ffn, d.vocab, d.max_pos)
 
 
-def shard_layout(dims, tp, rank=0, dtype=BF16):
+def shard_layout(dims, tp, rank=0, dtype=BF16, pp=1, stage=0):
+    """[(name, offset, bytes, rows, cols, split, tensor_id)], shard_bytes of (stage, TP rank)."""
     od = dims_of(dims)
     n = C.c_int()
     sb = C.c_uint64()
-    _check(lib().mpsw_shard_layout(C.byref(od), tp, rank, dtype, None, 0, C.byref(n), C.byref(sb)))
+    _check(lib().mpsw_shard_layout(C.byref(od), tp, pp, stage, rank, dtype, None, 0, C.byref(n), C.byref(sb)))
     arr = (TensorDesc * n.value)()
-    _check(lib().mpsw_shard_layout(C.byref(od), tp, rank, dtype, arr, n.value, C.byref(n), C.byref(sb)))
-    return [(t.name.decode(), t.offset, t.bytes, t.rows, t.cols, t.split) for t in arr], sb.value
+    _check(lib().mpsw_shard_layout(C.byref(od), tp, pp, stage, rank, dtype, arr, n.value, C.byref(n), C.byref(sb)))
+    return [(t.name.decode(), t.offset, t.bytes, t.rows, t.cols, t.split, t.tensor_id) for t in arr], sb.value
 
 
 class Ctx:
@@ -138,17 +139,20 @@ class Ctx:
 
     def __init__(self, device_ids=(0,), budget=1 << 30, max_batch=8, max_tokens=8, dtype=BF16,
                  max_inflight=1, swap_mode=SWAP_AUTO, chunk_bytes=0, writeback=1, trace=0, zc_ctas=0,
-                 world_size=1, world_rank=0, shm_name=None, gemm_impl=0):
-        """Single-process: one ctx over len(device_ids) ranks. Multi-process (world_size > 1):
-        device_ids = (this process's GPU,), rank world_rank of a TP group of world_size."""
+                 world_size=1, world_rank=0, shm_name=None, gemm_impl=0, pp=1):
+        """Single-process: one ctx over len(device_ids) = tp * pp ranks (global rank
+        g = stage * tp + tp_rank). Multi-process (world_size > 1): device_ids = (this process's
+        GPU,), rank world_rank of a TP group of world_size."""
         self._ids = (C.c_int * len(device_ids))(*device_ids)
         self.world_size, self.world_rank = world_size, world_rank
-        self.tp = world_size if world_size > 1 else len(device_ids)
+        self.pp = pp
+        self.nr = world_size if world_size > 1 else len(device_ids)      # ranks (workers)
+        self.tp = self.nr // pp                                            # TP degree
         self.local_ranks = [world_rank] if world_size > 1 else list(range(len(device_ids)))
         self._shm = shm_name.encode() if shm_name else None
         cfg = Config(len(device_ids), self._ids, self.tp, budget, 0, max_batch, max_tokens, dtype,
                      max_inflight, swap_mode, chunk_bytes, writeback, trace, zc_ctas, world_size, world_rank,
-                     self._shm, gemm_impl)
+                     self._shm, gemm_impl, pp)
         h = _P()
         _check(lib().mpsw_init(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -169,15 +173,15 @@ class Ctx:
         self.close()
 
     def register_model(self, dims, shards=None):
-        """shards: list of tp per-rank blobs (entries of non-local ranks may be None)."""
+        """shards: list of nr per-rank blobs in global-rank order (non-local entries may be None)."""
         od = dims_of(dims)
         mid = C.c_int()
         if shards is None:
             _check(lib().mpsw_register_model(self.h, C.byref(od), self.tp, None, None, C.byref(mid)))
         else:
             arrs = [None if s is None else np.ascontiguousarray(s) for s in shards]
-            ptrs = (_P * self.tp)(*[None if a is None else a.ctypes.data for a in arrs])
-            sizes = (C.c_uint64 * self.tp)(*[0 if a is None else a.nbytes for a in arrs])
+            ptrs = (_P * self.nr)(*[None if a is None else a.ctypes.data for a in arrs])
+            sizes = (C.c_uint64 * self.nr)(*[0 if a is None else a.nbytes for a in arrs])
             _check(lib().mpsw_register_model(self.h, C.byref(od), self.tp, ptrs, sizes, C.byref(mid)))
         self.vocab = dims.vocab
         return mid.value
@@ -205,13 +209,13 @@ class Ctx:
     def wait(self, ticket, timeout=-1.0):
         """(t_submit, [t_ack per rank]); on a follower only its own rank's entry is meaningful."""
         ts = C.c_double()
-        td = (C.c_double * self.tp)()
+        td = (C.c_double * self.nr)()
         _check(lib().mpsw_wait(self.h, ticket, timeout, C.byref(ts), td))
         return ts.value, list(td)
 
     def entry_gpu_ms(self, ticket):
         k, m = C.c_int(), C.c_int()
-        ms = (C.c_float * self.tp)()
+        ms = (C.c_float * self.nr)()
         _check(lib().mpsw_entry_gpu_ms(self.h, ticket, C.byref(k), C.byref(m), ms))
         return k.value, m.value, list(ms)
 

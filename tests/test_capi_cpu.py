@@ -28,18 +28,21 @@ def test_exports_every_declared_symbol(M):
         assert hasattr(L, n), n
 
 
-@pytest.mark.parametrize("name,tp", [("tiny", 1), ("tiny", 2), ("tiny", 4), ("opt-125m", 2), ("opt-13b", 4),
-                                     ("opt-30b", 8), ("opt-1.3b", 2)])
+@pytest.mark.parametrize("name,tp,pp", [("tiny", 1, 1), ("tiny", 2, 1), ("tiny", 4, 1), ("opt-125m", 2, 1),
+                                        ("opt-13b", 4, 1), ("opt-30b", 8, 1), ("opt-1.3b", 2, 1), ("tiny", 2, 2),
+                                        ("opt-13b", 2, 4), ("opt-125m", 1, 3)])
 @pytest.mark.parametrize("dtype", [0, 1])
-def test_layout_matches_oracle(M, name, tp, dtype):
+def test_layout_matches_oracle(M, name, tp, pp, dtype):
     d = opt_dims(name)
-    ours, sb = M.shard_layout(d, tp, tp - 1, dtype)
-    placed, total = OL.arena_layout(d, tp, tp - 1, "bf16" if dtype == 0 else "fp32")
-    assert sb == total
-    assert len(ours) == len(placed)
-    for (nm, off, nb, rows, cols, split), p in zip(ours, placed):
-        assert nm == p.spec.name and off == p.offset and nb == p.nbytes and split == p.spec.split
-        assert (rows, cols) == (p.shape if len(p.shape) == 2 else (p.shape[0], 1))
+    for stage in range(pp):
+        ours, sb = M.shard_layout(d, tp, tp - 1, dtype, pp, stage)
+        placed, total = OL.arena_layout(d, tp, tp - 1, "bf16" if dtype == 0 else "fp32", pp, stage)
+        assert sb == total
+        assert len(ours) == len(placed)
+        for (nm, off, nb, rows, cols, split, tid), p in zip(ours, placed):
+            assert nm == p.spec.name and off == p.offset and nb == p.nbytes and split == p.spec.split
+            assert tid == p.spec.tid
+            assert (rows, cols) == (p.shape if len(p.shape) == 2 else (p.shape[0], 1))
 
 
 def test_layout_errors(M):
@@ -48,6 +51,10 @@ def test_layout_errors(M):
     assert e.value.status == M.EINVAL
     with pytest.raises(M.MpswError):
         M.shard_layout(opt_dims("tiny"), 2, rank=2)
+    with pytest.raises(M.MpswError):
+        M.shard_layout(opt_dims("opt-13b"), 1, pp=3)      # 40 layers
+    with pytest.raises(M.MpswError):
+        M.shard_layout(opt_dims("tiny"), 1, pp=2, stage=2)
 
 
 def test_init_without_gpu_fails_cleanly(M):

@@ -85,3 +85,27 @@ def test_alignment_and_padding_zero():
 def test_invalid_tp():
     with pytest.raises(ValueError):
         layout.arena_layout(opt_dims("opt-125m"), 8, 0)   # 12 heads
+
+
+@pytest.mark.parametrize("pp", [1, 2])
+def test_pp_stages_partition_layers(pp):
+    """Every layer tensor is held by exactly one stage; embed_tokens by the first and the last
+    stage (tied lm_head), positions by the first, the final LN by the last."""
+    d = opt_dims("tiny")
+    holders = {}
+    for st in range(pp):
+        for p in layout.arena_layout(d, 1, 0, "bf16", pp, st)[0]:
+            holders.setdefault(p.spec.name, []).append(st)
+    for s in layout.canonical_tensors(d):
+        h = holders[s.name]
+        if s.name == "decoder.embed_tokens.weight":
+            assert h == sorted({0, pp - 1})
+        elif s.name == "decoder.embed_positions.weight":
+            assert h == [0]
+        elif s.name.startswith("decoder.final_layer_norm"):
+            assert h == [pp - 1]
+        else:
+            assert len(h) == 1 and h[0] == int(s.name.split(".")[2]) // (d.n_layers // pp)
+    total = sum(layout.shard_bytes(d, 1, "bf16", pp, st) for st in range(pp))
+    emb = layout.arena_layout(d, 1, 0)[0][0].nbytes
+    assert total == layout.shard_bytes(d, 1) + (emb if pp > 1 else 0)
