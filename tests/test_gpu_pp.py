@@ -17,10 +17,10 @@ def budget_for(d, tp, pp, k=1):
     return k * max((layout.shard_bytes(d, tp, "bf16", pp, st) + 4095) // 4096 * 4096 for st in range(pp))
 
 
-@pytest.mark.parametrize("tp,pp", [(1, 2), (2, 2), (1, 3)])
-def test_pp_swap_and_logits(tp, pp):
+@pytest.mark.parametrize("tp,pp,name", [(1, 2, "mid"), (2, 2, "mid"), (1, 3, "small"), (1, 4, "mid")])
+def test_pp_swap_and_logits(tp, pp, name):
     M = need_gpu()
-    d = opt_dims("small")
+    d = opt_dims(name)
     with M.Ctx(device_ids=(0,) * (tp * pp), pp=pp, budget=budget_for(d, tp, pp), max_batch=4, max_tokens=8) as ctx:
         assert ctx.tp == tp and ctx.nr == tp * pp
         m = ctx.register_model(d)
@@ -61,7 +61,7 @@ def test_pp_matches_no_pp_bitwise():
 
 def test_pp_engine_replay(tmp_path):
     M = need_gpu()
-    d = opt_dims("small")
+    d = opt_dims("mid")
     tp, pp = 2, 2
     reqs = alternating_blocking(8, 0, 4, d.vocab)
     with M.Ctx(device_ids=(0,) * 4, pp=pp, budget=budget_for(d, tp, pp), max_batch=2, max_tokens=8, trace=1) as ctx:
