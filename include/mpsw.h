@@ -168,7 +168,8 @@ mpsw_status mpsw_request(mpsw_ctx* ctx, int model_id, const int32_t* tokens, int
                          float* logits_out, int64_t* request_id);
 
 /* OK once the request's logits are in logits_out (t_arrival, t_done in engine seconds);
- * EAGAIN while pending; ENOENT unknown id. */
+ * EAGAIN while pending; ENOENT unknown id. The id is released after the first OK (a later
+ * poll/wait of the same id returns ENOENT). */
 mpsw_status mpsw_poll(mpsw_ctx* ctx, int64_t request_id, double* t_arrival, double* t_done);
 
 /* Blocking variant of mpsw_poll (timeout_s < 0 = forever). */

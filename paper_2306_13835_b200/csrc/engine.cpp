@@ -209,6 +209,7 @@ struct Entry {
     std::atomic<int> issued[kMaxRanks];
     int acked[kMaxRanks] = {};
     double t_ack[kMaxRanks] = {};
+    float gpu_ms[kMaxRanks] = {};                // device span per local rank, kept after events die
     int n_acked = 0;
     std::atomic<int> complete{0};
     Entry() {
@@ -700,6 +701,18 @@ void complete_batch(mpsw_ctx* c, Entry& e, double now) {
     c->done_cv.notify_all();
 }
 
+// Device span of a finished swap entry on every local rank; then its events are released (a
+// long run would otherwise keep 2 events per rank per swap).
+void finish_swap_events(mpsw_ctx* c, Entry& e) {
+    for (int r = 0; r < c->nr; ++r) {
+        if (e.ev_start[r] && e.ev_done[r] && cudaEventElapsedTime(&e.gpu_ms[r], e.ev_start[r], e.ev_done[r]) != cudaSuccess)
+            e.gpu_ms[r] = 0;
+        cudaGetLastError();
+        if (e.ev_start[r]) cudaEventDestroy(e.ev_start[r]), e.ev_start[r] = nullptr;
+        if (e.ev_done[r]) cudaEventDestroy(e.ev_done[r]), e.ev_done[r] = nullptr;
+    }
+}
+
 // Device time of a finished batch's forward on the first local rank (stats), then free its events.
 void record_fwd_time(mpsw_ctx* c, Entry& e) {
     const int r0 = c->ranks[0]->index;
@@ -759,6 +772,7 @@ bool poll_inflight(mpsw_ctx* c) {
                 record_fwd_time(c, e);
             } else {
                 (e.kind == E_LOAD ? c->swaps_in : c->swaps_out)++;
+                finish_swap_events(c, e);
                 std::lock_guard<std::mutex> lk(c->done_mu);
                 e.complete.store(1, std::memory_order_release);
             }
@@ -894,6 +908,7 @@ void follower_main(mpsw_ctx* c) {
                     (e.kind == E_LOAD ? c->swaps_in : c->swaps_out)++;
                     if (e.kind == E_LOAD) c->h2d_bytes += R.S;
                     else if (c->cfg.writeback) c->d2h_bytes += R.S;
+                    finish_swap_events(c, e);
                     std::lock_guard<std::mutex> lk(c->done_mu);
                     e.complete.store(1, std::memory_order_release);
                 }
@@ -1462,12 +1477,7 @@ mpsw_status mpsw_entry_gpu_ms(mpsw_ctx* c, uint64_t ticket, int* kind, int* mode
     if (kind) *kind = e->kind;
     if (model_id) *model_id = e->model;
     if (gpu_ms)
-        for (int r = 0; r < c->nr; ++r) {
-            float ms = 0;
-            if (c->local_of[r] >= 0 && e->ev_start[r] && e->ev_done[r])
-                MPSW_CU(cudaEventElapsedTime(&ms, e->ev_start[r], e->ev_done[r]));
-            gpu_ms[r] = ms;   // 0 for ranks driven by other processes
-        }
+        for (int r = 0; r < c->nr; ++r) gpu_ms[r] = e->gpu_ms[r];   // 0 for ranks of other processes
     return MPSW_OK;
     API_END
 }
@@ -1503,6 +1513,12 @@ mpsw_status mpsw_request(mpsw_ctx* c, int model_id, const int32_t* tokens, int n
     API_END
 }
 
+// A completed request is released once the caller has observed it (poll/wait returned OK).
+static void forget_req(mpsw_ctx* c, int64_t rid) {
+    std::lock_guard<std::mutex> lk(c->cmd_mu);
+    c->reqs.erase(rid);
+}
+
 static std::shared_ptr<ReqRec> find_req(mpsw_ctx* c, int64_t rid) {
     std::lock_guard<std::mutex> lk(c->cmd_mu);
     auto it = c->reqs.find(rid);
@@ -1520,6 +1536,7 @@ mpsw_status mpsw_poll(mpsw_ctx* c, int64_t rid, double* t_arrival, double* t_don
     }
     if (t_arrival) *t_arrival = rq->t_arr;
     if (t_done) *t_done = rq->t_done;
+    forget_req(c, rid);
     return MPSW_OK;
     API_END
 }
@@ -1537,6 +1554,8 @@ mpsw_status mpsw_wait_request(mpsw_ctx* c, int64_t rid, double timeout_s, double
     if (!rq->done.load()) return set_error(MPSW_ECUDA, "ctx poisoned: " + c->poison_msg);
     if (t_arrival) *t_arrival = rq->t_arr;
     if (t_done) *t_done = rq->t_done;
+    lk.unlock();
+    forget_req(c, rid);
     return MPSW_OK;
     API_END
 }

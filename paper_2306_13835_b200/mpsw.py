@@ -159,6 +159,7 @@ class Ctx:
         self.dtype = dtype
         self.vocab = None
         self._live = {}          # request id -> output array the library writes into (kept alive)
+        self._done = {}          # request id -> (t_arrival, t_done); the library releases ids on OK
 
     def close(self):
         if self.h:
@@ -233,17 +234,23 @@ class Ctx:
 
     def poll(self, rid):
         a, d = C.c_double(), C.c_double()
+        if rid in self._done:
+            return self._done[rid]
         st = lib().mpsw_poll(self.h, rid, C.byref(a), C.byref(d))
         if st == EAGAIN:
             return None
         _check(st)
         self._live.pop(rid, None)
+        self._done[rid] = (a.value, d.value)
         return a.value, d.value
 
     def wait_request(self, rid, timeout=-1.0):
+        if rid in self._done:
+            return self._done[rid]
         a, d = C.c_double(), C.c_double()
         _check(lib().mpsw_wait_request(self.h, rid, timeout, C.byref(a), C.byref(d)))
         self._live.pop(rid, None)
+        self._done[rid] = (a.value, d.value)
         return a.value, d.value
 
     def checksum(self, model_id, rank, on_device=True):
