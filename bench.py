@@ -227,11 +227,14 @@ def run_ours(args, rank, world):
         rid, _ = ctx.request(ids[r.model], r.tokens, out)
         return rid, ctx.wait_request(rid, 600)
 
+    # CPU (gloo) barriers for the long waits of the followers: an NCCL barrier would park a
+    # spinning kernel on every follower GPU while rank 0 drives the requests
+    cpu_group = dist.new_group(backend="gloo") if world > 1 else None
     if rank == 0:
         for r in reqs[:args.warmup]:
             one(r)
     if world > 1:
-        dist.barrier()
+        dist.barrier(group=cpu_group)
     torch.cuda.synchronize()
     st0 = ctx.stats()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -245,7 +248,7 @@ def run_ours(args, rank, world):
                 _, (ta, td) = one(r)
                 lat.append(td - ta)
         if world > 1:
-            dist.barrier()
+            dist.barrier(group=cpu_group)
         wall = time.perf_counter() - w0
         torch.cuda.synchronize()
         e1.record()
@@ -271,7 +274,7 @@ def run_ours(args, rank, world):
         tdev = "cuda" if dist.get_backend() == "nccl" else None
         h2d_ms = max_over_ranks(h2d_ms, device=tdev)
         dev_s = max_over_ranks([dev_s], device=tdev)[0]
-        dist.barrier()
+        dist.barrier(group=cpu_group)
     ctx.close()
     return {
         "h2d_ms": h2d_ms, "swapin_lat_s": swapin_lat, "req_lat_s": lat, "dev_s": dev_s, "wall_s": wall,
