@@ -52,7 +52,8 @@ typedef enum {
 } mpsw_status;
 
 enum { MPSW_BF16 = 0, MPSW_FP32 = 1 };                                 /* parameter/compute dtype */
-enum { MPSW_SWAP_AUTO = 0, MPSW_SWAP_COPY_ENGINE = 1, MPSW_SWAP_ZERO_COPY = 2 };
+enum { MPSW_SWAP_AUTO = 0, MPSW_SWAP_COPY_ENGINE = 1, MPSW_SWAP_ZERO_COPY = 2,
+       MPSW_SWAP_HYBRID = 3 /* ablation: CE head + zero-copy tail of one shard concurrently */ };
 enum { MPSW_EVICTED = 0, MPSW_LOADING = 1, MPSW_RESIDENT = 2, MPSW_OFFLOADING = 3 };
 
 typedef struct mpsw_ctx mpsw_ctx;   /* opaque; owns arenas, slots, streams, threads */
@@ -67,7 +68,7 @@ typedef struct {
     int max_tokens;               /* tokens per request, 1..128 (P:138 uses 2, P:166 uses 8)   */
     int dtype;                    /* MPSW_BF16 (1e-2 parity) or MPSW_FP32 (1e-5 parity)        */
     int max_inflight_batches;     /* D per TP group (reading #26); 0 => 1            */
-    int swap_mode;                /* MPSW_SWAP_*: copy engine, zero-copy kernel, or auto       */
+    int swap_mode;                /* MPSW_SWAP_*: copy engine, zero-copy kernel, auto, hybrid  */
     uint64_t chunk_bytes;         /* swap chunk c (multiple of 4096); 0 => 64 MiB              */
     int writeback;                /* 1 = offload copies the slot back to the arena      */
     int trace;                    /* 1 = record the NDJSON event/decision trace                */

@@ -237,6 +237,8 @@ struct Rank {
     cudaEvent_t ev_stage = nullptr;        // PP: residual stream of this stage is ready
     std::atomic<uint64_t> stage_out{0};    // PP: id+1 of the last batch whose ev_stage is recorded
     cudaStream_t compute = nullptr, h2d = nullptr, d2h = nullptr, aux = nullptr;
+    cudaStream_t h2d_zc = nullptr;         // hybrid swap: the zero-copy share of a swap-in
+    cudaEvent_t ev_zc = nullptr;
     uint8_t* region = nullptr;             // param budget (one cudaMalloc)
     std::vector<Slot> slots;
     uint8_t* ws_base = nullptr;
@@ -378,6 +380,14 @@ void group_barrier(mpsw_ctx* c, int stage = 0) {
     }
 }
 
+double hybrid_frac() {
+    static double f = [] {
+        const char* e = getenv("MPSW_HYBRID_FRAC");
+        return e ? atof(e) : 0.15;
+    }();
+    return f;
+}
+
 bool use_zero_copy(mpsw_ctx* c, uint64_t bytes) {
     if (c->cfg.swap_mode == MPSW_SWAP_ZERO_COPY) return true;
     if (c->cfg.swap_mode == MPSW_SWAP_COPY_ENGINE) return false;
@@ -408,7 +418,22 @@ void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
     // gates that already completed are skipped (a stream wait on another stream's event costs
     // tens of microseconds, which dominates small-shard swaps: DESIGN.md §8 cfg5)
     if (sl.whole_gate_valid && !event_done(sl.whole_gate)) MPSW_CU(cudaStreamWaitEvent(R.h2d, sl.whole_gate, 0));
-    if (!sl.chunk_gate_valid && zc) {
+    if (c->cfg.swap_mode == 3 && !sl.chunk_gate_valid && R.S >= (64ull << 20)) {
+        // HYBRID: the copy engine moves the head of the shard while the zero-copy kernel pulls
+        // the tail over the same link from the SMs (two independent PCIe read requesters)
+        const double f = hybrid_frac();
+        const uint64_t zc_bytes = ((uint64_t)(R.S * f) + 4095) / 4096 * 4096;
+        const uint64_t ce_bytes = R.S - zc_bytes;
+        MPSW_CU(cudaEventRecord(R.ev_zc, R.h2d));
+        MPSW_CU(cudaStreamWaitEvent(R.h2d_zc, R.ev_zc, 0));
+        launch_zero_copy(sl.base + ce_bytes, src + ce_bytes, zc_bytes, zc_ctas(c), R.h2d_zc);
+        c->launches++;
+        for (uint64_t off = 0; off < ce_bytes; off += c->chunk)
+            MPSW_CU(cudaMemcpyAsync(sl.base + off, src + off, std::min<uint64_t>(c->chunk, ce_bytes - off),
+                                    cudaMemcpyHostToDevice, R.h2d));
+        MPSW_CU(cudaEventRecord(R.ev_zc, R.h2d_zc));
+        MPSW_CU(cudaStreamWaitEvent(R.h2d, R.ev_zc, 0));
+    } else if (!sl.chunk_gate_valid && zc) {
         launch_zero_copy(sl.base, src, R.S, zc_ctas(c), R.h2d);
         c->launches++;
     } else {
@@ -1143,7 +1168,7 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     if (cfg->max_tokens < 1 || cfg->max_tokens > 128) return set_error(MPSW_EINVAL, "max_tokens must be 1..128");
     if (cfg->dtype != MPSW_BF16 && cfg->dtype != MPSW_FP32) return set_error(MPSW_EINVAL, "bad dtype");
     if (cfg->chunk_bytes % 4096) return set_error(MPSW_EINVAL, "chunk_bytes must be a multiple of 4096");
-    if (cfg->swap_mode < 0 || cfg->swap_mode > 2) return set_error(MPSW_EINVAL, "bad swap_mode");
+    if (cfg->swap_mode < 0 || cfg->swap_mode > 3) return set_error(MPSW_EINVAL, "bad swap_mode");
     if (cfg->param_budget_bytes_per_gpu == 0) return set_error(MPSW_EINVAL, "param budget is 0");
     if (cfg->gemm_impl < 0 || cfg->gemm_impl > 2) return set_error(MPSW_EINVAL, "bad gemm_impl");
     int ndev = 0;
@@ -1192,6 +1217,8 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
         MPSW_CU(cudaStreamCreateWithFlags(&R->h2d, cudaStreamNonBlocking));
         MPSW_CU(cudaStreamCreateWithFlags(&R->d2h, cudaStreamNonBlocking));
         MPSW_CU(cudaStreamCreateWithFlags(&R->aux, cudaStreamNonBlocking));
+        MPSW_CU(cudaStreamCreateWithFlags(&R->h2d_zc, cudaStreamNonBlocking));
+        MPSW_CU(cudaEventCreateWithFlags(&R->ev_zc, cudaEventDisableTiming));
         cudaError_t e = cudaMalloc(&R->region, cfg->param_budget_bytes_per_gpu);
         if (e != cudaSuccess) {
             cudaGetLastError();
@@ -1295,6 +1322,8 @@ mpsw_status mpsw_shutdown(mpsw_ctx* c) {
         cudaStreamDestroy(R->h2d);
         cudaStreamDestroy(R->d2h);
         cudaStreamDestroy(R->aux);
+        cudaStreamDestroy(R->h2d_zc);
+        cudaEventDestroy(R->ev_zc);
     }
     for (auto& kv : c->entries)
         for (int r = 0; r < c->nr; ++r) {

@@ -14,7 +14,7 @@ OK, EINVAL, ENOMEM, EBUSY, ENOENT, EAGAIN, ECUDA, ENCCL, EINVARIANT, ETIMEDOUT =
 STATUS_NAMES = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "EBUSY", -4: "ENOENT", -5: "EAGAIN", -6: "ECUDA",
                 -7: "ENCCL", -8: "EINVARIANT", -9: "ETIMEDOUT"}
 BF16, FP32 = 0, 1
-SWAP_AUTO, SWAP_COPY_ENGINE, SWAP_ZERO_COPY = 0, 1, 2
+SWAP_AUTO, SWAP_COPY_ENGINE, SWAP_ZERO_COPY, SWAP_HYBRID = 0, 1, 2, 3
 EVICTED, LOADING, RESIDENT, OFFLOADING = 0, 1, 2, 3
 NOOP_TICKET = (1 << 64) - 1
 
