@@ -320,7 +320,6 @@ struct mpsw_ctx {
     std::unordered_map<int64_t, std::shared_ptr<mpsw::ReqRec>> reqs;
     std::atomic<int64_t> next_rid{0};
     int ring_next = 0;
-    mpsw::SpinBarrier barrier;
     std::mutex api_mu;
     // follower-local view of residency (mp followers)
     std::vector<int> f_slot_of;
@@ -1193,7 +1192,6 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     c->sm.tp = c->nr;              // acks per entry: one per worker
     c->sm.max_batch = cfg->max_batch;
     c->sm.D = c->D;
-    c->barrier.n = mp ? 1 : c->tp;
     for (auto& b : c->stage_barrier) b.n = mp ? 1 : c->tp;
     c->models.reserve(kMaxModels);
     for (auto& x : c->local_of) x = -1;

@@ -418,8 +418,6 @@ static int tc_grid(int tiles, int K) {
     return (int)std::min<uint64_t>(units, 2 * (uint64_t)sm_count());
 }
 
-int tc_split_k(int n_total, int K) { return tc_grid((n_total + kBN - 1) / kBN, K); }
-
 size_t tc_partial_floats(int n_total, int K, int Mp) {
     return (size_t)tc_grid((n_total + kBN - 1) / kBN, K) * 2 * kBN * Mp;
 }

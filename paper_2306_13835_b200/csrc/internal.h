@@ -95,7 +95,6 @@ size_t workspace_bytes(const FwdShape& s, int max_rows, int max_batch);
 void workspace_carve(FwdWorkspace& w, const FwdShape& s, int max_rows, int max_batch, void* base);
 
 // tcgen05/TMA weight-streaming GEMM (gemm_tc.cu)
-int tc_split_k(int n_total, int K);
 size_t tc_partial_floats(int n_total, int K, int Mp);
 bool tc_supported(int M, int K);
 void tc_gemm(const void* const* W, const void* const* bias, const int* N, const float* scale, const int* out_col0,

@@ -97,3 +97,21 @@ def test_alternating_blocking_every_request_swaps(tmp_path):
     events, decisions = replay_check(p, 2, 1, 1, 8, 1)
     assert st["swaps_in"] == 10 and st["swaps_out"] == 9
     assert sum(1 for x in decisions if x["dec"] == "offload") == 9
+
+
+def test_request_id_released_after_ok():
+    """mpsw_poll / mpsw_wait_request release the id after the first OK (include/mpsw.h)."""
+    import ctypes as C
+    M = need_gpu()
+    d = opt_dims("small")
+    with M.Ctx(device_ids=(0,), budget=layout.shard_bytes(d, 1) + 4096) as ctx:
+        m = ctx.register_model(d)
+        ctx.synth_fill(m, 1)
+        rid, out = ctx.request(m, np.array([3, 4], np.int32))
+        ctx.wait_request(rid, 60)
+        a, b = C.c_double(), C.c_double()
+        assert M.lib().mpsw_poll(ctx.h, rid, C.byref(a), C.byref(b)) == M.ENOENT
+        assert ctx.poll(rid) is not None          # the binding keeps the observed result
+        with pytest.raises(M.MpswError) as e:
+            ctx.wait(123456)
+        assert e.value.status == M.ENOENT
