@@ -104,3 +104,55 @@ def test_full_size_opt13b_tp2_batch_invariance():
     tp1, _ = run_requests(M, d, 1, M.BF16, 1001, toks, max_batch=4)
     for a, b in zip(tp1, tp2_batched):
         assert forward.rel_l2(b, a) < 1e-2
+
+
+def test_max_tokens_and_max_rows():
+    """Edge sizes: L = 128 (attention maximum) and a full 32 x 8 batch (M = 256: the MMA N = 256
+    single-buffered-accumulator path), logits vs the oracle."""
+    M = need_gpu()
+    d = opt_dims("mid")
+    long_tok = [request_tokens(11, 0, 0, 128, d.vocab)]
+    outs, _ = run_requests(M, d, 1, M.BF16, 31, long_tok, max_batch=1)
+    W = layout.full_tensors(d, 31)
+    ref = forward.forward_bf16_emulated(d, W, long_tok[0][None])[0]
+    assert forward.rel_l2(outs[0], ref) < 1e-2
+    toks = [request_tokens(12, 0, i, 8, d.vocab) for i in range(32)]
+    S_ = layout.shard_bytes(d, 1)
+    with M.Ctx(device_ids=(0,), budget=S_ + 4096, max_batch=32, max_tokens=8) as ctx:
+        m = ctx.register_model(d)
+        ctx.synth_fill(m, 31)
+        ctx.wait(ctx.swap_in(m))
+        rids = [ctx.request(m, t) for t in toks]
+        for rid, _ in rids:
+            ctx.wait_request(rid, 120)
+        st = ctx.stats()
+    assert st["batches"] <= 3                       # most requests share one M = 248..256 batch
+    for t, (_, y) in list(zip(toks, rids))[::5]:
+        ref = forward.forward_bf16_emulated(d, W, t[None])[0]
+        assert forward.rel_l2(y, ref) < 1e-2
+
+
+@pytest.mark.slow
+def test_full_size_opt30b_tp8_logits_parity():
+    """cfg4's model at its TP degree (OPT-30B, TP8 as 8 virtual ranks on one B200; 7.5 GB per
+    rank): request logits vs the oracle streamed layer by layer."""
+    M = need_gpu()
+    d = opt_dims("opt-30b")
+    toks = [request_tokens(13, 0, 0, 8, d.vocab)]
+    outs, _ = run_requests(M, d, 8, M.BF16, 2000, toks, max_batch=1)
+    ref = forward.forward_bf16_emulated(d, layout.LazyFull(d, 2000), toks[0][None])[0]
+    assert forward.rel_l2(outs[0], ref) < 1e-2
+    assert int(np.argmax(outs[0])) == int(np.argmax(ref))
+
+
+@pytest.mark.slow
+def test_full_size_opt1_3b_tp2_vs_oracle():
+    """cfg2 at full size (OPT-1.3B TP2 (virtual ranks): logits vs the oracle."""
+    M = need_gpu()
+    d = opt_dims("opt-1.3b")
+    toks = [request_tokens(14, 0, i, 8, d.vocab) for i in range(4)]
+    outs, _ = run_requests(M, d, 2, M.BF16, 2001, toks, max_batch=8)
+    W = layout.LazyFull(d, 2001)
+    for t, y in zip(toks, outs):
+        ref = forward.forward_bf16_emulated(d, W, t[None])[0]
+        assert forward.rel_l2(y, ref) < 1e-2
