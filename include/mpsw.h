@@ -79,6 +79,9 @@ typedef struct {
     int gemm_impl;                /* 0 auto (tcgen05/TMA for bf16, M <= 256), 1 SIMT, 2 tcgen05 */
     int pp;                       /* pipeline stages (0/1 = none); ranks = tp * pp, global rank  */
                                   /* g = stage * tp + tp_rank; single-process only; needs D = 1  */
+    const int* helper_device_ids; /* NVLink fan-in (NEXT-2; single process): GPUs whose PCIe    */
+    int n_helpers;                /* links also pull chunks of every swap-in and forward them   */
+                                  /* to the owner over NVLink; 0 = off (copy-engine mode only)  */
 } mpsw_config;
 
 typedef struct { int n_layers, hidden, heads, ffn, vocab, max_pos; } mpsw_opt_dims;

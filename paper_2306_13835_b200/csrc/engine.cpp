@@ -52,6 +52,7 @@ namespace {
 constexpr uint64_t kNoopTicket = ~0ull;
 constexpr uint64_t kSlotAlign = 4096;
 constexpr int kMaxRanks = 8;
+constexpr int kMaxHelpers = 8;
 constexpr size_t kMaxModels = 4096;
 
 // ----------------------------------------------------------------------------- pinned store
@@ -210,6 +211,7 @@ struct Entry {
     int acked[kMaxRanks] = {};
     double t_ack[kMaxRanks] = {};
     float gpu_ms[kMaxRanks] = {};                // device span per local rank, kept after events die
+    cudaEvent_t ev_helper[kMaxRanks][kMaxHelpers] = {};   // fan-in: helper h done with rank r's chunks
     int n_acked = 0;
     std::atomic<int> complete{0};
     Entry() {
@@ -225,6 +227,19 @@ struct Slot {
     bool chunk_gate_valid = false;
     cudaEvent_t whole_gate = nullptr;      // clean eviction: last forward that read the slot
     bool whole_gate_valid = false;
+};
+
+// NVLink-assisted fan-in (NEXT-2): a helper GPU's own PCIe link pulls chunks of another rank's
+// shard into a 2-chunk staging ring in its HBM, then forwards each chunk to the owner's slot with
+// a peer copy over NVLink. Helpers are shared by all rank worker threads (mutex).
+struct Helper {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint8_t* staging = nullptr;            // 2 * chunk bytes
+    cudaEvent_t free_ev[2] = {nullptr, nullptr};
+    bool free_valid[2] = {false, false};
+    int next = 0;
+    std::mutex mu;
 };
 
 struct Rank {
@@ -281,6 +296,7 @@ struct mpsw_ctx {
     int world_rank = 0;
     uint64_t chunk = 64ull << 20;
     std::vector<std::unique_ptr<mpsw::Rank>> ranks;     // LOCAL ranks
+    std::vector<std::unique_ptr<mpsw::Helper>> helpers; // fan-in helper GPUs (single process)
     int local_of[mpsw::kMaxRanks];                        // global rank -> local index or -1
     std::vector<std::unique_ptr<mpsw::Model>> models;
     // geometry (fixed by the first registered model; homogeneous slots)
@@ -435,6 +451,41 @@ void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
     } else if (!sl.chunk_gate_valid && zc) {
         launch_zero_copy(sl.base, src, R.S, zc_ctas(c), R.h2d);
         c->launches++;
+    } else if (!c->helpers.empty() && !zc && R.n_chunks > 1) {
+        // fan-in: chunk i goes over link (i mod (1 + helpers)); lane 0 is the owner's own link
+        const int lanes = 1 + (int)c->helpers.size();
+        for (int i = 0; i < R.n_chunks; ++i) {
+            const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, R.S - off);
+            const int lane = i % lanes;
+            cudaEvent_t gate = sl.chunk_gate_valid && !event_done(sl.chunk_gate[i]) ? sl.chunk_gate[i] : nullptr;
+            if (lane == 0) {
+                if (gate) MPSW_CU(cudaStreamWaitEvent(R.h2d, gate, 0));
+                MPSW_CU(cudaMemcpyAsync(sl.base + off, src + off, n, cudaMemcpyHostToDevice, R.h2d));
+                continue;
+            }
+            Helper& H = *c->helpers[lane - 1];
+            std::lock_guard<std::mutex> lk(H.mu);
+            MPSW_CU(cudaSetDevice(H.device));
+            if (i == lane) {                   // first chunk of this load on this helper
+                MPSW_CU(cudaStreamWaitEvent(H.stream, e.ev_start[r], 0));
+                if (sl.whole_gate_valid && !event_done(sl.whole_gate))
+                    MPSW_CU(cudaStreamWaitEvent(H.stream, sl.whole_gate, 0));
+            }
+            if (gate) MPSW_CU(cudaStreamWaitEvent(H.stream, gate, 0));
+            const int j = H.next;
+            H.next ^= 1;
+            if (H.free_valid[j]) MPSW_CU(cudaStreamWaitEvent(H.stream, H.free_ev[j], 0));
+            uint8_t* stg = H.staging + (uint64_t)j * c->chunk;
+            MPSW_CU(cudaMemcpyAsync(stg, src + off, n, cudaMemcpyHostToDevice, H.stream));
+            MPSW_CU(cudaMemcpyPeerAsync(sl.base + off, R.device, stg, H.device, n, H.stream));
+            MPSW_CU(cudaEventRecord(H.free_ev[j], H.stream));
+            H.free_valid[j] = true;
+            if (!e.ev_helper[r][lane - 1]) MPSW_CU(cudaEventCreateWithFlags(&e.ev_helper[r][lane - 1], cudaEventDisableTiming));
+            MPSW_CU(cudaEventRecord(e.ev_helper[r][lane - 1], H.stream));
+            MPSW_CU(cudaSetDevice(R.device));
+        }
+        for (int h = 0; h < (int)c->helpers.size(); ++h)
+            if (e.ev_helper[r][h]) MPSW_CU(cudaStreamWaitEvent(R.h2d, e.ev_helper[r][h], 0));
     } else {
         for (int i = 0; i < R.n_chunks; ++i) {
             const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, R.S - off);
@@ -734,6 +785,8 @@ void finish_swap_events(mpsw_ctx* c, Entry& e) {
         cudaGetLastError();
         if (e.ev_start[r]) cudaEventDestroy(e.ev_start[r]), e.ev_start[r] = nullptr;
         if (e.ev_done[r]) cudaEventDestroy(e.ev_done[r]), e.ev_done[r] = nullptr;
+        for (auto& ev : e.ev_helper[r])
+            if (ev) cudaEventDestroy(ev), ev = nullptr;
     }
 }
 
@@ -1225,6 +1278,34 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
         MPSW_CU(cudaMalloc(&R->d_sum, sizeof(unsigned long long)));
         c->ranks.push_back(std::move(R));
     }
+    if (cfg->n_helpers < 0 || cfg->n_helpers > kMaxHelpers || (cfg->n_helpers && !cfg->helper_device_ids))
+        return set_error(MPSW_EINVAL, "n_helpers must be 0..8 with helper_device_ids");
+    if (mp && cfg->n_helpers) return set_error(MPSW_EINVAL, "fan-in helpers are single-process only");
+    for (int h = 0; h < cfg->n_helpers; ++h) {
+        const int dev = cfg->helper_device_ids[h];
+        if (dev < 0 || dev >= ndev) return set_error(MPSW_EINVAL, "helper device id out of range");
+        auto H = std::make_unique<Helper>();
+        H->device = dev;
+        MPSW_CU(cudaSetDevice(dev));
+        MPSW_CU(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
+        cudaError_t e = cudaMalloc(&H->staging, 2 * c->chunk);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return set_error(MPSW_ENOMEM, "cudaMalloc(fan-in staging)");
+        }
+        for (auto& ev : H->free_ev) MPSW_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        for (int r = 0; r < c->nr; ++r) {      // helper <-> owner peer access (NVLink)
+            const int od = c->device_ids[r];
+            if (od == dev) continue;
+            int ok = 0;
+            cudaDeviceCanAccessPeer(&ok, dev, od);
+            if (!ok) return set_error(MPSW_EINVAL, "helper GPU lacks peer access to a rank's GPU");
+            cudaError_t pe = cudaDeviceEnablePeerAccess(od, 0);
+            if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) MPSW_CU(pe);
+            cudaGetLastError();
+        }
+        c->helpers.push_back(std::move(H));
+    }
     if (!mp) {
         // peer access between distinct devices of the group (TP all-reduce reads peer partials)
         for (int a = 0; a < c->nr; ++a)
@@ -1299,6 +1380,13 @@ mpsw_status mpsw_shutdown(mpsw_ctx* c) {
     for (auto& R : c->ranks) {
         cudaSetDevice(R->device);
         cudaDeviceSynchronize();
+    }
+    for (auto& H : c->helpers) {
+        cudaSetDevice(H->device);
+        cudaStreamSynchronize(H->stream);
+        cudaStreamDestroy(H->stream);
+        cudaFree(H->staging);
+        for (auto ev : H->free_ev) cudaEventDestroy(ev);
     }
     for (auto p : c->ipc_mem_opened) cudaIpcCloseMemHandle(p);
     for (auto ev : c->ipc_ev_opened) cudaEventDestroy(ev);

@@ -32,7 +32,8 @@ class Config(C.Structure):
                 ("max_inflight_batches", C.c_int), ("swap_mode", C.c_int), ("chunk_bytes", C.c_uint64),
                 ("writeback", C.c_int), ("trace", C.c_int), ("zc_ctas", C.c_int),
                 ("world_size", C.c_int), ("world_rank", C.c_int), ("shm_name", C.c_char_p),
-                ("gemm_impl", C.c_int), ("pp", C.c_int)]
+                ("gemm_impl", C.c_int), ("pp", C.c_int), ("helper_device_ids", C.POINTER(C.c_int)),
+                ("n_helpers", C.c_int)]
 
 
 class OptDims(C.Structure):
@@ -139,7 +140,7 @@ class Ctx:
 
     def __init__(self, device_ids=(0,), budget=1 << 30, max_batch=8, max_tokens=8, dtype=BF16,
                  max_inflight=1, swap_mode=SWAP_AUTO, chunk_bytes=0, writeback=1, trace=0, zc_ctas=0,
-                 world_size=1, world_rank=0, shm_name=None, gemm_impl=0, pp=1):
+                 world_size=1, world_rank=0, shm_name=None, gemm_impl=0, pp=1, helper_device_ids=()):
         """Single-process: one ctx over len(device_ids) = tp * pp ranks (global rank
         g = stage * tp + tp_rank). Multi-process (world_size > 1): device_ids = (this process's
         GPU,), rank world_rank of a TP group of world_size."""
@@ -152,7 +153,9 @@ class Ctx:
         self._shm = shm_name.encode() if shm_name else None
         cfg = Config(len(device_ids), self._ids, self.tp, budget, 0, max_batch, max_tokens, dtype,
                      max_inflight, swap_mode, chunk_bytes, writeback, trace, zc_ctas, world_size, world_rank,
-                     self._shm, gemm_impl, pp)
+                     self._shm, gemm_impl, pp,
+                     (C.c_int * max(1, len(helper_device_ids)))(*helper_device_ids) if helper_device_ids else None,
+                     len(helper_device_ids))
         h = _P()
         _check(lib().mpsw_init(C.byref(cfg), C.byref(h)))
         self.h = h
