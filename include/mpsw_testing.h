@@ -23,6 +23,11 @@ extern "C" {
 mpsw_status mpsw_test_gemm(int device, int dtype, int impl, const void* W, const void* X, const void* bias,
                            int M, int N, int K, int epi, float scale, float* out);
 
+/* Microbenchmark: average device time (us) of `reps` back-to-back launches of one library GEMM
+ * (impl 1 SIMT, 2 tcgen05) with N x K bf16 weights, M tokens, fp32 output. Device buffers are
+ * allocated, filled with a constant and freed inside. */
+mpsw_status mpsw_bench_gemm(int device, int impl, int M, int N, int K, int reps, float* us);
+
 #ifdef __cplusplus
 }
 #endif

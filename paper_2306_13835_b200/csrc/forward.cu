@@ -673,3 +673,60 @@ extern "C" mpsw_status mpsw_test_gemm(int device, int dtype, int impl, const voi
         return set_error(e.status, e.what());
     }
 }
+
+// Microbenchmark hook: average device time of `reps` back-to-back launches of one library GEMM
+// (weights N x K bf16 larger than L2, so every launch streams them from HBM).
+extern "C" mpsw_status mpsw_bench_gemm(int device, int impl, int M, int N, int K, int reps, float* us) {
+    using namespace mpsw;
+    try {
+        if (M < 1 || N < 1 || K < 8 || K % 8 || reps < 1 || (impl != 1 && impl != 2))
+            return set_error(MPSW_EINVAL, "bad arguments");
+        if (impl == 2 && !tc_supported(M, K)) return set_error(MPSW_EINVAL, "tcgen05 path needs M <= 256");
+        MPSW_CU(cudaSetDevice(device));
+        void *dW, *dX, *dO;
+        float* dP;
+        int* dCnt;
+        const int Mp = std::max(16, (M + 15) / 16 * 16);
+        MPSW_CU(cudaMalloc(&dW, (size_t)N * K * 2));
+        MPSW_CU(cudaMalloc(&dX, (size_t)M * K * 2));
+        MPSW_CU(cudaMalloc(&dO, (size_t)M * N * 4));
+        MPSW_CU(cudaMalloc(&dP, std::max<size_t>(1, tc_partial_floats(N, K, Mp)) * 4));
+        MPSW_CU(cudaMalloc(&dCnt, ((N + 127) / 128 + 4) * 4));
+        MPSW_CU(cudaMemset(dCnt, 0, ((N + 127) / 128 + 4) * 4));
+        MPSW_CU(cudaMemset(dW, 0x3c, (size_t)N * K * 2));
+        MPSW_CU(cudaMemset(dX, 0x3c, (size_t)M * K * 2));
+        cudaStream_t st;
+        MPSW_CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        auto run = [&] {
+            if (impl == 2) {
+                const void* Wp[1] = {dW};
+                const void* Bp[1] = {nullptr};
+                int Np[1] = {N}, c0[1] = {0};
+                float sc[1] = {1.f};
+                tc_gemm(Wp, Bp, Np, sc, c0, 1, dX, M, M, K, 0, dO, N, nullptr, dP, dCnt, st);
+            } else {
+                GemmArgs g{};
+                g.A = dX; g.M = M; g.K = K; g.lda = K;
+                g.seg[0] = {dW, nullptr, N, 1.f, 0};
+                g.nseg = 1; g.out = dO; g.ldo = N;
+                launch_gemm(MPSW_BF16, EPI_F32, g, st);
+            }
+        };
+        for (int i = 0; i < 3; ++i) run();
+        cudaEvent_t e0, e1;
+        MPSW_CU(cudaEventCreate(&e0));
+        MPSW_CU(cudaEventCreate(&e1));
+        MPSW_CU(cudaEventRecord(e0, st));
+        for (int i = 0; i < reps; ++i) run();
+        MPSW_CU(cudaEventRecord(e1, st));
+        MPSW_CU(cudaEventSynchronize(e1));
+        float ms = 0;
+        MPSW_CU(cudaEventElapsedTime(&ms, e0, e1));
+        *us = ms * 1000.f / reps;
+        cudaEventDestroy(e0); cudaEventDestroy(e1); cudaStreamDestroy(st);
+        cudaFree(dW); cudaFree(dX); cudaFree(dO); cudaFree(dP); cudaFree(dCnt);
+        return MPSW_OK;
+    } catch (const Error& e) {
+        return set_error(e.status, e.what());
+    }
+}

@@ -20,6 +20,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -413,9 +414,22 @@ static int sm_count() {
 }
 
 // Persistent grid: two CTAs per SM (fixed, so the stream-K split never depends on M).
+// tuning knobs (development: MPSW_TC_CPS = CTAs per SM, MPSW_TC_SMEM_KB = smem budget per CTA)
+static int env_int(const char* n, int dflt) {
+    const char* e = getenv(n);
+    return e ? atoi(e) : dflt;
+}
+
+static int tc_ctas_per_sm() {
+    static int v = env_int("MPSW_TC_CPS", 2);
+    return v;
+}
+
+// Persistent grid: a fixed number of CTAs per SM (never a function of M, so the stream-K split
+// and the reduction order are batch-invariant).
 static int tc_grid(int tiles, int K) {
     const uint64_t units = (uint64_t)tiles * ((K + kBK - 1) / kBK);
-    return (int)std::min<uint64_t>(units, 2 * (uint64_t)sm_count());
+    return (int)std::min<uint64_t>(units, (uint64_t)tc_ctas_per_sm() * sm_count());
 }
 
 size_t tc_partial_floats(int n_total, int K, int Mp) {
@@ -424,8 +438,9 @@ size_t tc_partial_floats(int n_total, int K, int Mp) {
 
 // Stages sized so that two CTAs fit per SM (<= ~110 KB each).
 int tc_stages(int Mp) {
+    static int budget_kb = env_int("MPSW_TC_SMEM_KB", 104);
     const size_t per = kTileABytes + (size_t)Mp * kBK * 2;
-    return (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, (104 * 1024) / per));
+    return (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, ((size_t)budget_kb * 1024) / per));
 }
 
 size_t tc_smem_bytes(int Mp) {

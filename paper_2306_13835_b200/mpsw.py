@@ -75,6 +75,7 @@ _SIGS = {
     "mpsw_residency": [_P, C.c_int, C.POINTER(C.c_int)],
     "mpsw_trace_dump": [_P, C.c_char_p],
     "mpsw_get_stats": [_P, C.POINTER(Stats)],
+    "mpsw_bench_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)],
     "mpsw_test_gemm": [C.c_int, C.c_int, C.c_int, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float,
                        C.POINTER(C.c_float)],
 }
@@ -118,6 +119,13 @@ def test_gemm(W, X, bias=None, impl=2, epi=0, scale=1.0, dtype=BF16, device=0):
                                 None if b is None else b.ctypes.data, M, N, K, epi, scale,
                                 out.ctypes.data_as(C.POINTER(C.c_float))))
     return out
+
+
+def bench_gemm(M, N, K, impl=2, reps=20, device=0):
+    """Average device microseconds of one library GEMM launch (include/mpsw_testing.h)."""
+    us = C.c_float()
+    _check(lib().mpsw_bench_gemm(device, impl, M, N, K, reps, C.byref(us)))
+    return us.value
 
 
 def dims_of(d):
