@@ -322,19 +322,51 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                     __threadfence();
                     if (nvalid) {
                         const int first_tile_of_cf = (int)(ubeg(g, c_first) / g.kb);
-                        for (int m0 = 0; m0 < g.M; m0 += 4) {
-                            // 4 outputs per step, register resident; runs summed in fixed k order
-                            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-                            for (int cc = c_first; cc <= c_last; ++cc) {
-                                const int wh = (cc == c_first && first_tile_of_cf != tile) ? 1 : 0;
-                                const float4 q = __ldcg(reinterpret_cast<const float4*>(
-                                    g.partial + (((size_t)cc * 2 + wh) * kBN + row) * g.Mp + m0));
-                                x.x += q.x; x.y += q.y; x.z += q.z; x.w += q.w;
+                        // 16 outputs per step; two runs per iteration so 8 independent float4
+                        // loads are in flight; the sums stay in fixed run (k) order
+                        auto prow_of = [&](int cc) {
+                            const int wh = (cc == c_first && first_tile_of_cf != tile) ? 1 : 0;
+                            return reinterpret_cast<const float4*>(
+                                g.partial + (((size_t)cc * 2 + wh) * kBN + row) * g.Mp);
+                        };
+                        for (int m0 = 0; m0 < g.M; m0 += 16) {
+                            float4 acc[4];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            int cc = c_first;
+                            for (; cc + 1 <= c_last; cc += 2) {
+                                const float4* p0 = prow_of(cc) + m0 / 4;
+                                const float4* p1 = prow_of(cc + 1) + m0 / 4;
+                                float4 a[4], b[4];
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) a[j] = __ldcg(p0 + j);
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) b[j] = __ldcg(p1 + j);
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    acc[j].x += a[j].x; acc[j].y += a[j].y; acc[j].z += a[j].z; acc[j].w += a[j].w;
+                                }
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    acc[j].x += b[j].x; acc[j].y += b[j].y; acc[j].z += b[j].z; acc[j].w += b[j].w;
+                                }
                             }
-                            epi_store(g, seg, n, m0, x.x, bias_n);
-                            if (m0 + 1 < g.M) epi_store(g, seg, n, m0 + 1, x.y, bias_n);
-                            if (m0 + 2 < g.M) epi_store(g, seg, n, m0 + 2, x.z, bias_n);
-                            if (m0 + 3 < g.M) epi_store(g, seg, n, m0 + 3, x.w, bias_n);
+                            if (cc == c_last) {
+                                const float4* p0 = prow_of(cc) + m0 / 4;
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    const float4 a = __ldcg(p0 + j);
+                                    acc[j].x += a.x; acc[j].y += a.y; acc[j].z += a.z; acc[j].w += a.w;
+                                }
+                            }
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const int m = m0 + 4 * j;
+                                if (m < g.M) epi_store(g, seg, n, m, acc[j].x, bias_n);
+                                if (m + 1 < g.M) epi_store(g, seg, n, m + 1, acc[j].y, bias_n);
+                                if (m + 2 < g.M) epi_store(g, seg, n, m + 2, acc[j].z, bias_n);
+                                if (m + 3 < g.M) epi_store(g, seg, n, m + 3, acc[j].w, bias_n);
+                            }
                         }
                     }
                     if (row == 0) g.counters[tile] = 0;   // ready for the next launch

@@ -17,8 +17,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
         row["GBps"] = round(sum(2 * N * K for N, K in SHAPES.values()) / (tot * 1e3), 1)
         print(json.dumps(row), flush=True)
     sys.exit(0)
-configs = [("1", {}), ("2", {}), ("2", {"MPSW_TC_SMEM_KB": "72"}), ("2", {"MPSW_TC_SMEM_KB": "200", "MPSW_TC_CPS": "1"}),
-           ("2", {"MPSW_TC_CPS": "3", "MPSW_TC_SMEM_KB": "72"}), ("2", {"MPSW_TC_CPS": "4", "MPSW_TC_SMEM_KB": "52"})]
+configs = [("2", {})]
 for impl, env in configs:
     e = dict(os.environ); e.update(env)
     subprocess.run([sys.executable, __file__, "child", impl], env=e)
