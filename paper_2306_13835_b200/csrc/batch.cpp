@@ -1,0 +1,125 @@
+// Batch entries (a6 / a7): the TP (x PP) forward of one rank, with the all-reduce fused into the
+// LayerNorm kernel over peer memory, and the logits slice returned to the pinned staging ring.
+#include "runtime.h"
+
+#include <algorithm>
+
+namespace mpsw {
+
+void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
+    const FwdShape& s = R.fs;
+    const int B = e.B, M = e.M;
+    const TensorPtrs& Wt = R.wptr[e.slot];
+    cudaStream_t cs = R.compute;
+    const int r = R.index, t = c->tp;
+    const int g0 = R.stage * t;                    // first global rank of my stage
+    const bool first = R.stage == 0, last = R.stage == c->pp - 1;
+    MPSW_CU(cudaEventCreate(&e.ev_start[r]));
+    MPSW_CU(cudaEventCreate(&e.ev_done[r]));
+    MPSW_CU(cudaEventRecord(e.ev_start[r], cs));
+    // tokens + meta (packed by the engine into the pinned ring entry)
+    uint8_t* ring = c->stg + (size_t)e.ring * c->ring_stride;
+    const size_t meta_n = (size_t)(3 * B + 1 + 2 * M);
+    MPSW_CU(cudaMemcpyAsync(R.ws.tokens, ring + c->ring_tok_off, (size_t)M * 4, cudaMemcpyHostToDevice, cs));
+    MPSW_CU(cudaMemcpyAsync(R.ws.meta, ring + c->ring_tok_off + (size_t)c->max_rows * 4, meta_n * 4,
+                            cudaMemcpyHostToDevice, cs));
+    const int32_t* pos = R.ws.meta + 2 * B + 1;
+    int nl = 0, point = 0;
+    // all-reduce point: record my partial, barrier with the other TP ranks of my stage, wait for
+    // every peer's partial on my stream, then the fused reduce + bias + residual + LN kernel
+    // reads all t partials directly (peer / IPC mappings over NVLink).
+    auto allreduce_ln = [&](const float* residual, const void* bias, const void* pos_table, const void* g,
+                            const void* b) {
+        const int pb = point & 1;
+        const float* peers[kMaxRanks];
+        if (t > 1) {
+            MPSW_CU(cudaEventRecord(R.ev_point[pb], cs));
+            group_barrier(c, R.stage);
+            for (int p = 0; p < t; ++p)
+                if (g0 + p != r) MPSW_CU(cudaStreamWaitEvent(cs, c->peer_ev[g0 + p][pb], 0));
+        }
+        for (int p = 0; p < t; ++p) peers[p] = c->peer_partial[g0 + p][pb];
+        nl += fwd_reduce_ln(s, M, peers, t, residual, bias, pos_table, pos, g, b, R.ws.x, R.ws.a, cs);
+        ++point;
+    };
+    if (first) {
+        nl += fwd_embed(s, Wt, R.ws, M, R.ws.partial[point & 1], cs);
+        allreduce_ln(nullptr, nullptr, Wt.embed_pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b);
+    } else {
+        // PP hop ("PP communication occurs through FIFO pipes"): take the residual stream
+        // of the same TP rank of the previous stage (peer copy over NVLink), then LN1 of my
+        // first layer. D = 1 for pp > 1, so batches never overlap on a stage boundary.
+        Rank& P = *c->ranks[c->local_of[r - t]];
+        int spins = 0;
+        while (P.stage_out.load(std::memory_order_acquire) < e.id + 1) {
+            if (group_poisoned(c)) throw Error(MPSW_ECUDA, "peer failed");
+            spin_pause(spins);
+        }
+        MPSW_CU(cudaStreamWaitEvent(cs, P.ev_stage, 0));
+        MPSW_CU(cudaMemcpyAsync(R.ws.partial[0], P.ws.x, (size_t)M * s.hidden * 4, cudaMemcpyDeviceToDevice, cs));
+        const float* self[1] = {R.ws.partial[0]};
+        nl += fwd_reduce_ln(s, M, self, 1, nullptr, nullptr, nullptr, pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b,
+                            R.ws.x, R.ws.a, cs);
+        point = 1;
+    }
+    for (int l = 0; l < s.n_layers; ++l) {
+        const auto& L = Wt.layers[l];
+        nl += fwd_qkv(s, L, R.ws, M, cs);
+        nl += fwd_attention(s, R.ws, B, cs);
+        nl += fwd_out_proj(s, L, R.ws, M, R.ws.partial[point & 1], cs);
+        allreduce_ln(R.ws.x, L.o_b, nullptr, L.ln2_w, L.ln2_b);
+        nl += fwd_fc1(s, L, R.ws, M, cs);
+        nl += fwd_fc2(s, L, R.ws, M, R.ws.partial[point & 1], cs);
+        const bool lastl = l + 1 == s.n_layers;
+        // after a non-final stage's last layer only the residual stream matters; the LN output
+        // (computed with this layer's LN2 parameters) is unused
+        const void* ng = lastl ? (last ? Wt.lnf_w : L.ln2_w) : Wt.layers[l + 1].ln1_w;
+        const void* nb = lastl ? (last ? Wt.lnf_b : L.ln2_b) : Wt.layers[l + 1].ln1_b;
+        allreduce_ln(R.ws.x, L.fc2_b, nullptr, ng, nb);
+    }
+    if (last) {
+        nl += fwd_lm_head(s, Wt, R.ws, B, M, cs);
+        float* logits_host = (float*)(ring) + (size_t)R.trank * s.vocab_local;
+        MPSW_CU(cudaMemcpy2DAsync(logits_host, (size_t)s.vocab * 4, R.ws.logits, (size_t)s.vocab_local * 4,
+                                  (size_t)s.vocab_local * 4, B, cudaMemcpyDeviceToHost, cs));
+    } else {
+        MPSW_CU(cudaEventRecord(R.ev_stage, cs));
+        R.stage_out.store(e.id + 1, std::memory_order_release);
+    }
+    MPSW_CU(cudaEventRecord(e.ev_done[r], cs));
+    MPSW_CU(cudaEventRecord(R.last_compute[e.model], cs));
+    R.last_compute_valid[e.model] = 1;
+    c->launches += nl;
+}
+
+// Weight pointers of one rank's slot, looked up by HF name in that rank's layout (stage-local
+// layers only; embeddings / final LN only where the stage holds them).
+TensorPtrs make_ptrs(const Layout& L, const uint8_t* base, int layer0, int n_layers) {
+    std::unordered_map<std::string, const void*> by;
+    for (const auto& t : L.t) by[t.name] = base + t.offset;
+    auto p = [&](const std::string& n) -> const void* {
+        auto it = by.find(n);
+        return it == by.end() ? nullptr : it->second;
+    };
+    TensorPtrs w;
+    w.embed_tok = p("decoder.embed_tokens.weight");
+    w.embed_pos = p("decoder.embed_positions.weight");
+    w.lnf_w = p("decoder.final_layer_norm.weight");
+    w.lnf_b = p("decoder.final_layer_norm.bias");
+    for (int l = layer0; l < layer0 + n_layers; ++l) {
+        const std::string q = "decoder.layers." + std::to_string(l) + ".";
+        TensorPtrs::Layer x;
+        x.k_w = p(q + "self_attn.k_proj.weight"); x.k_b = p(q + "self_attn.k_proj.bias");
+        x.v_w = p(q + "self_attn.v_proj.weight"); x.v_b = p(q + "self_attn.v_proj.bias");
+        x.q_w = p(q + "self_attn.q_proj.weight"); x.q_b = p(q + "self_attn.q_proj.bias");
+        x.o_w = p(q + "self_attn.out_proj.weight"); x.o_b = p(q + "self_attn.out_proj.bias");
+        x.ln1_w = p(q + "self_attn_layer_norm.weight"); x.ln1_b = p(q + "self_attn_layer_norm.bias");
+        x.fc1_w = p(q + "fc1.weight"); x.fc1_b = p(q + "fc1.bias");
+        x.fc2_w = p(q + "fc2.weight"); x.fc2_b = p(q + "fc2.bias");
+        x.ln2_w = p(q + "final_layer_norm.weight"); x.ln2_b = p(q + "final_layer_norm.bias");
+        w.layers.push_back(x);
+    }
+    return w;
+}
+
+}  // namespace mpsw

@@ -1,0 +1,272 @@
+// Runtime types shared by the library's translation units (not part of the C-ABI): pinned
+// store, shm control plane, entries, per-rank state, the ctx, and cross-file function decls.
+#pragma once
+
+#include "internal.h"
+#include "statemachine.h"
+
+#include <immintrin.h>
+
+#include <functional>
+#include <future>
+#include <map>
+#include <string>
+#include <unordered_map>
+
+namespace mpsw {
+
+constexpr uint64_t kNoopTicket = ~0ull;
+constexpr uint64_t kSlotAlign = 4096;
+constexpr int kMaxRanks = 8;
+constexpr int kMaxHelpers = 8;
+constexpr size_t kMaxModels = 4096;
+
+struct PinnedBuf {
+    uint8_t* p = nullptr;
+    uint64_t bytes = 0;
+    uint64_t map_bytes = 0;
+};
+
+inline void spin_pause(int& spins) {
+    if (++spins < 2048) _mm_pause();
+    else std::this_thread::yield();
+}
+
+struct SpinBarrier {
+    std::atomic<int> count{0};
+    std::atomic<int> gen{0};
+    int n = 1;
+    void wait() {
+        if (n <= 1) return;
+        const int g = gen.load(std::memory_order_acquire);
+        if (count.fetch_add(1, std::memory_order_acq_rel) + 1 == n) {
+            count.store(0, std::memory_order_relaxed);
+            gen.fetch_add(1, std::memory_order_acq_rel);
+        } else {
+            int spins = 0;
+            while (gen.load(std::memory_order_acquire) == g) spin_pause(spins);
+        }
+    }
+};
+
+// ----------------------------------------------------------------------------- shm control plane
+constexpr uint64_t kShmMagic = 0x314d485357534d50ull;  // "PMSWSHM1"
+constexpr uint64_t kLogCap = 1 << 16;
+constexpr uint64_t kAckCap = 1 << 16;
+
+struct ShmRec {            // one decision published by the leader
+    uint64_t id;
+    int32_t kind, model, slot, ring, B, M;
+};
+
+struct ShmCtl {
+    std::atomic<uint64_t> magic;
+    int32_t world;
+    std::atomic<int32_t> joined;
+    std::atomic<int32_t> stop;            // leader has shut down
+    std::atomic<int32_t> poisoned;
+    char poison_msg[256];
+    std::atomic<int32_t> bar_count, bar_gen;
+    std::atomic<int32_t> stg_ready;       // leader created the staging segment
+    uint64_t stg_bytes;
+    std::atomic<uint64_t> log_tail;       // records published
+    std::atomic<uint64_t> consumed[kMaxRanks];   // records taken by each follower
+    cudaIpcMemHandle_t ws_handle[kMaxRanks];
+    uint64_t partial_off[kMaxRanks][2];
+    cudaIpcEventHandle_t ev_handle[kMaxRanks][2];
+    ShmRec log[kLogCap];
+    std::atomic<uint64_t> ack[kAckCap][kMaxRanks];
+};
+
+// ----------------------------------------------------------------------------- entries
+struct ReqRec {
+    int64_t rid;
+    int model;
+    std::vector<int32_t> tokens;
+    float* out;
+    double t_arr = 0, t_done = 0;
+    std::atomic<int> done{0};
+};
+
+struct Entry {
+    uint64_t id = 0;
+    int kind = 0, model = -1, slot = -1;
+    std::vector<std::shared_ptr<ReqRec>> reqs;   // leader only
+    int ring = 0, B = 0, M = 0;
+    double t_submit = 0;
+    cudaEvent_t ev_start[kMaxRanks] = {};        // indexed by GLOBAL rank; only local ranks set
+    cudaEvent_t ev_done[kMaxRanks] = {};
+    std::atomic<int> issued[kMaxRanks];
+    int acked[kMaxRanks] = {};
+    double t_ack[kMaxRanks] = {};
+    float gpu_ms[kMaxRanks] = {};                // device span per local rank, kept after events die
+    cudaEvent_t ev_helper[kMaxRanks][kMaxHelpers] = {};   // fan-in: helper h done with rank r's chunks
+    int n_acked = 0;
+    std::atomic<int> complete{0};
+    Entry() {
+        for (auto& a : issued) a.store(0);
+    }
+};
+using EntryP = std::shared_ptr<Entry>;
+
+// ----------------------------------------------------------------------------- per-rank state
+struct Slot {
+    uint8_t* base = nullptr;
+    std::vector<cudaEvent_t> chunk_gate;   // recorded by the last writeback offload, per chunk
+    bool chunk_gate_valid = false;
+    cudaEvent_t whole_gate = nullptr;      // clean eviction: last forward that read the slot
+    bool whole_gate_valid = false;
+};
+
+// NVLink-assisted fan-in (NEXT-2): a helper GPU's own PCIe link pulls chunks of another rank's
+// shard into a 2-chunk staging ring in its HBM, then forwards each chunk to the owner's slot with
+// a peer copy over NVLink. Helpers are shared by all rank worker threads (mutex).
+struct Helper {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint8_t* staging = nullptr;            // 2 * chunk bytes
+    cudaEvent_t free_ev[2] = {nullptr, nullptr};
+    bool free_valid[2] = {false, false};
+    int next = 0;
+    std::mutex mu;
+};
+
+struct Rank {
+    int index = 0, local = 0, device = 0, numa = -1;   // index = global rank = stage * tp + trank
+    int stage = 0, trank = 0;              // pipeline stage, TP rank inside the stage
+    Layout layout;                         // this rank's arena layout (stage-dependent)
+    uint64_t S = 0, stride = 0;            // arena bytes, slot stride
+    int n_chunks = 0;
+    FwdShape fs{};                         // forward shape of this rank (its stage's layers)
+    cudaEvent_t ev_stage = nullptr;        // PP: residual stream of this stage is ready
+    std::atomic<uint64_t> stage_out{0};    // PP: id+1 of the last batch whose ev_stage is recorded
+    cudaStream_t compute = nullptr, h2d = nullptr, d2h = nullptr, aux = nullptr;
+    cudaStream_t h2d_zc = nullptr;         // hybrid swap: the zero-copy share of a swap-in
+    cudaEvent_t ev_zc = nullptr;
+    uint8_t* region = nullptr;             // param budget (one cudaMalloc)
+    std::vector<Slot> slots;
+    uint8_t* ws_base = nullptr;
+    FwdWorkspace ws;
+    std::vector<TensorPtrs> wptr;          // per slot
+    cudaEvent_t ev_point[2] = {nullptr, nullptr};   // partial-ready events (interprocess in mp mode)
+    std::vector<cudaEvent_t> last_compute; // per model
+    std::vector<char> last_compute_valid;
+    unsigned long long* d_sum = nullptr;
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<EntryP> fifo;
+};
+
+struct Model {
+    mpsw_opt_dims dims;
+    std::vector<PinnedBuf> arena;  // per LOCAL rank
+};
+
+struct Cmd {
+    int kind;  // 0 arrival, 1 swap_in, 2 swap_out
+    int model;
+    std::shared_ptr<ReqRec> req;
+    std::promise<std::pair<mpsw_status, uint64_t>>* reply = nullptr;
+};
+
+}  // namespace mpsw
+
+struct mpsw_ctx {
+    mpsw_config cfg{};
+    std::vector<int> device_ids;
+    std::chrono::steady_clock::time_point t0;
+    int tp = 1, D = 1;
+    int pp = 1, nr = 1;        // pipeline stages; ranks = tp * pp (workers, acks per entry)
+    mpsw::SpinBarrier stage_barrier[mpsw::kMaxRanks];   // TP barrier of each stage (single process)
+    bool mp = false;           // multi-process mode
+    bool leader = true;        // runs the engine (single-process mode: always)
+    int world_rank = 0;
+    uint64_t chunk = 64ull << 20;
+    std::vector<std::unique_ptr<mpsw::Rank>> ranks;     // LOCAL ranks
+    std::vector<std::unique_ptr<mpsw::Helper>> helpers; // fan-in helper GPUs (single process)
+    int local_of[mpsw::kMaxRanks];                        // global rank -> local index or -1
+    std::vector<std::unique_ptr<mpsw::Model>> models;
+    // geometry (fixed by the first registered model; homogeneous slots)
+    bool geom = false;
+    mpsw_opt_dims dims{};
+    int k = 0;
+    uint64_t rank_S[mpsw::kMaxRanks] = {};   // arena bytes per global rank
+    int vocab = 0;
+    int max_rows = 0;
+    // TP peers (global rank -> partial buffers / partial-ready events)
+    float* peer_partial[mpsw::kMaxRanks][2] = {};
+    cudaEvent_t peer_ev[mpsw::kMaxRanks][2] = {};
+    std::vector<void*> ipc_mem_opened;
+    std::vector<cudaEvent_t> ipc_ev_opened;
+    // logits / tokens staging ring (pinned; shm in mp mode), D + 1 entries
+    int ring_n = 2;
+    uint8_t* stg = nullptr;
+    mpsw::PinnedBuf stg_local;
+    size_t stg_map_bytes = 0;
+    size_t ring_stride = 0, ring_tok_off = 0;
+    // multi-process control plane
+    std::string shm_name;
+    mpsw::ShmCtl* ctl = nullptr;
+    // engine
+    mpsw::StateMachine sm;
+    std::mutex cmd_mu;
+    std::condition_variable cmd_cv;
+    std::deque<mpsw::Cmd> cmds;
+    std::thread engine;
+    std::atomic<bool> stop{false};
+    std::atomic<int> poisoned{0};
+    std::string poison_msg;
+    std::vector<mpsw::EntryP> inflight;
+    std::mutex done_mu;
+    std::condition_variable done_cv;
+    std::unordered_map<uint64_t, mpsw::EntryP> entries;        // swap entries by ticket
+    std::unordered_map<int64_t, std::shared_ptr<mpsw::ReqRec>> reqs;
+    std::atomic<int64_t> next_rid{0};
+    int ring_next = 0;
+    std::mutex api_mu;
+    // follower-local view of residency (mp followers)
+    std::vector<int> f_slot_of;
+    std::vector<int> f_state;
+    std::mutex f_mu;
+    // trace + stats
+    bool trace = false;
+    std::mutex trace_mu;
+    std::vector<std::string> trace_lines;
+    std::mutex sm_mu;
+    std::unordered_map<int64_t, std::shared_ptr<mpsw::ReqRec>> eng_reqs;   // engine-private
+    std::atomic<uint64_t> launches{0}, h2d_bytes{0}, d2h_bytes{0}, swaps_in{0}, swaps_out{0}, n_batches{0},
+        n_requests{0}, rejected{0}, fwd_us_sum{0}, fwd_n{0};
+};
+
+namespace mpsw {
+
+// store.cpp
+int gpu_numa_node(int dev);
+PinnedBuf pin_alloc(uint64_t bytes, int numa_node);
+void pin_free(PinnedBuf& b);
+void parallel_memcpy(uint8_t* dst, const uint8_t* src, uint64_t n);
+void* shm_map(const std::string& name, size_t bytes, bool create);
+
+// engine.cpp
+std::string fmt_d(double v);
+void poison(mpsw_ctx* c, const std::string& msg);
+bool group_poisoned(mpsw_ctx* c);
+void group_barrier(mpsw_ctx* c, int stage = 0);
+void worker_main(mpsw_ctx* c, Rank* R);
+void engine_main(mpsw_ctx* c);
+void follower_main(mpsw_ctx* c);
+void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& d);
+
+// swap.cpp
+bool event_done(cudaEvent_t ev);
+bool use_zero_copy(mpsw_ctx* c, uint64_t bytes);
+void issue_load(mpsw_ctx* c, Rank& R, Entry& e);
+void issue_offload(mpsw_ctx* c, Rank& R, Entry& e);
+void finish_swap_events(mpsw_ctx* c, Entry& e);
+
+// batch.cpp
+void issue_batch(mpsw_ctx* c, Rank& R, Entry& e);
+TensorPtrs make_ptrs(const Layout& L, const uint8_t* base, int layer0, int n_layers);
+
+}  // namespace mpsw

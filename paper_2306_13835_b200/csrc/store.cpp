@@ -1,0 +1,93 @@
+// Pinned shard store ("the parameters are kept pinned in CPU memory") and the POSIX
+// shared-memory segments of the multi-process control plane.
+#include "runtime.h"
+
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstring>
+#include <fstream>
+
+namespace mpsw {
+
+int gpu_numa_node(int dev) {
+    char bus[64] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof(bus), dev) != cudaSuccess) return -1;
+    for (char* c = bus; *c; ++c) *c = (char)tolower(*c);
+    std::ifstream f(std::string("/sys/bus/pci/devices/") + bus + "/numa_node");
+    int node = -1;
+    if (f) f >> node;
+    return node;
+}
+
+// NUMA-affine page-locked arena: anonymous mmap, transparent huge pages, bound to the
+// GPU's NUMA node when the platform reports one, then registered (portable + mapped so the
+// zero-copy kernel can read it through UVA).
+PinnedBuf pin_alloc(uint64_t bytes, int numa_node) {
+    PinnedBuf b;
+    b.bytes = bytes;
+    b.map_bytes = (std::max<uint64_t>(bytes, 1) + (2ull << 20) - 1) / (2ull << 20) * (2ull << 20);
+    void* p = mmap(nullptr, b.map_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+    if (p == MAP_FAILED) throw Error(MPSW_ENOMEM, "mmap of pinned arena failed");
+    madvise(p, b.map_bytes, MADV_HUGEPAGE);
+    if (numa_node >= 0 && numa_node < 64) {
+        unsigned long mask = 1ul << numa_node;
+        syscall(SYS_mbind, p, b.map_bytes, 2 /*MPOL_BIND*/, &mask, 64, 0);
+    }
+    cudaError_t e = cudaHostRegister(p, b.map_bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        munmap(p, b.map_bytes);
+        throw Error(MPSW_ENOMEM, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
+    }
+    b.p = (uint8_t*)p;
+    return b;
+}
+
+void pin_free(PinnedBuf& b) {
+    if (!b.p) return;
+    cudaHostUnregister(b.p);
+    munmap(b.p, b.map_bytes);
+    b.p = nullptr;
+}
+
+void parallel_memcpy(uint8_t* dst, const uint8_t* src, uint64_t n) {
+    const int T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (n < (64ull << 20)) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+        th.emplace_back([=] {
+            const uint64_t b = n * t / T, e = n * (t + 1) / T;
+            std::memcpy(dst + b, src + b, e - b);
+        });
+    for (auto& x : th) x.join();
+}
+
+void* shm_map(const std::string& name, size_t bytes, bool create) {
+    int fd = create ? shm_open(name.c_str(), O_CREAT | O_RDWR | O_TRUNC, 0600) : shm_open(name.c_str(), O_RDWR, 0600);
+    if (fd < 0) return nullptr;
+    if (create && ftruncate(fd, (off_t)bytes) != 0) {
+        close(fd);
+        throw Error(MPSW_ENOMEM, "ftruncate of shm segment failed");
+    }
+    if (!create) {
+        struct stat st;
+        if (fstat(fd, &st) != 0 || (size_t)st.st_size < bytes) {
+            close(fd);
+            return nullptr;
+        }
+    }
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) throw Error(MPSW_ENOMEM, "mmap of shm segment failed");
+    return p;
+}
+
+}  // namespace mpsw
