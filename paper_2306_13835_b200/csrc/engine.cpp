@@ -1,5 +1,6 @@
-// mpsw runtime: pinned shard store, device slots, per-rank workers, the engine (scheduler)
-// thread, the multi-process control plane and the C-ABI entry points.
+// mpsw runtime core: per-rank workers, the engine (scheduler) thread, the multi-process follower
+// and control plane, and the slot geometry. (Store: store.cpp; swap entries: swap.cpp; batch
+// entries: batch.cpp; C-ABI: capi.cpp; types and the ctx: runtime.h.)
 //
 // Architecture (§3.1 Fig. 1, §3.2, §4):
 //   * one engine thread = the paper's centralised engine (statemachine.h): per-model FIFO
