@@ -196,6 +196,12 @@ mpsw_status mpsw_residency(mpsw_ctx* ctx, int model_id, int* state);
 /* Write the recorded events and decisions, in engine order, as NDJSON (trace = 1). */
 mpsw_status mpsw_trace_dump(mpsw_ctx* ctx, const char* ndjson_path);
 
+/* Write this process's device timeline as NDJSON (trace = 1): one line per finished entry per
+ * local rank, {"kind": "load"|"offload"|"batch", "id", "model", "rank", "device", "t0_ms",
+ * "t1_ms"}, times from CUDA events relative to one origin event per device (so spans of the
+ * ranks that share a GPU are comparable: evidence of swap / forward overlap). */
+mpsw_status mpsw_timeline_dump(mpsw_ctx* ctx, const char* ndjson_path);
+
 typedef struct {
     uint64_t kernel_launches;     /* kernels this library launched (all ranks)              */
     uint64_t h2d_bytes, d2h_bytes;/* bytes moved by swaps                                   */

@@ -90,6 +90,7 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     c->D = cfg->max_inflight_batches > 0 ? cfg->max_inflight_batches : 1;
     c->chunk = cfg->chunk_bytes ? cfg->chunk_bytes : (64ull << 20);
     c->trace = cfg->trace != 0 && c->leader;
+    c->timeline_on = cfg->trace != 0;
     c->device_ids.assign(cfg->device_ids, cfg->device_ids + cfg->n_gpus);
     c->sm.tp = c->nr;              // acks per entry: one per worker
     c->sm.max_batch = cfg->max_batch;
@@ -125,6 +126,16 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
             return set_error(MPSW_ENOMEM, std::string("cudaMalloc(param budget): ") + cudaGetErrorString(e));
         }
         MPSW_CU(cudaMalloc(&R->d_sum, sizeof(unsigned long long)));
+        if (cfg->trace) {
+            // one timeline origin per device, shared by the ranks that live on it
+            for (auto& Q : c->ranks)
+                if (Q->device == dev) R->ev_base = Q->ev_base;
+            if (!R->ev_base) {
+                MPSW_CU(cudaEventCreate(&R->ev_base));
+                MPSW_CU(cudaEventRecord(R->ev_base, R->compute));
+                MPSW_CU(cudaEventSynchronize(R->ev_base));
+            }
+        }
         c->ranks.push_back(std::move(R));
     }
     if (cfg->n_helpers < 0 || cfg->n_helpers > kMaxHelpers || (cfg->n_helpers && !cfg->helper_device_ids))
@@ -248,6 +259,12 @@ mpsw_status mpsw_shutdown(mpsw_ctx* c) {
         for (auto ev : R->ev_point)
             if (ev) cudaEventDestroy(ev);
         if (R->ev_stage) cudaEventDestroy(R->ev_stage);
+        if (R->ev_base) {
+            for (auto& Q : c->ranks)
+                if (Q.get() != R.get() && Q->ev_base == R->ev_base) Q->ev_base = nullptr;
+            cudaEventDestroy(R->ev_base);
+            R->ev_base = nullptr;
+        }
         for (auto ev : R->last_compute)
             if (ev) cudaEventDestroy(ev);
         cudaFree(R->region);
@@ -599,6 +616,18 @@ mpsw_status mpsw_trace_dump(mpsw_ctx* c, const char* path) {
     std::ofstream f(path);
     if (!f) return set_error(MPSW_EINVAL, "cannot open trace path");
     for (const auto& l : c->trace_lines) f << l << "\n";
+    return MPSW_OK;
+    API_END
+}
+
+mpsw_status mpsw_timeline_dump(mpsw_ctx* c, const char* path) {
+    API_BEGIN
+    if (!c || !path) return set_error(MPSW_EINVAL, "NULL argument");
+    if (!c->timeline_on) return set_error(MPSW_EINVAL, "timeline disabled (cfg.trace = 0)");
+    std::lock_guard<std::mutex> lk(c->trace_mu);
+    std::ofstream f(path);
+    if (!f) return set_error(MPSW_EINVAL, "cannot open timeline path");
+    for (const auto& l : c->timeline) f << l << "\n";
     return MPSW_OK;
     API_END
 }

@@ -235,7 +235,28 @@ void complete_batch(mpsw_ctx* c, Entry& e, double now) {
 }
 
 // Device time of a finished batch's forward on the first local rank (stats), then free its events.
+void record_spans(mpsw_ctx* c, Entry& e) {
+    if (!c->trace && !c->timeline_on) return;
+    static const char* kinds[] = {"load", "offload", "batch"};
+    for (auto& Rp : c->ranks) {
+        const int r = Rp->index;
+        float t0 = 0, t1 = 0;
+        if (!Rp->ev_base || !e.ev_start[r] || !e.ev_done[r]) continue;
+        if (cudaEventElapsedTime(&t0, Rp->ev_base, e.ev_start[r]) != cudaSuccess ||
+            cudaEventElapsedTime(&t1, Rp->ev_base, e.ev_done[r]) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        std::ostringstream o;
+        o << "{\"kind\":\"" << kinds[e.kind] << "\",\"id\":" << e.id << ",\"model\":" << e.model << ",\"rank\":" << r
+          << ",\"device\":" << Rp->device << ",\"t0_ms\":" << fmt_d(t0) << ",\"t1_ms\":" << fmt_d(t1) << "}";
+        std::lock_guard<std::mutex> lk(c->trace_mu);
+        c->timeline.push_back(o.str());
+    }
+}
+
 void record_fwd_time(mpsw_ctx* c, Entry& e) {
+    record_spans(c, e);
     const int r0 = c->ranks[0]->index;
     float ms = 0;
     if (e.ev_start[r0] && e.ev_done[r0] && cudaEventElapsedTime(&ms, e.ev_start[r0], e.ev_done[r0]) == cudaSuccess) {

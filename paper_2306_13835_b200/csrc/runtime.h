@@ -139,6 +139,7 @@ struct Rank {
     int n_chunks = 0;
     FwdShape fs{};                         // forward shape of this rank (its stage's layers)
     cudaEvent_t ev_stage = nullptr;        // PP: residual stream of this stage is ready
+    cudaEvent_t ev_base = nullptr;         // timeline origin of this rank's device (trace = 1)
     std::atomic<uint64_t> stage_out{0};    // PP: id+1 of the last batch whose ev_stage is recorded
     cudaStream_t compute = nullptr, h2d = nullptr, d2h = nullptr, aux = nullptr;
     cudaStream_t h2d_zc = nullptr;         // hybrid swap: the zero-copy share of a swap-in
@@ -231,8 +232,10 @@ struct mpsw_ctx {
     std::mutex f_mu;
     // trace + stats
     bool trace = false;
+    bool timeline_on = false;   // record device spans (cfg.trace), on every rank / process
     std::mutex trace_mu;
     std::vector<std::string> trace_lines;
+    std::vector<std::string> timeline;     // device spans of entries (trace = 1), NDJSON
     std::mutex sm_mu;
     std::unordered_map<int64_t, std::shared_ptr<mpsw::ReqRec>> eng_reqs;   // engine-private
     std::atomic<uint64_t> launches{0}, h2d_bytes{0}, d2h_bytes{0}, swaps_in{0}, swaps_out{0}, n_batches{0},
@@ -257,6 +260,10 @@ void worker_main(mpsw_ctx* c, Rank* R);
 void engine_main(mpsw_ctx* c);
 void follower_main(mpsw_ctx* c);
 void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& d);
+
+// engine.cpp: device timeline (trace = 1): [t0, t1] of an entry on each local rank, relative to
+// the rank's device origin event; called before the entry's events are destroyed
+void record_spans(mpsw_ctx* c, Entry& e);
 
 // swap.cpp
 bool event_done(cudaEvent_t ev);

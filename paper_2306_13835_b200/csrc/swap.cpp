@@ -151,6 +151,7 @@ void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
 // Device span of a finished swap entry on every local rank; then its events are released (a
 // long run would otherwise keep 2 events per rank per swap).
 void finish_swap_events(mpsw_ctx* c, Entry& e) {
+    record_spans(c, e);
     for (int r = 0; r < c->nr; ++r) {
         if (e.ev_start[r] && e.ev_done[r] && cudaEventElapsedTime(&e.gpu_ms[r], e.ev_start[r], e.ev_done[r]) != cudaSuccess)
             e.gpu_ms[r] = 0;

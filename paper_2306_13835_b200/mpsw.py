@@ -74,6 +74,7 @@ _SIGS = {
     "mpsw_peek": [_P, C.c_int, C.c_int, C.c_uint64, C.c_uint64, _P],
     "mpsw_residency": [_P, C.c_int, C.POINTER(C.c_int)],
     "mpsw_trace_dump": [_P, C.c_char_p],
+    "mpsw_timeline_dump": [_P, C.c_char_p],
     "mpsw_get_stats": [_P, C.POINTER(Stats)],
     "mpsw_bench_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)],
     "mpsw_test_gemm": [C.c_int, C.c_int, C.c_int, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float,
@@ -281,6 +282,9 @@ class Ctx:
 
     def trace_dump(self, path):
         _check(lib().mpsw_trace_dump(self.h, path.encode()))
+
+    def timeline_dump(self, path):
+        _check(lib().mpsw_timeline_dump(self.h, path.encode()))
 
     def stats(self):
         s = Stats()

@@ -68,8 +68,17 @@ def test_gamma_trace_replay_and_outcomes(tmp_path, tp, D):
             ctx.wait_request(rid, 120)
         p = str(tmp_path / "trace.ndjson")
         ctx.trace_dump(p)
+        tl = str(tmp_path / "timeline.ndjson")
+        ctx.timeline_dump(tl)
         st = ctx.stats()
     assert st["k_slots"] == k
+    spans = [json.loads(l) for l in open(tl)]
+    assert spans and all(s["t1_ms"] >= s["t0_ms"] >= 0 for s in spans)
+    by_entry = {}
+    for s in spans:
+        by_entry.setdefault((s["kind"], s["id"]), set()).add(s["rank"])
+    assert all(r == set(range(tp)) for r in by_entry.values())      # every rank's span recorded
+    assert sum(1 for k_ in by_entry if k_[0] == "load") == st["swaps_in"]
     replay_check(p, nm, k, tp, mb, D)
     assert st["swaps_in"] >= nm
     Ws = {m: layout.full_tensors(d, 500 + m) for m in range(nm)}

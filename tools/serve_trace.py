@@ -83,6 +83,7 @@ def main():
                 lat.append(td - ta)
         tpath = "/tmp/serve_trace.ndjson"
         ctx.trace_dump(tpath)
+        ctx.timeline_dump("/tmp/serve_timeline.ndjson")
         st = ctx.stats()
         loads = [json.loads(l) for l in open(tpath) if '"dec":"load"' in l]
         h2d = []   # host-observed swap-in latency (submit -> last rank's ack), ms: virtual ranks share
@@ -96,6 +97,21 @@ def main():
     res["swap_in_GBps_median"] = float(np.median([tp * S_r / (ms / 1e3) / 1e9 for ms in h2d])) if h2d else None
     res["batches"] = st["batches"]
     res["fwd_ms_mean"] = st["fwd_gpu_us_sum"] / 1e3 / max(1, st["fwd_gpu_n"])
+    # device timeline: how much forward time ran while a swap-in was streaming on the same GPU
+    # ("a later batch entry [proceeds] without waiting for a previous load entry")
+    spans = [json.loads(l) for l in open("/tmp/serve_timeline.ndjson")]
+    loads = sorted((s_["t0_ms"], s_["t1_ms"]) for s_ in spans if s_["kind"] == "load")
+    fwd = [(s_["t0_ms"], s_["t1_ms"]) for s_ in spans if s_["kind"] == "batch"]
+    merged = []
+    for a, b in loads:
+        if merged and a <= merged[-1][1]:
+            merged[-1][1] = max(merged[-1][1], b)
+        else:
+            merged.append([a, b])
+    ov = sum(max(0.0, min(b, y) - max(a, x)) for a, b in fwd for x, y in merged)
+    tot = sum(b - a for a, b in fwd)
+    res["fwd_ms_total"] = tot
+    res["fwd_overlapped_with_swapin_frac"] = ov / tot if tot else 0.0
     # replay parity of the engine's decisions (oracle C1)
     evs, decs = [], []
     for line in open(tpath):
