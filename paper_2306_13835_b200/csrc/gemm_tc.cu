@@ -128,8 +128,9 @@ struct TcArgs {
     void* out;
     int ldo;
     const int32_t* row_of_m;     // optional: output row for token m (-1 = drop); lm_head
-    float* partial;              // [G][2][128][Mp]: a CTA's first / last partial run
+    float* partial;              // [G][2][Mp][128]: a CTA's first / last partial run (row fastest)
     int* counters;               // [tiles], self-resetting
+    int ext_fixup;               // 1: split tiles are reduced by tc_fixup_kernel, not in-kernel
 };
 
 // Stream-K work split: CTA c owns units [ubeg(c), ubeg(c+1)) of the linearised (tile, k-block)
@@ -141,6 +142,13 @@ __device__ __forceinline__ int cta_of(const TcArgs& g, uint64_t u) {
     while (c + 1 < g.G && ubeg(g, c + 1) <= u) ++c;
     while (c > 0 && ubeg(g, c) > u) --c;
     return c;
+}
+
+// Partial run of CTA cc on a split tile: slot 0 if the tile is cc's first tile, else slot 1
+// (a CTA touches at most two split tiles: where its range starts and where it ends).
+__device__ __forceinline__ const float* partial_run(const TcArgs& g, int cc, int c_first, int tile, int row) {
+    const int wh = (cc == c_first && (int)(ubeg(g, c_first) / g.kb) != tile) ? 1 : 0;
+    return g.partial + ((size_t)cc * 2 + wh) * (size_t)g.Mp * kBN + row;
 }
 
 __device__ __forceinline__ void epi_store(const TcArgs& g, const TcSeg& seg, int n, int m, float x, float bias_n) {
@@ -293,7 +301,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             const int c_first = cta_of(g, (uint64_t)tile * g.kb), c_last = cta_of(g, tend - 1);
             const bool whole = c_first == c_last;
             const int which = tile == cfirst_run_tile ? 0 : 1;
-            float* prow = g.partial + (((size_t)c * 2 + which) * kBN + row) * g.Mp;
+            float* prow = g.partial + ((size_t)c * 2 + which) * (size_t)g.Mp * kBN + row;
             const int b = nacc == 2 ? (run & 1) : 0;
             const int use = nacc == 2 ? (run >> 1) : run;
             mbar_wait(&tmem_full[b], (uint32_t)use & 1u);
@@ -301,18 +309,19 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             float v[16];
             for (int col = 0; col < g.Mp; col += 16) {
                 tmem_ld16(tmem_base + (uint32_t)b * nbuf + ((uint32_t)(q * 32) << 16) + (uint32_t)col, v);
-                if (!whole) {
+                if (!whole) {              // token-major partial: one 128-B store per warp per token
 #pragma unroll
-                    for (int j = 0; j < 16; j += 4)
-                        *reinterpret_cast<float4*>(prow + col + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    for (int j = 0; j < 16; ++j) prow[(size_t)(col + j) * kBN] = v[j];
                 } else if (nvalid) {
-                    for (int j = 0; j < 16 && col + j < g.M; ++j) epi_store(g, seg, n, col + j, v[j], bias_n);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (col + j < g.M) epi_store(g, seg, n, col + j, v[j], bias_n);
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[b])) : "memory");
-            if (!whole) {
+            if (!whole && !g.ext_fixup) {
                 // fix-up: the last CTA to finish a run of this tile sums all runs in k order
                 __threadfence();
                 asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -321,52 +330,34 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                 if (s_last) {
                     __threadfence();
                     if (nvalid) {
-                        const int first_tile_of_cf = (int)(ubeg(g, c_first) / g.kb);
-                        // 16 outputs per step; two runs per iteration so 8 independent float4
-                        // loads are in flight; the sums stay in fixed run (k) order
-                        auto prow_of = [&](int cc) {
-                            const int wh = (cc == c_first && first_tile_of_cf != tile) ? 1 : 0;
-                            return reinterpret_cast<const float4*>(
-                                g.partial + (((size_t)cc * 2 + wh) * kBN + row) * g.Mp);
-                        };
-                        for (int m0 = 0; m0 < g.M; m0 += 16) {
-                            float4 acc[4];
+                        // 8 tokens per step, two runs per iteration: 16 coalesced loads in
+                        // flight per thread; the sums stay in fixed run (k) order
+                        for (int m0 = 0; m0 < g.M; m0 += 8) {
+                            float acc[8];
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
                             int cc = c_first;
                             for (; cc + 1 <= c_last; cc += 2) {
-                                const float4* p0 = prow_of(cc) + m0 / 4;
-                                const float4* p1 = prow_of(cc + 1) + m0 / 4;
-                                float4 a[4], b[4];
+                                const float* p0 = partial_run(g, cc, c_first, tile, row) + (size_t)m0 * kBN;
+                                const float* p1 = partial_run(g, cc + 1, c_first, tile, row) + (size_t)m0 * kBN;
+                                float a[8], b[8];
 #pragma unroll
-                                for (int j = 0; j < 4; ++j) a[j] = __ldcg(p0 + j);
+                                for (int j = 0; j < 8; ++j) a[j] = __ldcg(p0 + j * kBN);
 #pragma unroll
-                                for (int j = 0; j < 4; ++j) b[j] = __ldcg(p1 + j);
+                                for (int j = 0; j < 8; ++j) b[j] = __ldcg(p1 + j * kBN);
 #pragma unroll
-                                for (int j = 0; j < 4; ++j) {
-                                    acc[j].x += a[j].x; acc[j].y += a[j].y; acc[j].z += a[j].z; acc[j].w += a[j].w;
-                                }
+                                for (int j = 0; j < 8; ++j) acc[j] += a[j];
 #pragma unroll
-                                for (int j = 0; j < 4; ++j) {
-                                    acc[j].x += b[j].x; acc[j].y += b[j].y; acc[j].z += b[j].z; acc[j].w += b[j].w;
-                                }
+                                for (int j = 0; j < 8; ++j) acc[j] += b[j];
                             }
                             if (cc == c_last) {
-                                const float4* p0 = prow_of(cc) + m0 / 4;
+                                const float* p0 = partial_run(g, cc, c_first, tile, row) + (size_t)m0 * kBN;
 #pragma unroll
-                                for (int j = 0; j < 4; ++j) {
-                                    const float4 a = __ldcg(p0 + j);
-                                    acc[j].x += a.x; acc[j].y += a.y; acc[j].z += a.z; acc[j].w += a.w;
-                                }
+                                for (int j = 0; j < 8; ++j) acc[j] += __ldcg(p0 + j * kBN);
                             }
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                const int m = m0 + 4 * j;
-                                if (m < g.M) epi_store(g, seg, n, m, acc[j].x, bias_n);
-                                if (m + 1 < g.M) epi_store(g, seg, n, m + 1, acc[j].y, bias_n);
-                                if (m + 2 < g.M) epi_store(g, seg, n, m + 2, acc[j].z, bias_n);
-                                if (m + 3 < g.M) epi_store(g, seg, n, m + 3, acc[j].w, bias_n);
-                            }
+                            for (int j = 0; j < 8; ++j)
+                                if (m0 + j < g.M) epi_store(g, seg, n, m0 + j, acc[j], bias_n);
                         }
                     }
                     if (row == 0) g.counters[tile] = 0;   // ready for the next launch
@@ -379,6 +370,36 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
+}
+
+// Split-tile reduction as its own grid (ext_fixup, large M): CTA (tile, 16-token group), thread =
+// weight row. Same fixed run order as the in-kernel fix-up, so the bits do not depend on which
+// of the two reduces (the choice may follow M; the split itself never does).
+__global__ void __launch_bounds__(kBN) tc_fixup_kernel(TcArgs g) {
+    pdl_wait();                                    // every partial of the GEMM is written
+    pdl_trigger();
+    const int tile = blockIdx.x, row = threadIdx.x, m0 = blockIdx.y * 16;
+    const uint64_t tend = (uint64_t)(tile + 1) * g.kb;
+    const int c_first = cta_of(g, (uint64_t)tile * g.kb), c_last = cta_of(g, tend - 1);
+    if (c_first == c_last || m0 >= g.M) return;   // whole tile: stored by the GEMM itself
+    const TcSeg& seg = g.seg[seg_of(g, tile)];
+    const int n = (tile - seg.tile0) * kBN + row;
+    if (n >= seg.N) return;
+    const float bias_n = seg.bias ? __bfloat162float(seg.bias[n]) : 0.f;
+    float acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+    for (int cc = c_first; cc <= c_last; ++cc) {
+        const float* p = partial_run(g, cc, c_first, tile, row) + (size_t)m0 * kBN;
+        float t[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) t[j] = __ldcg(p + j * kBN);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] += t[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+        if (m0 + j < g.M) epi_store(g, seg, n, m0 + j, acc[j], bias_n);
 }
 
 // ----------------------------------------------------------------------------- host side
@@ -450,6 +471,13 @@ static int sm_count() {
 static int env_int(const char* n, int dflt) {
     const char* e = getenv(n);
     return e ? atoi(e) : dflt;
+}
+
+// tokens (padded) from which split tiles are reduced by a separate wide grid: a single CTA
+// summing ~8 runs of 128 x Mp fp32 partials serialises the tail of the GEMM at large M
+static int tc_ext_fixup_min() {
+    static int v = env_int("MPSW_TC_EXT_MIN", 64);
+    return v;
 }
 
 static int tc_ctas_per_sm() {
@@ -524,7 +552,9 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
         MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = smem;
     }
+    g.ext_fixup = Mp >= tc_ext_fixup_min() ? 1 : 0;
     launch_pdl(tc_gemm_kernel, g.G, kThreads, smem, st, m0, m1, m2, mx, g);
+    if (g.ext_fixup) launch_pdl(tc_fixup_kernel, dim3(tiles, Mp / 16), kBN, 0, st, g);
     MPSW_CU(cudaGetLastError());
 }
 

@@ -18,6 +18,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
         print(json.dumps(row), flush=True)
     sys.exit(0)
 configs = [("2", {})]
+if len(sys.argv) > 1 and sys.argv[1] == "ext":
+    configs = [("2", {"MPSW_TC_EXT_MIN": v}) for v in ("16", "32", "64", "100000")]
 for impl, env in configs:
     e = dict(os.environ); e.update(env)
     subprocess.run([sys.executable, __file__, "child", impl], env=e)
