@@ -723,6 +723,28 @@ extern "C" mpsw_status mpsw_bench_gemm(int device, int impl, int M, int N, int K
         float ms = 0;
         MPSW_CU(cudaEventElapsedTime(&ms, e0, e1));
         *us = ms * 1000.f / reps;
+        // dev: MPSW_TC_TRACE=path dumps per-CTA phase stamps of one more (PDL back-to-back) launch
+        if (const char* tp = getenv("MPSW_TC_TRACE"); tp && impl == 2) {
+            const int G = tc_grid_for(N, K);
+            unsigned long long* dT;
+            MPSW_CU(cudaMalloc(&dT, (size_t)G * 8 * 8));
+            MPSW_CU(cudaMemset(dT, 0, (size_t)G * 8 * 8));
+            run();
+            tc_set_trace(dT);
+            run();
+            tc_set_trace(nullptr);
+            run();
+            MPSW_CU(cudaStreamSynchronize(st));
+            std::vector<unsigned long long> h((size_t)G * 8);
+            MPSW_CU(cudaMemcpy(h.data(), dT, h.size() * 8, cudaMemcpyDeviceToHost));
+            cudaFree(dT);
+            if (FILE* f = fopen(tp, "a")) {
+                fprintf(f, "{\"M\":%d,\"N\":%d,\"K\":%d,\"G\":%d,\"t\":[", M, N, K, G);
+                for (size_t i = 0; i < h.size(); ++i) fprintf(f, "%s%llu", i ? "," : "", h[i]);
+                fprintf(f, "]}\n");
+                fclose(f);
+            }
+        }
         cudaEventDestroy(e0); cudaEventDestroy(e1); cudaStreamDestroy(st);
         cudaFree(dW); cudaFree(dX); cudaFree(dO); cudaFree(dP); cudaFree(dCnt);
         return MPSW_OK;

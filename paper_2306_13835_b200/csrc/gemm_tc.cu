@@ -30,7 +30,7 @@ namespace {
 
 constexpr int kBK = 64;             // K elements per stage (128 bytes of bf16 = one swizzle row)
 constexpr int kBN = 128;            // weight rows per tile (MMA M)
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 12;
 constexpr int kThreads = 256;
 constexpr uint32_t kTileABytes = kBN * kBK * 2;   // 16 KB
 
@@ -63,6 +63,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "memory");
         if (it > (1u << 26)) __trap();
     }
+}
+
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1) : "memory");
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -131,7 +135,18 @@ struct TcArgs {
     float* partial;              // [G][2][Mp][128]: a CTA's first / last partial run (row fastest)
     int* counters;               // [tiles], self-resetting
     int ext_fixup;               // 1: split tiles are reduced by tc_fixup_kernel, not in-kernel
+    int nacc;                    // TMEM accumulator buffers (2 = epilogue overlaps the next run)
+    unsigned long long* trace;   // dev: [G][8] %globaltimer stamps per CTA phase, or null
+    int l2_prefetch;             // weight units per CTA prefetched into L2 before griddepcontrol.wait
 };
+
+__device__ __forceinline__ void stamp(const TcArgs& g, int c, int i) {
+    if (g.trace) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+        g.trace[c * 8 + i] = t;
+    }
+}
 
 // Stream-K work split: CTA c owns units [ubeg(c), ubeg(c+1)) of the linearised (tile, k-block)
 // space. Depends only on (tiles, kb, G) — never on M — so it is batch-invariant.
@@ -189,10 +204,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
     const uint64_t u0 = ubeg(g, c), u1 = ubeg(g, c + 1);
     pdl_trigger();                                 // let the next kernel's CTAs get scheduled
     if (u0 >= u1) return;                          // uniform for the whole CTA
+    if (threadIdx.x == 0) stamp(g, c, 0);          // phase 0: CTA start
     uint32_t nbuf = 32;                            // TMEM columns per accumulator: pow2 >= max(32, Mp)
     while ((int)nbuf < g.Mp) nbuf <<= 1;
-    // double-buffered accumulator while two CTAs per SM still fit in the 512 TMEM columns
-    const int nacc = nbuf <= 128 ? 2 : 1;
+    // double-buffered accumulator while every resident CTA's buffers fit in the 512 TMEM columns
+    const int nacc = g.nacc;
     const uint32_t ncols = (uint32_t)nacc * nbuf;
 
     if (warp == 0 && lane == 0) {
@@ -224,6 +240,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
         if (lane == 0) {                           // ---- TMA producer: continuous across tiles
             // Weights do not depend on the previous kernel: the first kStages weight tiles are in
             // flight before griddepcontrol.wait, overlapping the previous kernel's tail (PDL).
+            stamp(g, c, 1);                        // phase 1: prologue done (barriers, TMEM)
             const int pre = (int)(u1 - u0 < (uint64_t)kStages ? u1 - u0 : (uint64_t)kStages);
             for (int i = 0; i < pre; ++i) {
                 const uint64_t u = u0 + i;
@@ -233,7 +250,19 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                 mbar_expect_tx(&full[i], kTileABytes + tile_b_bytes);
                 tma_load_2d(sa + i * kTileABytes, mw, &full[i], kbi * kBK, (tile - g.seg[si].tile0) * kBN);
             }
+            // ...and the next l2_prefetch units go to L2, so the weight stream keeps HBM busy
+            // across the kernel boundary (the smem ring alone holds only `stages` units)
+            {
+                const uint64_t pe = u0 + pre + (uint64_t)g.l2_prefetch < u1 ? u0 + pre + g.l2_prefetch : u1;
+                for (uint64_t u = u0 + pre; u < pe; ++u) {
+                    const int tile = (int)(u / g.kb), kbi = (int)(u % g.kb);
+                    const int si = seg_of(g, tile);
+                    const CUtensorMap* mw = si == 0 ? &map_w0 : (si == 1 ? &map_w1 : &map_w2);
+                    tma_prefetch_l2(mw, kbi * kBK, (tile - g.seg[si].tile0) * kBN);
+                }
+            }
             pdl_wait();
+            stamp(g, c, 2);                        // phase 2: previous kernel complete
             for (int i = 0; i < pre; ++i)
                 tma_load_2d(sb + i * tile_b_bytes, &map_x, &full[i], (int)((u0 + i) % g.kb) * kBK, 0);
             for (uint64_t u = u0 + pre; u < u1; ++u) {
@@ -272,6 +301,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                 }
                 mbar_wait(&full[s], ph);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (u == u0) stamp(g, c, 3);       // phase 3: first stage landed
                 const uint32_t a0 = smem_u32(sa + s * kTileABytes), b0 = smem_u32(sb + s * tile_b_bytes);
 #pragma unroll
                 for (int kk = 0; kk < kBK / 16; ++kk)
@@ -282,6 +312,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                     ++run;
                 }
             }
+            stamp(g, c, 4);                        // phase 4: last MMA issued
         }
     } else if (warp >= 4) {                        // ---- epilogue: TMEM lane = weight row
         pdl_wait();                                // outputs / partials written only after it
@@ -306,6 +337,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             const int use = nacc == 2 ? (run >> 1) : run;
             mbar_wait(&tmem_full[b], (uint32_t)use & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (row == 0 && rend == u1) stamp(g, c, 5);   // phase 5: last accumulator ready
             float v[16];
             for (int col = 0; col < g.Mp; col += 16) {
                 tmem_ld16(tmem_base + (uint32_t)b * nbuf + ((uint32_t)(q * 32) << 16) + (uint32_t)col, v);
@@ -321,14 +353,20 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[b])) : "memory");
+            if (row == 0 && rend == u1) stamp(g, c, 6);   // phase 6: last run drained
             if (!whole && !g.ext_fixup) {
-                // fix-up: the last CTA to finish a run of this tile sums all runs in k order
-                __threadfence();
+                // fix-up: the last CTA to finish a run of this tile sums all runs in k order.
+                // bar.sync orders the 128 threads' partial stores before thread 0's gpu-scope
+                // acq_rel atomic (release is cumulative); the acquire + bar.sync orders the
+                // reads of the other CTAs' partials after it. No full fences needed.
                 asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (row == 0) s_last = atomicAdd(&g.counters[tile], 1) == c_last - c_first;
+                if (row == 0) {
+                    int old;
+                    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(&g.counters[tile]) : "memory");
+                    s_last = old == c_last - c_first;
+                }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (s_last) {
-                    __threadfence();
                     if (nvalid) {
                         // 8 tokens per step, two runs per iteration: 16 coalesced loads in
                         // flight per thread; the sums stay in fixed run (k) order
@@ -369,6 +407,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (threadIdx.x == 0) stamp(g, c, 7);          // phase 7: CTA done
     if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
 }
 
@@ -480,6 +519,11 @@ static int tc_ext_fixup_min() {
     return v;
 }
 
+static int tc_l2_prefetch() {
+    static int v = env_int("MPSW_TC_L2PF", 0);   // measured: any prefetch depth slows the stream
+    return v;
+}
+
 static int tc_ctas_per_sm() {
     static int v = env_int("MPSW_TC_CPS", 2);
     return v;
@@ -506,6 +550,10 @@ int tc_stages(int Mp) {
 size_t tc_smem_bytes(int Mp) {
     return 1024 + tc_stages(Mp) * (kTileABytes + (size_t)Mp * kBK * 2) + (2 * kMaxStages + 4) * 8 + 16;
 }
+
+static unsigned long long* g_tc_trace = nullptr;   // dev instrumentation (mpsw_bench_gemm only)
+void tc_set_trace(unsigned long long* p) { g_tc_trace = p; }
+int tc_grid_for(int n_total, int K) { return tc_grid((n_total + kBN - 1) / kBN, K); }
 
 bool tc_supported(int M, int K) { return M >= 1 && M <= 256 && K % 8 == 0; }
 
@@ -553,6 +601,11 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
         attr_set = smem;
     }
     g.ext_fixup = Mp >= tc_ext_fixup_min() ? 1 : 0;
+    g.trace = g_tc_trace;
+    g.l2_prefetch = tc_l2_prefetch();
+    int nbuf = 32;
+    while (nbuf < Mp) nbuf <<= 1;
+    g.nacc = 2 * nbuf * tc_ctas_per_sm() <= 512 ? 2 : 1;
     launch_pdl(tc_gemm_kernel, g.G, kThreads, smem, st, m0, m1, m2, mx, g);
     if (g.ext_fixup) launch_pdl(tc_fixup_kernel, dim3(tiles, Mp / 16), kBN, 0, st, g);
     MPSW_CU(cudaGetLastError());

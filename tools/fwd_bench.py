@@ -1,5 +1,6 @@
 """Steady-state forward timing through the C-ABI (dev tool): one resident model, back-to-back
-blocking batches, per-batch device time from the library's CUDA events; SIMT vs tcgen05 GEMMs."""
+blocking batches, per-batch device time from the library's CUDA events; SIMT vs tcgen05 GEMMs.
+usage: python tools/fwd_bench.py [model=opt-13b] [tc]"""
 import json
 import sys
 import time
@@ -15,28 +16,35 @@ name = sys.argv[1] if len(sys.argv) > 1 else "opt-13b"
 d = opt_dims(name)
 S = layout.shard_bytes(d, 1)
 for B, L in [(1, 2), (8, 8), (32, 8)]:
-    for impl in (1, 2):
+    for impl in ((2,) if "tc" in sys.argv[2:] else (1, 2)):
         with M.Ctx(device_ids=(0,), budget=S + 4096, max_batch=B, max_tokens=L, gemm_impl=impl) as ctx:
             m = ctx.register_model(d)
             ctx.synth_fill(m, 1)
             ctx.wait(ctx.swap_in(m))
             toks = [request_tokens(0, 0, i, L, d.vocab) for i in range(B)]
-            outs = [np.empty(d.vocab, np.float32) for _ in range(B)]
-            for it in range(3):
-                rids = [ctx.request(m, t, o)[0] for t, o in zip(toks, outs)]
-                for r in rids:
+            outs = [[np.empty(d.vocab, np.float32) for _ in range(B)] for _ in range(2)]
+
+            def submit(k):
+                return [ctx.request(m, t, o)[0] for t, o in zip(toks, outs[k % 2])]
+
+            # pipelined: round i+1 is queued while round i's batch runs, so after the first round
+            # every batch holds exactly B requests (D = 1 dynamic batching)
+            warm, n = 3, 10
+            pending = submit(0)
+            for it in range(warm + n):
+                nxt = submit(it + 1)
+                for r in pending:
                     ctx.wait_request(r, 60)
-            s0 = ctx.stats()
-            t0 = time.perf_counter()
-            n = 10
-            for it in range(n):
-                rids = [ctx.request(m, t, o)[0] for t, o in zip(toks, outs)]
-                for r in rids:
-                    ctx.wait_request(r, 60)
+                pending = nxt
+                if it == warm - 1:
+                    s0 = ctx.stats()
+                    t0 = time.perf_counter()
+            for r in pending:
+                ctx.wait_request(r, 60)
             wall = (time.perf_counter() - t0) / n
             s1 = ctx.stats()
             nb = s1["fwd_gpu_n"] - s0["fwd_gpu_n"]
             ms = (s1["fwd_gpu_us_sum"] - s0["fwd_gpu_us_sum"]) / 1e3 / max(1, nb)
-            print(json.dumps({"model": name, "B": B, "L": L, "impl": ["", "simt", "tcgen05"][impl], "batches": nb,
+            print(json.dumps({"model": name, "B": B, "L": L, "impl": ["", "simt", "tcgen05"][impl], "batches": nb, "batch_rows": B * L,
                               "fwd_ms_device": ms, "GBps": S / (ms / 1e3) / 1e9, "wall_ms_per_round": wall * 1e3}),
                   flush=True)
