@@ -6,7 +6,8 @@
  * parallel configuration). Inside the library there is one engine thread (the paper's
  * centralised engine) and one worker thread per rank. Each rank owns:
  *   - a parameter region of `param_budget_bytes_per_gpu` bytes in HBM, allocated ONCE at
- *     mpsw_init and carved into k = floor(budget / S_r) slots (reading #8);
+ *     mpsw_init; models are placed in it first-fit (readings #8, #28; equal-size
+ *     models: k = floor(budget / S_r) slots);
  *   - a compute stream plus two copy streams, load (H2D) and offload (D2H) ("two
  *     additional streams to run loading and offloading operations concurrently");
  *   - page-locked host arenas, one contiguous blob per (model, rank) ("the parameters
@@ -56,13 +57,17 @@ enum { MPSW_SWAP_AUTO = 0, MPSW_SWAP_COPY_ENGINE = 1, MPSW_SWAP_ZERO_COPY = 2,
        MPSW_SWAP_HYBRID = 3 /* ablation: CE head + zero-copy tail of one shard concurrently */ };
 enum { MPSW_EVICTED = 0, MPSW_LOADING = 1, MPSW_RESIDENT = 2, MPSW_OFFLOADING = 3 };
 
-typedef struct mpsw_ctx mpsw_ctx;   /* opaque; owns arenas, slots, streams, threads */
+typedef struct mpsw_ctx mpsw_ctx;   /* opaque; owns arenas, the region, streams, threads */
+
+/* OPT shape (HF OPTConfig: num_hidden_layers, hidden_size, num_attention_heads, ffn_dim,
+ * vocab_size, max_position_embeddings) */
+typedef struct { int n_layers, hidden, heads, ffn, vocab, max_pos; } mpsw_opt_dims;
 
 typedef struct {
     int n_gpus;                   /* ranks driven by THIS process (tp*pp, or 1 in multi-process) */
     const int* device_ids;        /* n_gpus CUDA ordinals (caller-owned, read during init)     */
     int tp;                       /* TP degree t: tp * pp == n_gpus, or tp == world_size       */
-    uint64_t param_budget_bytes_per_gpu;  /* parameter slots per rank (the swapping budget)    */
+    uint64_t param_budget_bytes_per_gpu;  /* parameter region per rank (the swapping budget)   */
     uint64_t workspace_bytes_per_gpu;     /* 0 = auto (activations, partials, logits staging)  */
     int max_batch;                /* requests per batch entry, 1..256 (P:168 uses 8, P:196 32) */
     int max_tokens;               /* tokens per request, 1..128 (P:138 uses 2, P:166 uses 8)   */
@@ -82,9 +87,11 @@ typedef struct {
     const int* helper_device_ids; /* NVLink fan-in (NEXT-2; single process): GPUs whose PCIe    */
     int n_helpers;                /* links also pull chunks of every swap-in and forward them   */
                                   /* to the owner over NVLink; 0 = off (copy-engine mode only)  */
+    mpsw_opt_dims max_dims;
+                                  /* heterogeneous models (NEXT-4): the forward workspace is     */
+                                  /* sized for hidden/ffn/vocab up to these; all zero = the dims */
+                                  /* of the first registered model (later ones must not exceed)  */
 } mpsw_config;
-
-typedef struct { int n_layers, hidden, heads, ffn, vocab, max_pos; } mpsw_opt_dims;
 
 typedef struct {
     char name[64];                /* HF parameter name, e.g. "decoder.layers.3.fc1.weight"    */
@@ -118,9 +125,13 @@ mpsw_status mpsw_shard_layout(const mpsw_opt_dims* dims, int tp, int pp, int sta
  * array of tp caller-owned host blobs in the mpsw_shard_layout format, each of
  * shard_bytes[r] == S_r bytes; they are COPIED into library-owned pinned arenas before
  * return. shards == NULL allocates the arenas and leaves them for in-place filling via
- * mpsw_model_arena / mpsw_synth_fill. All models of a ctx must have identical dims
- * (homogeneous slots). The model starts EVICTED.
- * Errors: EINVAL (dims/tp/sizes), ENOMEM (budget < S_r, or pinning failed). */
+ * mpsw_model_arena / mpsw_synth_fill. Models may differ in size (NEXT-4, §6): every rank's
+ * region of budget bytes holds each resident model in one range of size(m) = max_r S_r(m)
+ * rounded up to 4 KiB, at the same offset on every rank, placed first-fit (DESIGN.md reading
+ * #28); equal-size models reduce to k = floor(budget / size) slots. hidden, ffn and vocab must
+ * not exceed mpsw_config.max_dims (or the first registered model's). The model starts EVICTED.
+ * Errors: EINVAL (dims/tp/sizes, or beyond the workspace dims), ENOMEM (budget < size(m), or
+ * pinning failed). */
 mpsw_status mpsw_register_model(mpsw_ctx* ctx, const mpsw_opt_dims* dims, int tp,
                                 const void* const* shards, const uint64_t* shard_bytes,
                                 int* model_id);
@@ -138,13 +149,13 @@ mpsw_status mpsw_synth_fill(mpsw_ctx* ctx, int model_id, int rank, uint64_t mode
  * accepted on the leader only (EINVAL on followers); mpsw_checksum / mpsw_peek / mpsw_wait /
  * mpsw_entry_gpu_ms / mpsw_residency act on the calling process's rank. */
 
-/* Explicit load entry: asynchronously copy every rank's shard into a free slot.
- * Goes through the engine queue, ordered with requests. *ticket identifies the entry.
- * OK with an already-complete ticket if RESIDENT or LOADING (no-op). ENOMEM if no slot
- * is free (explicit swaps never evict), EBUSY if the model is OFFLOADING. */
+/* Explicit load entry: asynchronously copy every rank's shard into the lowest free
+ * range of the region that fits it. Goes through the engine queue, ordered with requests.
+ * *ticket identifies the entry. OK with an already-complete ticket if RESIDENT or LOADING
+ * (no-op). ENOMEM if no free range fits (explicit swaps never evict), EBUSY if OFFLOADING. */
 mpsw_status mpsw_swap_in(mpsw_ctx* ctx, int model_id, uint64_t* ticket);
 
-/* Explicit offload entry: write the slot back to the arena (writeback=1) and free it.
+/* Explicit offload entry: write the model's range back to the arena (writeback=1), free it.
  * EBUSY if the model has in-flight batches or is LOADING (eviction never races a request).
  * OK no-op if EVICTED/OFFLOADING. */
 mpsw_status mpsw_swap_out(mpsw_ctx* ctx, int model_id, uint64_t* ticket);
@@ -181,11 +192,11 @@ mpsw_status mpsw_wait_request(mpsw_ctx* ctx, int64_t request_id, double timeout_
                               double* t_arrival, double* t_done);
 
 /* 64-bit order-independent checksum (C4) of (model, rank)'s bytes:
- * on_device = 1 hashes the resident slot with the sm_100a checksum kernel (EINVAL unless
+ * on_device = 1 hashes the resident range with the sm_100a checksum kernel (EINVAL unless
  * RESIDENT); on_device = 0 hashes the pinned host arena on the host. */
 mpsw_status mpsw_checksum(mpsw_ctx* ctx, int model_id, int rank, int on_device, uint64_t* out);
 
-/* Copy `bytes` at `offset` of a RESIDENT model's device slot (rank) into host `dst`
+/* Copy `bytes` at `offset` of a RESIDENT model's device range (rank) into host `dst`
  * (verification: sampled parity against the oracle). */
 mpsw_status mpsw_peek(mpsw_ctx* ctx, int model_id, int rank, uint64_t offset, uint64_t bytes,
                       void* dst);
@@ -193,7 +204,11 @@ mpsw_status mpsw_peek(mpsw_ctx* ctx, int model_id, int rank, uint64_t offset, ui
 /* MPSW_EVICTED / LOADING / RESIDENT / OFFLOADING as seen by the engine. */
 mpsw_status mpsw_residency(mpsw_ctx* ctx, int model_id, int* state);
 
-/* Write the recorded events and decisions, in engine order, as NDJSON (trace = 1). */
+/* Write the recorded events and decisions, in engine order, as NDJSON (trace = 1). The first
+ * line is {"cfg": {"cap", "sizes", "acks", "max_batch", "D"}}: the state machine's
+ * configuration (region bytes, placement bytes per model, acks per entry), enough to replay
+ * the log through the oracle scheduler. Decisions: {"dec": "load"|"offload", "id", "model",
+ * "off"} (byte offset in every rank's region), {"dec": "batch"|"complete", "id", "rids"}, ... */
 mpsw_status mpsw_trace_dump(mpsw_ctx* ctx, const char* ndjson_path);
 
 /* Write this process's device timeline as NDJSON (trace = 1): one line per finished entry per
@@ -208,10 +223,12 @@ typedef struct {
     uint64_t swaps_in, swaps_out; /* load / offload entries completed                       */
     uint64_t batches, requests;   /* batch entries / requests completed                     */
     uint64_t rejected;            /* requests rejected with ENOENT                          */
-    int k_slots;                  /* slots per rank (0 before the first registration)       */
-    uint64_t shard_bytes;         /* S_r                                                    */
+    int k_slots;                  /* floor(region / size(model 0)): the slot count for      */
+                                  /* equal-size models (0 before the first registration)    */
+    uint64_t shard_bytes;         /* S_r of model 0 on rank 0                               */
     uint64_t fwd_gpu_us_sum;      /* sum of per-batch forward device time (first local rank) */
     uint64_t fwd_gpu_n;           /* batches in that sum                                    */
+    uint64_t region_bytes;        /* parameter region per rank (budget rounded down to 4 KiB) */
 } mpsw_stats;
 
 mpsw_status mpsw_get_stats(mpsw_ctx* ctx, mpsw_stats* out);

@@ -9,9 +9,14 @@ later batches for other models proceed), P:114 ("scheduled in batches based on t
 timestamp", "LRU replacement policy"), P:129 (offload submitted first, overlapped with load).
 Readings (DESIGN.md): #1 global oldest head, ties by registration order; #2 take what is
 queued up to max_batch; #3 last_use = batch submission time; #4 victim eligibility; #5
-chunk-paired in-place swap (victim's slot handed to the requester at once); #7 concurrent swaps
-allowed when slots permit; #21 tie-breaks by registration order; #24 requests for a LOADING
-model queue; #26 at most D batches in flight per TP group (default 1).
+chunk-paired in-place swap (victim's range handed to the requester at once); #7 concurrent swaps
+allowed when space permits; #21 tie-breaks by registration order; #24 requests for a LOADING
+model queue; #26 at most D batches in flight per TP group (default 1); #28 placement of models
+of different sizes (NEXT-4, §6): each rank's region holds `cap` bytes, model m occupies
+[off, off + size[m]) on every rank, loads go to the lowest-address free range that fits (first
+fit); with no fit, eligible victims are removed in victim-key order until a first fit exists and
+only the victims overlapping that range are offloaded. Equal sizes reduce to k slots
+(cap = k, size 1: off is the slot index).
 
 `Engine` is a deterministic state machine.  `step(event)` applies one event and returns the
 decisions it caused.  Two drivers use it:
@@ -34,6 +39,35 @@ class EngineConfig:
     tp: int
     max_batch: int
     max_inflight: int = 1       # D (reading #26)
+    cap: int = None             # region bytes per rank (reading #28); None: k_slots unit slots
+    sizes: list = None          # placement bytes per model; None: 1 each
+
+    def region(self):
+        return self.k_slots if self.cap is None else self.cap
+
+    def size(self, m):
+        return 1 if self.sizes is None else self.sizes[m]
+
+
+def config_from_trace(cfg):
+    """EngineConfig from the {"cfg": ...} header line of the engine's trace (mpsw_trace_dump)."""
+    c = cfg["cfg"]
+    return EngineConfig(len(c["sizes"]), 0, c["acks"], c["max_batch"], c["D"], cap=c["cap"], sizes=list(c["sizes"]))
+
+
+def read_trace(path):
+    """(EngineConfig, events, decisions) of an engine trace file."""
+    import json
+    cfg, evs, decs = None, [], []
+    for line in open(path):
+        o = json.loads(line)
+        if "cfg" in o:
+            cfg = config_from_trace(o)
+        elif "ev" in o:
+            evs.append(o)
+        else:
+            decs.append(o)
+    return cfg, evs, decs
 
 
 class InvariantViolation(Exception):
@@ -47,8 +81,7 @@ class Engine:
     state: list = field(init=False)
     last_use: list = field(init=False)
     outstanding: list = field(init=False)
-    owner: list = field(init=False)
-    slot_of: list = field(init=False)
+    off_of: list = field(init=False)         # model -> offset of its range, None if it owns none
     pending: dict = field(init=False)        # entry id -> [kind, model, acks left, set(ranks acked)]
     batches: dict = field(init=False)        # batch id -> (model, rids)
     inflight: int = 0
@@ -60,8 +93,7 @@ class Engine:
         self.state = [EVICTED] * n
         self.last_use = [float("-inf")] * n
         self.outstanding = [0] * n
-        self.owner = [None] * self.cfg.k_slots
-        self.slot_of = [None] * n
+        self.off_of = [None] * n
         self.pending = {}
         self.batches = {}
 
@@ -74,29 +106,32 @@ class Engine:
     def _head_key(self, m):
         return (self.queue[m][0][1], m)
 
-    def _load(self, m, slot, out):
+    def _load(self, m, off, out):
         e = self._eid()
-        self.owner[slot] = m
-        self.slot_of[m] = slot
+        self.off_of[m] = off
         self.state[m] = LOADING
         self.pending[e] = ["load", m, self.cfg.tp, set()]
-        out.append({"dec": "load", "id": e, "model": m, "slot": slot})
+        out.append({"dec": "load", "id": e, "model": m, "off": off})
 
     def _offload(self, v, out):
         e = self._eid()
-        slot = self.slot_of[v]
-        self.owner[slot] = None
-        self.slot_of[v] = None
+        off = self.off_of[v]
+        self.off_of[v] = None
         self.state[v] = OFFLOADING
         self.pending[e] = ["offload", v, self.cfg.tp, set()]
-        out.append({"dec": "offload", "id": e, "model": v, "slot": slot})
-        return slot
+        out.append({"dec": "offload", "id": e, "model": v, "off": off})
 
-    def _free_slot(self):
-        for s, o in enumerate(self.owner):
-            if o is None:
-                return s
-        return None
+    def _first_fit(self, need, without=()):
+        """Lowest offset o such that [o, o + need) lies in the region and overlaps no range
+        owned by a model outside `without`; None if there is none."""
+        owned = sorted((self.off_of[m], self.off_of[m] + self.cfg.size(m)) for m in range(self.cfg.n_models)
+                       if self.off_of[m] is not None and m not in without)
+        o = 0
+        for lo, hi in owned:
+            if lo - o >= need:
+                return o
+            o = max(o, hi)
+        return o if self.cfg.region() - o >= need else None
 
     # ---- SCHEDULE (P:74, P:114) ----------------------------------------------------------
     def schedule(self, now, out):
@@ -122,18 +157,26 @@ class Engine:
             elif st in (LOADING, OFFLOADING):
                 blocked.add(m)
             else:  # EVICTED
-                s = self._free_slot()
-                if s is not None:
-                    self._load(m, s, out)
+                need = self.cfg.size(m)
+                o = self._first_fit(need)
+                if o is not None:
+                    self._load(m, o, out)
                 else:
                     hk = self._head_key(m)
-                    vics = [v for v in range(self.cfg.n_models)
-                            if self.state[v] == RESIDENT and self.outstanding[v] == 0
-                            and (not self.queue[v] or self._head_key(v) > hk)]
-                    if vics:
-                        v = min(vics, key=lambda v: (1 if self.queue[v] else 0, self.last_use[v], v))
-                        s = self._offload(v, out)
-                        self._load(m, s, out)
+                    vics = sorted((v for v in range(self.cfg.n_models)
+                                   if self.state[v] == RESIDENT and self.outstanding[v] == 0
+                                   and (not self.queue[v] or self._head_key(v) > hk)),
+                                  key=lambda v: (1 if self.queue[v] else 0, self.last_use[v], v))
+                    for j in range(1, len(vics) + 1):
+                        o = self._first_fit(need, set(vics[:j]))
+                        if o is None:
+                            continue
+                        for w in vics[:j]:
+                            lo = self.off_of[w]
+                            if lo < o + need and o < lo + self.cfg.size(w):
+                                self._offload(w, out)
+                        self._load(m, o, out)
+                        break
                 blocked.add(m)
 
     # ---- events ----------------------------------------------------------------------------
@@ -176,11 +219,11 @@ class Engine:
             elif st == OFFLOADING:
                 out.append({"dec": "reject", "model": m, "status": "EBUSY"})
             else:
-                s = self._free_slot()
-                if s is None:
+                o = self._first_fit(self.cfg.size(m))
+                if o is None:
                     out.append({"dec": "reject", "model": m, "status": "ENOMEM"})
                 else:
-                    self._load(m, s, out)
+                    self._load(m, o, out)
         elif kind == "cmd_swap_out":
             m = ev["model"]
             st = self.state[m]
@@ -197,16 +240,24 @@ class Engine:
         return out
 
     def check(self):
-        """Invariants: owned slots <= k (by construction of owner[]), a model with in-flight
-        batches is RESIDENT, slot ownership consistent, inflight <= D."""
-        owned = [o for o in self.owner if o is not None]
-        if len(owned) != len(set(owned)):
-            raise InvariantViolation("model owns two slots")
+        """Invariants: owned ranges lie inside the region and never overlap (so bytes held per
+        rank <= cap <= budget), LOADING/RESIDENT models and only they own a range, a model with
+        in-flight batches is RESIDENT, inflight <= D."""
+        ranges = []
         for m in range(self.cfg.n_models):
             if self.outstanding[m] > 0 and self.state[m] != RESIDENT:
                 raise InvariantViolation(f"model {m} has in-flight batches but is {STATE_NAMES[self.state[m]]}")
-            if self.state[m] in (LOADING, RESIDENT) and self.owner[self.slot_of[m]] != m:
-                raise InvariantViolation("slot ownership")
+            owns = self.state[m] in (LOADING, RESIDENT)
+            if owns != (self.off_of[m] is not None):
+                raise InvariantViolation("range ownership")
+            if owns:
+                ranges.append((self.off_of[m], self.off_of[m] + self.cfg.size(m)))
+        ranges.sort()
+        for i, (lo, hi) in enumerate(ranges):
+            if lo < 0 or hi > self.cfg.region():
+                raise InvariantViolation("range outside the region")
+            if i and lo < ranges[i - 1][1]:
+                raise InvariantViolation("overlapping ranges")
         if self.inflight > self.cfg.max_inflight:
             raise InvariantViolation("D exceeded")
 
@@ -239,7 +290,8 @@ class Costs:
 def simulate(cfg: EngineConfig, costs: Costs, arrivals, token_len: int, blocking=False):
     """arrivals: list of (rid, model, t_arr) (open loop) or, with blocking=True, a list of
     (rid, model) issued one after the previous completes (P:127 alternating blocking).
-    Returns (events, decisions, t_done dict, entry_log) with events in processing order."""
+    Returns (events, decisions, t_done dict, entry_log) with events in processing order.
+    Models are equal-size here (one shard_bytes): the chunk gates are keyed by range offset."""
     eng = Engine(cfg)
     pq, seq = [], 0
 
@@ -287,7 +339,7 @@ def simulate(cfg: EngineConfig, costs: Costs, arrivals, token_len: int, blocking
                         d2h_free[r] = tt
                     else:                       # clean eviction: nothing to copy
                         tt, times = t, [t] * len(sizes)
-                    slot_chunk_free[(r, dcs["slot"])] = times
+                    slot_chunk_free[(r, dcs["off"])] = times
                     entry_log[dcs["id"]]["done"][r] = tt
                     push(tt, {"ev": "ack", "entry": dcs["id"], "rank": r})
             elif k == "load":
@@ -295,13 +347,13 @@ def simulate(cfg: EngineConfig, costs: Costs, arrivals, token_len: int, blocking
                 for r in range(tp):
                     extra = costs.rank_delay[r] if r < len(costs.rank_delay) else 0.0
                     tt = max(t, h2d_free[r]) + extra
-                    gate = slot_chunk_free.get((r, dcs["slot"]), [])
+                    gate = slot_chunk_free.get((r, dcs["off"]), [])
                     for i, c in enumerate(sizes):
                         if i < len(gate):
                             tt = max(tt, gate[i])
                         tt += costs.alpha + c / costs.b_in
                     h2d_free[r] = tt
-                    slot_chunk_free[(r, dcs["slot"])] = []
+                    slot_chunk_free[(r, dcs["off"])] = []
                     entry_log[dcs["id"]]["done"][r] = tt
                     push(tt, {"ev": "ack", "entry": dcs["id"], "rank": r})
             elif k == "batch":

@@ -13,6 +13,10 @@ Per rank, the parameter region is k slots of S_r bytes, each split into chunks o
   offload(v):              arena[v] := slot[s] (writeback) or untouched (clean eviction)
 Budget: every byte held by any model lives inside one of the k slots, so bytes held <= k*S_r
 <= budget at every instant (stricter than SPEC's slot count).
+
+`SwapModel` takes decisions of unit-size scheduler configs (off = slot index).
+`RegionSwapModel` is the byte-level version for models of different sizes (reading #28): the
+region of each rank is `cap` bytes and a model's shard lives at [off, off + S_m,r).
 """
 import numpy as np
 
@@ -71,13 +75,13 @@ class SwapModel:
             d = decisions[i]
             if d["dec"] == "offload":
                 nxt = decisions[i + 1] if i + 1 < len(decisions) else None
-                if nxt and nxt["dec"] == "load" and nxt["slot"] == d["slot"]:
-                    self.paired(d["slot"], nxt["model"])
+                if nxt and nxt["dec"] == "load" and nxt["off"] == d["off"]:
+                    self.paired(d["off"], nxt["model"])
                     i += 2
                     continue
-                self.offload(d["slot"])
+                self.offload(d["off"])
             elif d["dec"] == "load":
-                self.load(d["model"], d["slot"])
+                self.load(d["model"], d["off"])
             i += 1
 
     def expected_slot_hashes(self):
@@ -87,3 +91,48 @@ class SwapModel:
 
     def expected_host_hashes(self):
         return {m: [checksum(a) for a in ims] for m, ims in self.host.items()}
+
+
+class RegionSwapModel:
+    """C3 for models of different sizes (reading #28, NEXT-4). Per rank: one region of
+    `cap` bytes; a resident model m occupies [off_m, off_m + S_m,r). Decisions apply in engine
+    order: offload(v) writes v's bytes back to its arena (writeback) or leaves the arena
+    untouched (clean eviction) and frees the range; load(m, off) copies m's arena into
+    [off, off + S_m,r). The engine overlaps an offload with the loads that reuse its bytes
+    chunk by chunk, gating every load chunk on the D2H of the bytes it overwrites, which gives
+    exactly this sequential result."""
+
+    def __init__(self, images, cap, writeback=True):
+        """images: dict model -> list (per rank) of uint8 arrays (the C0 shard images)."""
+        self.host = {m: [im.copy() for im in ims] for m, ims in images.items()}
+        self.tp = len(next(iter(images.values())))
+        self.cap = cap
+        self.writeback = writeback
+        self.region = [np.zeros(cap, np.uint8) for _ in range(self.tp)]
+        self.off = {}
+
+    def apply(self, decisions):
+        for d in decisions:
+            m = d.get("model")
+            if d["dec"] == "offload":
+                o = self.off.pop(m)
+                assert o == d["off"], "offload of a range the model does not own"
+                if self.writeback:
+                    for r in range(self.tp):
+                        n = self.host[m][r].size
+                        self.host[m][r][:] = self.region[r][o:o + n]
+            elif d["dec"] == "load":
+                o = d["off"]
+                for r in range(self.tp):
+                    n = self.host[m][r].size
+                    assert o + n <= self.cap, "range beyond the region"
+                    for w, ow in self.off.items():     # never overwrite a resident model
+                        nw = self.host[w][r].size
+                        assert ow + nw <= o or o + n <= ow, "load overlaps a resident model"
+                    self.region[r][o:o + n] = self.host[m][r]
+                self.off[m] = o
+
+    def expected_resident_hashes(self):
+        """{model: [hash per rank]} of every model the decisions left resident."""
+        return {m: [checksum(self.region[r][o:o + self.host[m][r].size]) for r in range(self.tp)]
+                for m, o in self.off.items()}

@@ -7,9 +7,9 @@
 namespace mpsw {
 
 void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
-    const FwdShape& s = R.fs;
+    const FwdShape& s = c->models[e.model]->fs[R.local];
     const int B = e.B, M = e.M;
-    const TensorPtrs& Wt = R.wptr[e.slot];
+    const TensorPtrs& Wt = R.wptr[e.model];      // set by this worker when it issued the load
     cudaStream_t cs = R.compute;
     const int r = R.index, t = c->tp;
     const int g0 = R.stage * t;                    // first global rank of my stage
@@ -92,7 +92,7 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
     c->launches += nl;
 }
 
-// Weight pointers of one rank's slot, looked up by HF name in that rank's layout (stage-local
+// Weight pointers of one model's range on one rank, looked up by HF name in that rank's layout (stage-local
 // layers only; embeddings / final LN only where the stage holds them).
 TensorPtrs make_ptrs(const Layout& L, const uint8_t* base, int layer0, int n_layers) {
     std::unordered_map<std::string, const void*> by;

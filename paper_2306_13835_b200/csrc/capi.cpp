@@ -110,6 +110,7 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
         R->numa = gpu_numa_node(dev);
         R->last_compute.reserve(kMaxModels);
         R->last_compute_valid.reserve(kMaxModels);
+        R->wptr.reserve(kMaxModels);
         c->local_of[R->index] = l;
         MPSW_CU(cudaSetDevice(dev));
         int hp = 0, lp = 0;
@@ -252,10 +253,8 @@ mpsw_status mpsw_shutdown(mpsw_ctx* c) {
     for (auto ev : c->ipc_ev_opened) cudaEventDestroy(ev);
     for (auto& R : c->ranks) {
         cudaSetDevice(R->device);
-        for (auto& sl : R->slots) {
-            for (auto ev : sl.chunk_gate) cudaEventDestroy(ev);
-            if (sl.whole_gate) cudaEventDestroy(sl.whole_gate);
-        }
+        for (auto& g : R->gates) cudaEventDestroy(g.ev);
+        R->gates.clear();
         for (auto ev : R->ev_point)
             if (ev) cudaEventDestroy(ev);
         if (R->ev_stage) cudaEventDestroy(R->ev_stage);
@@ -306,25 +305,41 @@ mpsw_status mpsw_register_model(mpsw_ctx* c, const mpsw_opt_dims* dims, int tp, 
     if (group_poisoned(c)) return set_error(MPSW_ECUDA, "ctx poisoned: " + c->poison_msg);
     if (tp != c->tp) return set_error(MPSW_EINVAL, "model tp must equal the ctx tp");
     std::lock_guard<std::mutex> api(c->api_mu);
-    Layout L;
-    mpsw_status s = compute_layout(*dims, tp, c->pp, 0, 0, c->cfg.dtype, L);
-    if (s != MPSW_OK) return s;
-    {
-        std::lock_guard<std::mutex> lk(c->cmd_mu);
-        if (!c->geom) setup_geometry(c, *dims);
-        else if (std::memcmp(&c->dims, dims, sizeof(*dims)) != 0)
-            return set_error(MPSW_EINVAL, "all models of a ctx must share dims (homogeneous slots, P:229)");
-    }
-    if (shards && shard_bytes)
-        for (auto& R : c->ranks)
-            if (shards[R->index] && shard_bytes[R->index] != R->S)
-                return set_error(MPSW_EINVAL, "shard_bytes != S_r of the layout");
     auto m = std::make_unique<Model>();
     m->dims = *dims;
+    for (int g = 0; g < c->nr; ++g) {       // every global rank's shard (stage-dependent)
+        Layout L;
+        mpsw_status s = compute_layout(*dims, tp, c->pp, g / tp, g % tp, c->cfg.dtype, L);
+        if (s != MPSW_OK) return s;
+        m->rank_S[g] = L.bytes;
+        m->size = std::max(m->size, (L.bytes + kSlotAlign - 1) / kSlotAlign * kSlotAlign);
+    }
+    {
+        std::lock_guard<std::mutex> lk(c->cmd_mu);
+        if (!c->geom) {
+            const mpsw_opt_dims& x = c->cfg.max_dims;
+            const bool given = x.hidden > 0 && x.ffn > 0 && x.vocab > 0 && x.heads > 0;
+            check_dims(c, *dims);
+            setup_geometry(c, given ? x : *dims);
+        }
+    }
+    check_dims(c, *dims);                   // kernel limits + fits the workspace
+    if (m->size > c->cap)
+        return set_error(MPSW_ENOMEM, "param budget cannot hold the model (size " + std::to_string(m->size) + " B)");
+    if (shards && shard_bytes)
+        for (auto& R : c->ranks)
+            if (shards[R->index] && shard_bytes[R->index] != m->rank_S[R->index])
+                return set_error(MPSW_EINVAL, "shard_bytes != S_r of the layout");
     try {
         for (auto& R : c->ranks) {
-            m->arena.push_back(pin_alloc(R->S, R->numa));
-            if (shards && shards[R->index]) parallel_memcpy(m->arena.back().p, (const uint8_t*)shards[R->index], R->S);
+            Layout L;
+            if (compute_layout(*dims, tp, c->pp, R->stage, R->trank, c->cfg.dtype, L) != MPSW_OK)
+                throw Error(MPSW_EINVAL, tls_error());
+            m->layout.push_back(L);
+            m->fs.push_back(fwd_shape(c, *dims, *R));
+            const uint64_t S = m->rank_S[R->index];
+            m->arena.push_back(pin_alloc(S, R->numa));
+            if (shards && shards[R->index]) parallel_memcpy(m->arena.back().p, (const uint8_t*)shards[R->index], S);
         }
     } catch (...) {
         for (auto& a : m->arena) pin_free(a);
@@ -337,15 +352,17 @@ mpsw_status mpsw_register_model(mpsw_ctx* c, const mpsw_opt_dims* dims, int tp, 
         std::lock_guard<std::mutex> lk(R->mu);
         R->last_compute.push_back(ev);     // capacity reserved at init: no reallocation
         R->last_compute_valid.push_back(0);
+        R->wptr.emplace_back();
     }
     {
         std::lock_guard<std::mutex> lk(c->cmd_mu);
         std::lock_guard<std::mutex> lk2(c->sm_mu);
         std::lock_guard<std::mutex> lk3(c->f_mu);
         if (c->models.size() >= kMaxModels) return set_error(MPSW_ENOMEM, "too many models");
+        const uint64_t size = m->size;
         c->models.push_back(std::move(m));   // capacity reserved at init: no reallocation
-        c->sm.add_model();
-        c->f_slot_of.push_back(-1);
+        c->sm.add_model(size);
+        c->f_off_of.push_back(-1);
         c->f_state.push_back(ST_EVICTED);
         *model_id = (int)c->models.size() - 1;
     }
@@ -360,7 +377,7 @@ mpsw_status mpsw_model_arena(mpsw_ctx* c, int model_id, int rank, void** host, u
     const int li = local_index(c, rank);
     if (li < 0) return set_error(MPSW_EINVAL, "rank out of range or not driven by this process");
     if (host) *host = c->models[model_id]->arena[li].p;
-    if (bytes) *bytes = c->ranks[li]->S;
+    if (bytes) *bytes = c->models[model_id]->rank_S[c->ranks[li]->index];
     return MPSW_OK;
     API_END
 }
@@ -372,7 +389,7 @@ mpsw_status mpsw_synth_fill(mpsw_ctx* c, int model_id, int rank, uint64_t seed, 
     if (rank != -1 && local_index(c, rank) < 0) return set_error(MPSW_EINVAL, "rank out of range or not local");
     for (auto& R : c->ranks)
         if (rank < 0 || rank == R->index)
-            synth_fill_arena(c->dims, c->tp, c->pp, R->stage, R->trank, c->cfg.dtype, seed,
+            synth_fill_arena(c->models[model_id]->dims, c->tp, c->pp, R->stage, R->trank, c->cfg.dtype, seed,
                              c->models[model_id]->arena[R->local].p, threads);
     return MPSW_OK;
     API_END
@@ -473,10 +490,11 @@ mpsw_status mpsw_request(mpsw_ctx* c, int model_id, const int32_t* tokens, int n
         c->rejected++;
         return set_error(MPSW_ENOENT, "unknown model");
     }
-    if (n_tokens < 1 || n_tokens > c->cfg.max_tokens || n_tokens > c->dims.max_pos)
+    const mpsw_opt_dims& md = c->models[model_id]->dims;
+    if (n_tokens < 1 || n_tokens > c->cfg.max_tokens || n_tokens > md.max_pos)
         return set_error(MPSW_EINVAL, "n_tokens out of range");
     for (int i = 0; i < n_tokens; ++i)
-        if (tokens[i] < 0 || tokens[i] >= c->dims.vocab) return set_error(MPSW_EINVAL, "token id out of range");
+        if (tokens[i] < 0 || tokens[i] >= md.vocab) return set_error(MPSW_EINVAL, "token id out of range");
     auto rq = std::make_shared<ReqRec>();
     rq->model = model_id;
     rq->tokens.assign(tokens, tokens + n_tokens);
@@ -541,14 +559,14 @@ mpsw_status mpsw_wait_request(mpsw_ctx* c, int64_t rid, double timeout_s, double
     API_END
 }
 
-// Slot of a model that is resident as seen by this process (-1 otherwise).
-static int resident_slot(mpsw_ctx* c, int model_id) {
+// Region offset of a model that is resident as seen by this process (-1 otherwise).
+static int64_t resident_off(mpsw_ctx* c, int model_id) {
     if (c->leader) {
         std::lock_guard<std::mutex> lk(c->sm_mu);
-        return c->sm.state[model_id] == ST_RESIDENT ? c->sm.slot_of[model_id] : -1;
+        return c->sm.state[model_id] == ST_RESIDENT ? c->sm.off_of[model_id] : -1;
     }
     std::lock_guard<std::mutex> lk(c->f_mu);
-    return c->f_state[model_id] == ST_RESIDENT ? c->f_slot_of[model_id] : -1;
+    return c->f_state[model_id] == ST_RESIDENT ? c->f_off_of[model_id] : -1;
 }
 
 mpsw_status mpsw_residency(mpsw_ctx* c, int model_id, int* state) {
@@ -572,16 +590,17 @@ mpsw_status mpsw_checksum(mpsw_ctx* c, int model_id, int rank, int on_device, ui
     if (model_id < 0 || model_id >= (int)c->models.size()) return set_error(MPSW_ENOENT, "unknown model");
     const int li = local_index(c, rank);
     if (li < 0) return set_error(MPSW_EINVAL, "rank out of range or not driven by this process");
+    const uint64_t S = c->models[model_id]->rank_S[c->ranks[li]->index];
     if (!on_device) {
-        *out = host_checksum(c->models[model_id]->arena[li].p, c->ranks[li]->S, 0);
+        *out = host_checksum(c->models[model_id]->arena[li].p, S, 0);
         return MPSW_OK;
     }
-    const int slot = resident_slot(c, model_id);
-    if (slot < 0) return set_error(MPSW_EINVAL, "model not RESIDENT");
+    const int64_t off = resident_off(c, model_id);
+    if (off < 0) return set_error(MPSW_EINVAL, "model not RESIDENT");
     Rank& R = *c->ranks[li];
     MPSW_CU(cudaSetDevice(R.device));
     MPSW_CU(cudaMemsetAsync(R.d_sum, 0, 8, R.aux));
-    launch_checksum(R.slots[slot].base, R.S, R.d_sum, R.aux);
+    launch_checksum(R.region + off, S, R.d_sum, R.aux);
     c->launches += 2;
     unsigned long long h = 0;
     MPSW_CU(cudaMemcpyAsync(&h, R.d_sum, 8, cudaMemcpyDeviceToHost, R.aux));
@@ -596,12 +615,13 @@ mpsw_status mpsw_peek(mpsw_ctx* c, int model_id, int rank, uint64_t offset, uint
     if (!c || !dst) return set_error(MPSW_EINVAL, "NULL argument");
     if (model_id < 0 || model_id >= (int)c->models.size()) return set_error(MPSW_ENOENT, "unknown model");
     const int li = local_index(c, rank);
-    if (li < 0 || offset + bytes > c->ranks[li]->S) return set_error(MPSW_EINVAL, "rank or range");
-    const int slot = resident_slot(c, model_id);
-    if (slot < 0) return set_error(MPSW_EINVAL, "model not RESIDENT");
+    if (li < 0 || offset + bytes > c->models[model_id]->rank_S[c->ranks[li]->index])
+        return set_error(MPSW_EINVAL, "rank or range");
+    const int64_t off = resident_off(c, model_id);
+    if (off < 0) return set_error(MPSW_EINVAL, "model not RESIDENT");
     Rank& R = *c->ranks[li];
     MPSW_CU(cudaSetDevice(R.device));
-    MPSW_CU(cudaMemcpyAsync(dst, R.slots[slot].base + offset, bytes, cudaMemcpyDeviceToHost, R.aux));
+    MPSW_CU(cudaMemcpyAsync(dst, R.region + off + offset, bytes, cudaMemcpyDeviceToHost, R.aux));
     MPSW_CU(cudaStreamSynchronize(R.aux));
     return MPSW_OK;
     API_END
@@ -615,6 +635,12 @@ mpsw_status mpsw_trace_dump(mpsw_ctx* c, const char* path) {
     std::lock_guard<std::mutex> lk(c->trace_mu);
     std::ofstream f(path);
     if (!f) return set_error(MPSW_EINVAL, "cannot open trace path");
+    {
+        std::lock_guard<std::mutex> sl(c->sm_mu);
+        f << "{\"cfg\":{\"cap\":" << c->sm.cap << ",\"sizes\":[";
+        for (int m = 0; m < c->sm.n_models; ++m) f << (m ? "," : "") << c->sm.size[m];
+        f << "],\"acks\":" << c->sm.tp << ",\"max_batch\":" << c->sm.max_batch << ",\"D\":" << c->sm.D << "}}\n";
+    }
     for (const auto& l : c->trace_lines) f << l << "\n";
     return MPSW_OK;
     API_END
@@ -643,8 +669,9 @@ mpsw_status mpsw_get_stats(mpsw_ctx* c, mpsw_stats* o) {
     o->batches = c->n_batches.load();
     o->requests = c->n_requests.load();
     o->rejected = c->rejected.load();
-    o->k_slots = c->k;
-    o->shard_bytes = c->rank_S[0];
+    o->k_slots = c->models.empty() ? 0 : (int)(c->cap / c->models[0]->size);
+    o->shard_bytes = c->models.empty() ? 0 : c->models[0]->rank_S[0];
+    o->region_bytes = c->cap;
     o->fwd_gpu_us_sum = c->fwd_us_sum.load();
     o->fwd_gpu_n = c->fwd_n.load();
     return MPSW_OK;

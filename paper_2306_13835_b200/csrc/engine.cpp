@@ -1,5 +1,5 @@
 // mpsw runtime core: per-rank workers, the engine (scheduler) thread, the multi-process follower
-// and control plane, and the slot geometry. (Store: store.cpp; swap entries: swap.cpp; batch
+// and control plane, and the region / workspace geometry. (Store: store.cpp; swap entries: swap.cpp; batch
 // entries: batch.cpp; C-ABI: capi.cpp; types and the ctx: runtime.h.)
 //
 // Architecture (§3.1 Fig. 1, §3.2, §4):
@@ -124,8 +124,8 @@ void log_decisions(mpsw_ctx* c, const std::vector<Decision>& ds) {
     for (const auto& d : ds) {
         std::ostringstream o;
         switch (d.kind) {
-            case 0: o << "{\"dec\":\"load\",\"id\":" << d.id << ",\"model\":" << d.model << ",\"slot\":" << d.slot << "}"; break;
-            case 1: o << "{\"dec\":\"offload\",\"id\":" << d.id << ",\"model\":" << d.model << ",\"slot\":" << d.slot << "}"; break;
+            case 0: o << "{\"dec\":\"load\",\"id\":" << d.id << ",\"model\":" << d.model << ",\"off\":" << d.off << "}"; break;
+            case 1: o << "{\"dec\":\"offload\",\"id\":" << d.id << ",\"model\":" << d.model << ",\"off\":" << d.off << "}"; break;
             case 2:
             case 3: {
                 o << "{\"dec\":\"" << (d.kind == 2 ? "batch" : "complete") << "\",\"id\":" << d.id;
@@ -154,7 +154,7 @@ void publish(mpsw_ctx* c, const Entry& e) {
     rec.id = e.id;
     rec.kind = e.kind;
     rec.model = e.model;
-    rec.slot = e.slot;
+    rec.off = e.off;
     rec.ring = e.ring;
     rec.B = e.B;
     rec.M = e.M;
@@ -168,10 +168,10 @@ void dispatch(mpsw_ctx* c, const std::vector<Decision>& ds, double now) {
         e->id = d.id;
         e->kind = d.kind;
         e->model = d.model;
-        e->slot = d.slot;
+        e->off = d.off;
         e->t_submit = now;
         if (d.kind == E_BATCH) {
-            e->slot = c->sm.slot_of[d.model];
+            e->off = (uint64_t)c->sm.off_of[d.model];
             // pack tokens + meta into the pinned ring entry (shm in mp mode: every rank reads it)
             e->ring = c->ring_next;
             c->ring_next = (c->ring_next + 1) % c->ring_n;
@@ -218,7 +218,7 @@ void step_and_dispatch(mpsw_ctx* c, const std::function<void(std::vector<Decisio
 
 void complete_batch(mpsw_ctx* c, Entry& e, double now) {
     const uint8_t* ring = c->stg + (size_t)e.ring * c->ring_stride;
-    const int V = c->vocab;
+    const int V = c->models[e.model]->dims.vocab;
     for (size_t b = 0; b < e.reqs.size(); ++b) {
         auto& rq = e.reqs[b];
         std::memcpy(rq->out, (const float*)ring + b * (size_t)V, (size_t)V * 4);
@@ -301,8 +301,8 @@ bool poll_inflight(mpsw_ctx* c) {
                 log_event(c, "{\"ev\":\"ack\",\"t\":" + fmt_d(now) + ",\"entry\":" + std::to_string(e.id) +
                                  ",\"rank\":" + std::to_string(r) + "}");
                 step_and_dispatch(c, [&](std::vector<Decision>& ds) { c->sm.ack(e.id, r, now, ds); }, now);
-                if (e.kind == E_LOAD) c->h2d_bytes += c->rank_S[r];
-                else if (c->cfg.writeback) c->d2h_bytes += c->rank_S[r];
+                if (e.kind == E_LOAD) c->h2d_bytes += c->models[e.model]->rank_S[r];
+                else if (c->cfg.writeback) c->d2h_bytes += c->models[e.model]->rank_S[r];
             }
         }
         if (e.n_acked == c->nr) {
@@ -411,7 +411,7 @@ void follower_main(mpsw_ctx* c) {
             e->id = rec.id;
             e->kind = rec.kind;
             e->model = rec.model;
-            e->slot = rec.slot;
+            e->off = rec.off;
             e->ring = rec.ring;
             e->B = rec.B;
             e->M = rec.M;
@@ -422,8 +422,8 @@ void follower_main(mpsw_ctx* c) {
             }
             {
                 std::lock_guard<std::mutex> lk(c->f_mu);
-                if (e->kind == E_LOAD) { c->f_slot_of[e->model] = e->slot; c->f_state[e->model] = ST_LOADING; }
-                if (e->kind == E_OFFLOAD) { c->f_slot_of[e->model] = -1; c->f_state[e->model] = ST_OFFLOADING; }
+                if (e->kind == E_LOAD) { c->f_off_of[e->model] = (int64_t)e->off; c->f_state[e->model] = ST_LOADING; }
+                if (e->kind == E_OFFLOAD) { c->f_off_of[e->model] = -1; c->f_state[e->model] = ST_OFFLOADING; }
             }
             c->inflight.push_back(e);
             push_to_workers(c, e);
@@ -440,7 +440,7 @@ void follower_main(mpsw_ctx* c) {
                 s->ack[e.id % kAckCap][r].store(e.id + 1, std::memory_order_release);
                 {
                     std::lock_guard<std::mutex> lk(c->f_mu);
-                    if (e.kind == E_LOAD && c->f_slot_of[e.model] == e.slot) c->f_state[e.model] = ST_RESIDENT;
+                    if (e.kind == E_LOAD && c->f_off_of[e.model] == (int64_t)e.off) c->f_state[e.model] = ST_RESIDENT;
                     if (e.kind == E_OFFLOAD && c->f_state[e.model] == ST_OFFLOADING) c->f_state[e.model] = ST_EVICTED;
                 }
                 if (e.kind == E_BATCH) {
@@ -448,8 +448,8 @@ void follower_main(mpsw_ctx* c) {
                     c->n_batches++;
                 } else {
                     (e.kind == E_LOAD ? c->swaps_in : c->swaps_out)++;
-                    if (e.kind == E_LOAD) c->h2d_bytes += R.S;
-                    else if (c->cfg.writeback) c->d2h_bytes += R.S;
+                    if (e.kind == E_LOAD) c->h2d_bytes += c->models[e.model]->rank_S[R.index];
+                    else if (c->cfg.writeback) c->d2h_bytes += c->models[e.model]->rank_S[R.index];
                     finish_swap_events(c, e);
                     std::lock_guard<std::mutex> lk(c->done_mu);
                     e.complete.store(1, std::memory_order_release);
@@ -474,58 +474,51 @@ void follower_main(mpsw_ctx* c) {
     }
 }
 
-// Fix the slot geometry at the first registration: k = floor(budget / S_r) slots per rank
-// carved from the region allocated at init; workspaces sized for max_batch * max_tokens rows;
-// TP peers wired (collective in multi-process mode: IPC handles exchanged through shm).
-void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& d) {
+// Kernel limits of a model and, once the geometry is fixed, that it fits the workspace.
+void check_dims(mpsw_ctx* c, const mpsw_opt_dims& d) {
     const int hd = d.hidden / d.heads;
     if (hd % 8 || hd > 128) throw Error(MPSW_EINVAL, "head_dim must be a multiple of 8 and <= 128");
     if ((d.hidden / c->tp) % 8 || (d.ffn / c->tp) % 8 || d.hidden % 8)
         throw Error(MPSW_EINVAL, "hidden/tp, ffn/tp and hidden must be multiples of 8");
     if (d.hidden > 12288) throw Error(MPSW_EINVAL, "hidden too large for the LN kernel");
-    // every global rank's arena size (stage-dependent) and the slot count k, the same on all
-    // ranks (a model occupies one slot on every worker): k = min_r floor(budget / stride_r)
-    int k = 1024;
-    for (int g = 0; g < c->nr; ++g) {
-        Layout L;
-        if (compute_layout(d, c->tp, c->pp, g / c->tp, g % c->tp, c->cfg.dtype, L) != MPSW_OK)
-            throw Error(MPSW_EINVAL, tls_error());
-        c->rank_S[g] = L.bytes;
-        const uint64_t stride = (L.bytes + kSlotAlign - 1) / kSlotAlign * kSlotAlign;
-        k = (int)std::min<uint64_t>((uint64_t)k, c->cfg.param_budget_bytes_per_gpu / stride);
+    if (c->geom) {
+        const mpsw_opt_dims& x = c->dims_max;
+        if (d.hidden > x.hidden || d.ffn > x.ffn || d.vocab > x.vocab)
+            throw Error(MPSW_EINVAL, "model exceeds the ctx's workspace dims (set mpsw_config.max_dims, or register "
+                                     "the largest model first)");
     }
-    if (k < 1)
-        throw Error(MPSW_ENOMEM, "param budget cannot hold one shard (S_r = " + std::to_string(c->rank_S[0]) + ")");
-    c->dims = d;
-    c->vocab = d.vocab;
-    c->k = k;
+}
+
+// Forward shape of model d on rank R (its stage's layers).
+FwdShape fwd_shape(mpsw_ctx* c, const mpsw_opt_dims& d, const Rank& R) {
+    FwdShape f{};
+    f.n_layers = d.n_layers / c->pp; f.hidden = d.hidden; f.heads_local = d.heads / c->tp;
+    f.head_dim = d.hidden / d.heads;
+    f.ffn_local = d.ffn / c->tp; f.vocab_local = d.vocab / c->tp; f.vocab = d.vocab; f.tp = c->tp;
+    f.rank = R.trank;
+    f.dtype = c->cfg.dtype;
+    f.gemm_impl = c->cfg.gemm_impl;
+    f.max_rows = c->max_rows;
+    return f;
+}
+
+// Fix the geometry at the first registration: the region of every rank is `cap` bytes (budget
+// rounded down to 4 KiB; models are placed in it by the state machine); the forward workspace is
+// sized for dims_max (elementwise max shape) and max_batch * max_tokens rows; TP peers wired
+// (collective in multi-process mode: IPC handles exchanged through shm).
+void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& dmax) {
+    check_dims(c, dmax);
+    c->dims_max = dmax;
+    c->cap = c->cfg.param_budget_bytes_per_gpu / kSlotAlign * kSlotAlign;
     c->max_rows = c->cfg.max_batch * c->cfg.max_tokens;
     const unsigned ev_flags = c->mp ? (cudaEventInterprocess | cudaEventDisableTiming) : cudaEventDisableTiming;
     for (auto& Rp : c->ranks) {
         Rank& R = *Rp;
         MPSW_CU(cudaSetDevice(R.device));
-        if (compute_layout(d, c->tp, c->pp, R.stage, R.trank, c->cfg.dtype, R.layout) != MPSW_OK)
-            throw Error(MPSW_EINVAL, tls_error());
-        R.S = R.layout.bytes;
-        R.stride = (R.S + kSlotAlign - 1) / kSlotAlign * kSlotAlign;
-        R.n_chunks = (int)((R.S + c->chunk - 1) / c->chunk);
-        FwdShape& f = R.fs;
-        f.n_layers = d.n_layers / c->pp; f.hidden = d.hidden; f.heads_local = d.heads / c->tp; f.head_dim = hd;
-        f.ffn_local = d.ffn / c->tp; f.vocab_local = d.vocab / c->tp; f.vocab = d.vocab; f.tp = c->tp;
-        f.rank = R.trank;
-        f.dtype = c->cfg.dtype;
-        f.gemm_impl = c->cfg.gemm_impl;
-        f.max_rows = c->max_rows;
+        FwdShape f = fwd_shape(c, dmax, R);
+        f.n_layers = 1;                                  // the workspace does not depend on depth
+        R.fs_max = f;
         const size_t wsb = workspace_bytes(f, c->max_rows, c->cfg.max_batch);
-        R.slots.resize(k);
-        for (int s = 0; s < k; ++s) {
-            Slot& sl = R.slots[s];
-            sl.base = R.region + (uint64_t)s * R.stride;
-            sl.chunk_gate.resize(R.n_chunks);
-            for (auto& ev : sl.chunk_gate) MPSW_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-            MPSW_CU(cudaEventCreateWithFlags(&sl.whole_gate, cudaEventDisableTiming));
-            R.wptr.push_back(make_ptrs(R.layout, sl.base, R.stage * f.n_layers, f.n_layers));
-        }
         MPSW_CU(cudaMalloc(&R.ws_base, wsb));
         MPSW_CU(cudaMemset(R.ws_base, 0, wsb));
         workspace_carve(R.ws, f, c->max_rows, c->cfg.max_batch, R.ws_base);
@@ -536,6 +529,7 @@ void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& d) {
             c->peer_ev[R.index][pb] = R.ev_point[pb];
         }
     }
+    const mpsw_opt_dims& d = dmax;
     // staging ring: per entry [max_batch * V] fp32 logits, then tokens [max_rows] + meta
     c->ring_n = c->D + 1;
     const size_t logits_b = ((size_t)c->cfg.max_batch * d.vocab * 4 + 255) & ~size_t(255);
@@ -586,8 +580,7 @@ void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& d) {
     }
     {
         std::lock_guard<std::mutex> lk(c->sm_mu);
-        c->sm.k = k;
-        c->sm.owner.assign(k, -1);
+        c->sm.cap = c->cap;
     }
     c->geom = true;
 }

@@ -56,7 +56,8 @@ constexpr uint64_t kAckCap = 1 << 16;
 
 struct ShmRec {            // one decision published by the leader
     uint64_t id;
-    int32_t kind, model, slot, ring, B, M;
+    uint64_t off;          // load / offload: byte offset of the model's range
+    int32_t kind, model, ring, B, M;
 };
 
 struct ShmCtl {
@@ -90,7 +91,8 @@ struct ReqRec {
 
 struct Entry {
     uint64_t id = 0;
-    int kind = 0, model = -1, slot = -1;
+    int kind = 0, model = -1;
+    uint64_t off = 0;                            // load / offload: byte offset in the region
     std::vector<std::shared_ptr<ReqRec>> reqs;   // leader only
     int ring = 0, B = 0, M = 0;
     double t_submit = 0;
@@ -110,12 +112,13 @@ struct Entry {
 using EntryP = std::shared_ptr<Entry>;
 
 // ----------------------------------------------------------------------------- per-rank state
-struct Slot {
-    uint8_t* base = nullptr;
-    std::vector<cudaEvent_t> chunk_gate;   // recorded by the last writeback offload, per chunk
-    bool chunk_gate_valid = false;
-    cudaEvent_t whole_gate = nullptr;      // clean eviction: last forward that read the slot
-    bool whole_gate_valid = false;
+// A byte range of the region that a load must not overwrite before `ev` completes: one per D2H
+// chunk of a writeback offload (the chunk pairing of reading #5), or one per clean-evicted model
+// (its last forward). Kept until a load covers the range or the event is found complete.
+struct Gate {
+    uint64_t lo, hi;
+    cudaEvent_t ev;
+    bool chunk;        // a writeback D2H chunk (else: a clean-evicted model's last forward)
 };
 
 // NVLink-assisted fan-in (NEXT-2): a helper GPU's own PCIe link pulls chunks of another rank's
@@ -134,21 +137,18 @@ struct Helper {
 struct Rank {
     int index = 0, local = 0, device = 0, numa = -1;   // index = global rank = stage * tp + trank
     int stage = 0, trank = 0;              // pipeline stage, TP rank inside the stage
-    Layout layout;                         // this rank's arena layout (stage-dependent)
-    uint64_t S = 0, stride = 0;            // arena bytes, slot stride
-    int n_chunks = 0;
-    FwdShape fs{};                         // forward shape of this rank (its stage's layers)
+    FwdShape fs_max{};                     // workspace shape: elementwise max over the ctx's models
     cudaEvent_t ev_stage = nullptr;        // PP: residual stream of this stage is ready
     cudaEvent_t ev_base = nullptr;         // timeline origin of this rank's device (trace = 1)
     std::atomic<uint64_t> stage_out{0};    // PP: id+1 of the last batch whose ev_stage is recorded
     cudaStream_t compute = nullptr, h2d = nullptr, d2h = nullptr, aux = nullptr;
     cudaStream_t h2d_zc = nullptr;         // hybrid swap: the zero-copy share of a swap-in
     cudaEvent_t ev_zc = nullptr;
-    uint8_t* region = nullptr;             // param budget (one cudaMalloc)
-    std::vector<Slot> slots;
+    uint8_t* region = nullptr;             // param budget: cap bytes (one cudaMalloc)
+    std::vector<Gate> gates;               // worker-thread private
     uint8_t* ws_base = nullptr;
     FwdWorkspace ws;
-    std::vector<TensorPtrs> wptr;          // per slot
+    std::vector<TensorPtrs> wptr;          // per model: pointers into its current range
     cudaEvent_t ev_point[2] = {nullptr, nullptr};   // partial-ready events (interprocess in mp mode)
     std::vector<cudaEvent_t> last_compute; // per model
     std::vector<char> last_compute_valid;
@@ -161,7 +161,11 @@ struct Rank {
 
 struct Model {
     mpsw_opt_dims dims;
+    uint64_t size = 0;             // placement bytes: max over global ranks of round_up(S_r, 4 KiB)
     std::vector<PinnedBuf> arena;  // per LOCAL rank
+    std::vector<Layout> layout;    // per LOCAL rank (stage-dependent)
+    std::vector<FwdShape> fs;      // per LOCAL rank
+    uint64_t rank_S[kMaxRanks] = {};   // arena bytes per GLOBAL rank
 };
 
 struct Cmd {
@@ -188,12 +192,11 @@ struct mpsw_ctx {
     std::vector<std::unique_ptr<mpsw::Helper>> helpers; // fan-in helper GPUs (single process)
     int local_of[mpsw::kMaxRanks];                        // global rank -> local index or -1
     std::vector<std::unique_ptr<mpsw::Model>> models;
-    // geometry (fixed by the first registered model; homogeneous slots)
+    // geometry: region of cap bytes per rank; forward workspace sized for dims_max (cfg.max_dims,
+    // else the first registered model), fixed at the first registration
     bool geom = false;
-    mpsw_opt_dims dims{};
-    int k = 0;
-    uint64_t rank_S[mpsw::kMaxRanks] = {};   // arena bytes per global rank
-    int vocab = 0;
+    mpsw_opt_dims dims_max{};
+    uint64_t cap = 0;
     int max_rows = 0;
     // TP peers (global rank -> partial buffers / partial-ready events)
     float* peer_partial[mpsw::kMaxRanks][2] = {};
@@ -227,7 +230,7 @@ struct mpsw_ctx {
     int ring_next = 0;
     std::mutex api_mu;
     // follower-local view of residency (mp followers)
-    std::vector<int> f_slot_of;
+    std::vector<int64_t> f_off_of;
     std::vector<int> f_state;
     std::mutex f_mu;
     // trace + stats
@@ -259,7 +262,9 @@ void group_barrier(mpsw_ctx* c, int stage = 0);
 void worker_main(mpsw_ctx* c, Rank* R);
 void engine_main(mpsw_ctx* c);
 void follower_main(mpsw_ctx* c);
-void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& d);
+void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& dmax);
+void check_dims(mpsw_ctx* c, const mpsw_opt_dims& d);   // kernel limits + fits dims_max (after geometry)
+FwdShape fwd_shape(mpsw_ctx* c, const mpsw_opt_dims& d, const Rank& R);
 
 // engine.cpp: device timeline (trace = 1): [t0, t1] of an entry on each local rank, relative to
 // the rank's device origin event; called before the entry's events are destroyed

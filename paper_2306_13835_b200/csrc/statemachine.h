@@ -7,6 +7,7 @@
 
 #include "internal.h"
 
+#include <algorithm>
 #include <cmath>
 #include <deque>
 #include <map>
@@ -21,58 +22,72 @@ enum { ST_EVICTED = 0, ST_LOADING = 1, ST_RESIDENT = 2, ST_OFFLOADING = 3 };
 struct Decision {
     int kind;  // 0 load, 1 offload, 2 batch, 3 complete, 4 noop, 5 reject
     uint64_t id = 0;
-    int model = -1, slot = -1;
+    int model = -1;
+    uint64_t off = 0;  // load / offload: byte offset of the model's range in every rank's region
     std::vector<int64_t> rids;
     const char* status = "";
 };
 
-// Deterministic engine state machine.
+// Deterministic engine state machine. Placement (reading #28, NEXT-4):
+// each rank's parameter region is `cap` bytes; model m occupies [off[m], off[m] + size[m]) on
+// every rank (size = its largest per-rank shard, 4 KiB-aligned). A load takes the lowest-address
+// free range that fits (first fit). With no fit, eligible victims are taken in victim-key order
+// until a first fit appears, and only the victims overlapping that range are evicted. For
+// equal-size models this is exactly the k = floor(cap / size) slot scheme (off = slot * size).
 struct StateMachine {
-    int n_models = 0, k = 0, tp = 1, max_batch = 1, D = 1;
+    int n_models = 0, tp = 1, max_batch = 1, D = 1;
+    uint64_t cap = 0;
+    std::vector<uint64_t> size;
     std::vector<std::deque<std::pair<int64_t, double>>> queue;
-    std::vector<int> state, outstanding, slot_of;
+    std::vector<int> state, outstanding;
+    std::vector<int64_t> off_of;   // -1 = owns no range (EVICTED / OFFLOADING)
     std::vector<double> last_use;
-    std::vector<int> owner;  // slot -> model or -1
     struct Pend { int kind, model, left; uint32_t mask; };
     std::map<uint64_t, Pend> pending;
     std::map<uint64_t, std::pair<int, std::vector<int64_t>>> batches;
     int inflight = 0;
     uint64_t next_id = 0;
 
-    void add_model() {
+    void add_model(uint64_t bytes) {
         queue.emplace_back();
         state.push_back(ST_EVICTED);
         outstanding.push_back(0);
-        slot_of.push_back(-1);
+        off_of.push_back(-1);
         last_use.push_back(-INFINITY);
+        size.push_back(bytes);
         ++n_models;
     }
     bool head_less(int a, int b) const {  // (head t_arr, reg order)
         const double ta = queue[a].front().second, tb = queue[b].front().second;
         return ta < tb || (ta == tb && a < b);
     }
-    int free_slot() const {
-        for (int s = 0; s < k; ++s)
-            if (owner[s] < 0) return s;
-        return -1;
+    // lowest offset o with [o, o + need) free of every range owned by a model not in `skip`
+    int64_t first_fit(uint64_t need, const std::vector<char>& skip) const {
+        std::vector<std::pair<uint64_t, uint64_t>> iv;
+        for (int m = 0; m < n_models; ++m)
+            if (off_of[m] >= 0 && !skip[m]) iv.push_back({(uint64_t)off_of[m], (uint64_t)off_of[m] + size[m]});
+        std::sort(iv.begin(), iv.end());
+        uint64_t cur = 0;
+        for (const auto& r : iv) {
+            if (r.first >= cur + need) return (int64_t)cur;
+            cur = std::max(cur, r.second);
+        }
+        return cap >= cur + need ? (int64_t)cur : -1;
     }
-    void load(int m, int s, std::vector<Decision>& out) {
-        Decision d{0, next_id++, m, s};
-        owner[s] = m;
-        slot_of[m] = s;
+    int64_t free_range(int m) const { return first_fit(size[m], std::vector<char>(n_models, 0)); }
+    void load(int m, uint64_t o, std::vector<Decision>& out) {
+        Decision d{0, next_id++, m, o};
+        off_of[m] = (int64_t)o;
         state[m] = ST_LOADING;
         pending[d.id] = {E_LOAD, m, tp, 0u};
         out.push_back(d);
     }
-    int offload(int v, std::vector<Decision>& out) {
-        const int s = slot_of[v];
-        Decision d{1, next_id++, v, s};
-        owner[s] = -1;
-        slot_of[v] = -1;
+    void offload(int v, std::vector<Decision>& out) {
+        Decision d{1, next_id++, v, (uint64_t)off_of[v]};
+        off_of[v] = -1;
         state[v] = ST_OFFLOADING;
         pending[d.id] = {E_OFFLOAD, v, tp, 0u};
         out.push_back(d);
-        return s;
     }
     void schedule(double now, std::vector<Decision>& out) {
         std::vector<char> blocked(n_models, 0);
@@ -101,25 +116,36 @@ struct StateMachine {
             } else if (st == ST_LOADING || st == ST_OFFLOADING) {
                 blocked[m] = 1;
             } else {
-                const int s = free_slot();
-                if (s >= 0) {
-                    load(m, s, out);
+                const int64_t o = free_range(m);
+                if (o >= 0) {
+                    load(m, (uint64_t)o, out);
                 } else {
-                    int best = -1;
                     auto key_less = [&](int a, int b) {  // prefer empty queue, then LRU, then reg order
                         const int qa = queue[a].empty() ? 0 : 1, qb = queue[b].empty() ? 0 : 1;
                         if (qa != qb) return qa < qb;
                         if (last_use[a] != last_use[b]) return last_use[a] < last_use[b];
                         return a < b;
                     };
+                    std::vector<int> vics;
                     for (int v = 0; v < n_models; ++v) {
                         if (state[v] != ST_RESIDENT || outstanding[v] != 0) continue;
                         if (!queue[v].empty() && !head_less(m, v)) continue;   // older head: not a victim
-                        if (best < 0 || key_less(v, best)) best = v;
+                        vics.push_back(v);
                     }
-                    if (best >= 0) {
-                        const int sv = offload(best, out);
-                        load(m, sv, out);
+                    std::sort(vics.begin(), vics.end(), key_less);
+                    std::vector<char> skip(n_models, 0);
+                    for (int v : vics) {
+                        skip[v] = 1;
+                        const int64_t f = first_fit(size[m], skip);
+                        if (f < 0) continue;
+                        const uint64_t lo = (uint64_t)f, hi = lo + size[m];
+                        for (int w : vics) {                       // evict only what overlaps the fit
+                            if (!skip[w]) break;
+                            const uint64_t wl = (uint64_t)off_of[w], wh = wl + size[w];
+                            if (wl < hi && lo < wh) offload(w, out);
+                        }
+                        load(m, lo, out);
+                        break;
                     }
                 }
                 blocked[m] = 1;
@@ -162,13 +188,13 @@ struct StateMachine {
             d.status = "EBUSY";
             out.push_back(d);
         } else {
-            const int s = free_slot();
-            if (s < 0) {
+            const int64_t o = free_range(m);
+            if (o < 0) {
                 Decision d{5, 0, m};
                 d.status = "ENOMEM";
                 out.push_back(d);
             } else {
-                load(m, s, out);
+                load(m, (uint64_t)o, out);
             }
         }
         schedule(t, out);
@@ -187,15 +213,18 @@ struct StateMachine {
         schedule(t, out);
     }
     void check() const {
-        int owned = 0;
-        for (int s = 0; s < k; ++s)
-            if (owner[s] >= 0) ++owned;
-        if (owned > k) throw Error(MPSW_EINVARIANT, "more owned slots than k");
+        std::vector<std::pair<uint64_t, uint64_t>> iv;
         for (int m = 0; m < n_models; ++m) {
             if (outstanding[m] > 0 && state[m] != ST_RESIDENT)
                 throw Error(MPSW_EINVARIANT, "in-flight batch on a non-resident model");
-            if ((state[m] == ST_LOADING || state[m] == ST_RESIDENT) && owner[slot_of[m]] != m)
-                throw Error(MPSW_EINVARIANT, "slot ownership");
+            const bool owns = state[m] == ST_LOADING || state[m] == ST_RESIDENT;
+            if (owns != (off_of[m] >= 0)) throw Error(MPSW_EINVARIANT, "range ownership");
+            if (owns) iv.push_back({(uint64_t)off_of[m], (uint64_t)off_of[m] + size[m]});
+        }
+        std::sort(iv.begin(), iv.end());
+        for (size_t i = 0; i < iv.size(); ++i) {
+            if (iv[i].second > cap) throw Error(MPSW_EINVARIANT, "range beyond the budget");
+            if (i && iv[i].first < iv[i - 1].second) throw Error(MPSW_EINVARIANT, "overlapping ranges");
         }
         if (inflight > D) throw Error(MPSW_EINVARIANT, "D exceeded");
     }

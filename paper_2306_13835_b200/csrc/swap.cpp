@@ -35,45 +35,94 @@ bool event_done(cudaEvent_t ev) {
     return false;
 }
 
+// ----------------------------------------------------------------------------- range gates
+// Events of gates overlapping [lo, hi) that have not completed (duplicates removed).
+static void pending_gates(Rank& R, uint64_t lo, uint64_t hi, std::vector<cudaEvent_t>& out, bool* chunked) {
+    out.clear();
+    if (chunked) *chunked = false;
+    for (const Gate& g : R.gates) {
+        if (g.hi <= lo || hi <= g.lo) continue;
+        if (std::find(out.begin(), out.end(), g.ev) != out.end() || event_done(g.ev)) continue;
+        out.push_back(g.ev);
+        if (chunked && g.chunk) *chunked = true;
+    }
+}
+
+// After a load into [lo, hi) has been ordered after every gate overlapping it, gates lying inside
+// the range are superseded (any later writer of those bytes is ordered after this model's
+// forwards, hence after this load); completed gates are dropped too.
+static void retire_gates(Rank& R, uint64_t lo, uint64_t hi) {
+    size_t w = 0;
+    for (size_t i = 0; i < R.gates.size(); ++i) {
+        Gate& g = R.gates[i];
+        if ((lo <= g.lo && g.hi <= hi) || event_done(g.ev)) {
+            cudaEventDestroy(g.ev);
+        } else {
+            R.gates[w++] = g;
+        }
+    }
+    R.gates.resize(w);
+}
+
+static void add_gate(Rank& R, uint64_t lo, uint64_t hi, bool chunk, cudaStream_t st) {
+    cudaEvent_t ev;
+    MPSW_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    MPSW_CU(cudaEventRecord(ev, st));
+    R.gates.push_back({lo, hi, ev, chunk});
+}
+
 void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
-    Slot& sl = R.slots[e.slot];
+    const Model& md = *c->models[e.model];
+    const uint64_t S = md.rank_S[R.index], lo = e.off, hi = e.off + S;
+    const int n_chunks = (int)((S + c->chunk - 1) / c->chunk);
+    uint8_t* base = R.region + e.off;
     const uint8_t* src = arena_of(c, e.model, R);
-    const bool zc = use_zero_copy(c, R.S);
+    const bool zc = use_zero_copy(c, S);
     const int r = R.index;
+    {
+        const FwdShape& f = md.fs[R.local];
+        R.wptr[e.model] = make_ptrs(md.layout[R.local], base, R.stage * f.n_layers, f.n_layers);
+    }
     MPSW_CU(cudaEventCreate(&e.ev_start[r]));
     MPSW_CU(cudaEventCreate(&e.ev_done[r]));
     MPSW_CU(cudaEventRecord(e.ev_start[r], R.h2d));
     // gates that already completed are skipped (a stream wait on another stream's event costs
     // tens of microseconds, which dominates small-shard swaps: DESIGN.md §8 cfg5)
-    if (sl.whole_gate_valid && !event_done(sl.whole_gate)) MPSW_CU(cudaStreamWaitEvent(R.h2d, sl.whole_gate, 0));
-    if (c->cfg.swap_mode == 3 && !sl.chunk_gate_valid && R.S >= (64ull << 20)) {
+    std::vector<cudaEvent_t> evs;
+    bool chunked = false;
+    pending_gates(R, lo, hi, evs, &chunked);
+    if (!chunked)   // only whole-range gates (clean eviction): one wait up front
+        for (auto ev : evs) MPSW_CU(cudaStreamWaitEvent(R.h2d, ev, 0));
+    if (c->cfg.swap_mode == 3 && !chunked && S >= (64ull << 20)) {
         // HYBRID: the copy engine moves the head of the shard while the zero-copy kernel pulls
         // the tail over the same link from the SMs (two independent PCIe read requesters)
         const double f = hybrid_frac();
-        const uint64_t zc_bytes = ((uint64_t)(R.S * f) + 4095) / 4096 * 4096;
-        const uint64_t ce_bytes = R.S - zc_bytes;
+        const uint64_t zc_bytes = ((uint64_t)(S * f) + 4095) / 4096 * 4096;
+        const uint64_t ce_bytes = S - zc_bytes;
         MPSW_CU(cudaEventRecord(R.ev_zc, R.h2d));
         MPSW_CU(cudaStreamWaitEvent(R.h2d_zc, R.ev_zc, 0));
-        launch_zero_copy(sl.base + ce_bytes, src + ce_bytes, zc_bytes, zc_ctas(c), R.h2d_zc);
+        launch_zero_copy(base + ce_bytes, src + ce_bytes, zc_bytes, zc_ctas(c), R.h2d_zc);
         c->launches++;
         for (uint64_t off = 0; off < ce_bytes; off += c->chunk)
-            MPSW_CU(cudaMemcpyAsync(sl.base + off, src + off, std::min<uint64_t>(c->chunk, ce_bytes - off),
+            MPSW_CU(cudaMemcpyAsync(base + off, src + off, std::min<uint64_t>(c->chunk, ce_bytes - off),
                                     cudaMemcpyHostToDevice, R.h2d));
         MPSW_CU(cudaEventRecord(R.ev_zc, R.h2d_zc));
         MPSW_CU(cudaStreamWaitEvent(R.h2d, R.ev_zc, 0));
-    } else if (!sl.chunk_gate_valid && zc) {
-        launch_zero_copy(sl.base, src, R.S, zc_ctas(c), R.h2d);
+    } else if (!chunked && zc) {
+        launch_zero_copy(base, src, S, zc_ctas(c), R.h2d);
         c->launches++;
-    } else if (!c->helpers.empty() && !zc && R.n_chunks > 1) {
+    } else if (!c->helpers.empty() && !zc && n_chunks > 1) {
         // fan-in: chunk i goes over link (i mod (1 + helpers)); lane 0 is the owner's own link
         const int lanes = 1 + (int)c->helpers.size();
-        for (int i = 0; i < R.n_chunks; ++i) {
-            const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, R.S - off);
+        std::vector<cudaEvent_t> whole = chunked ? std::vector<cudaEvent_t>() : evs;
+        for (int i = 0; i < n_chunks; ++i) {
+            const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, S - off);
+            std::vector<cudaEvent_t> gate;
+            if (chunked) pending_gates(R, lo + off, lo + off + n, gate, nullptr);
             const int lane = i % lanes;
-            cudaEvent_t gate = sl.chunk_gate_valid && !event_done(sl.chunk_gate[i]) ? sl.chunk_gate[i] : nullptr;
             if (lane == 0) {
-                if (gate) MPSW_CU(cudaStreamWaitEvent(R.h2d, gate, 0));
-                MPSW_CU(cudaMemcpyAsync(sl.base + off, src + off, n, cudaMemcpyHostToDevice, R.h2d));
+                for (auto ev : gate) MPSW_CU(cudaStreamWaitEvent(R.h2d, ev, 0));
+                MPSW_CU(cudaMemcpyAsync(base + off, src + off, n, cudaMemcpyHostToDevice, R.h2d));
                 continue;
             }
             Helper& H = *c->helpers[lane - 1];
@@ -81,16 +130,15 @@ void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
             MPSW_CU(cudaSetDevice(H.device));
             if (i == lane) {                   // first chunk of this load on this helper
                 MPSW_CU(cudaStreamWaitEvent(H.stream, e.ev_start[r], 0));
-                if (sl.whole_gate_valid && !event_done(sl.whole_gate))
-                    MPSW_CU(cudaStreamWaitEvent(H.stream, sl.whole_gate, 0));
+                for (auto ev : whole) MPSW_CU(cudaStreamWaitEvent(H.stream, ev, 0));
             }
-            if (gate) MPSW_CU(cudaStreamWaitEvent(H.stream, gate, 0));
+            for (auto ev : gate) MPSW_CU(cudaStreamWaitEvent(H.stream, ev, 0));
             const int j = H.next;
             H.next ^= 1;
             if (H.free_valid[j]) MPSW_CU(cudaStreamWaitEvent(H.stream, H.free_ev[j], 0));
             uint8_t* stg = H.staging + (uint64_t)j * c->chunk;
             MPSW_CU(cudaMemcpyAsync(stg, src + off, n, cudaMemcpyHostToDevice, H.stream));
-            MPSW_CU(cudaMemcpyPeerAsync(sl.base + off, R.device, stg, H.device, n, H.stream));
+            MPSW_CU(cudaMemcpyPeerAsync(base + off, R.device, stg, H.device, n, H.stream));
             MPSW_CU(cudaEventRecord(H.free_ev[j], H.stream));
             H.free_valid[j] = true;
             if (!e.ev_helper[r][lane - 1]) MPSW_CU(cudaEventCreateWithFlags(&e.ev_helper[r][lane - 1], cudaEventDisableTiming));
@@ -100,27 +148,33 @@ void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
         for (int h = 0; h < (int)c->helpers.size(); ++h)
             if (e.ev_helper[r][h]) MPSW_CU(cudaStreamWaitEvent(R.h2d, e.ev_helper[r][h], 0));
     } else {
-        for (int i = 0; i < R.n_chunks; ++i) {
-            const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, R.S - off);
-            if (sl.chunk_gate_valid && !event_done(sl.chunk_gate[i]))
-                MPSW_CU(cudaStreamWaitEvent(R.h2d, sl.chunk_gate[i], 0));
+        // chunk i of the new model waits only for the D2H of the bytes it overwrites (chunk-paired
+        // in-place swap, reading #5; for equal-size models: the victim's chunk i)
+        std::vector<cudaEvent_t> gate;
+        for (int i = 0; i < n_chunks; ++i) {
+            const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, S - off);
+            if (chunked) {
+                pending_gates(R, lo + off, lo + off + n, gate, nullptr);
+                for (auto ev : gate) MPSW_CU(cudaStreamWaitEvent(R.h2d, ev, 0));
+            }
             if (zc) {
-                launch_zero_copy(sl.base + off, src + off, n, zc_ctas(c), R.h2d);
+                launch_zero_copy(base + off, src + off, n, zc_ctas(c), R.h2d);
                 c->launches++;
             } else {
-                MPSW_CU(cudaMemcpyAsync(sl.base + off, src + off, n, cudaMemcpyHostToDevice, R.h2d));
+                MPSW_CU(cudaMemcpyAsync(base + off, src + off, n, cudaMemcpyHostToDevice, R.h2d));
             }
         }
     }
-    sl.chunk_gate_valid = false;
-    sl.whole_gate_valid = false;
+    retire_gates(R, lo, hi);
     MPSW_CU(cudaEventRecord(e.ev_done[r], R.h2d));
 }
 
 void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
-    Slot& sl = R.slots[e.slot];
+    const uint64_t S = c->models[e.model]->rank_S[R.index], lo = e.off;
+    const int n_chunks = (int)((S + c->chunk - 1) / c->chunk);
+    const uint8_t* base = R.region + e.off;
     uint8_t* dst = arena_of(c, e.model, R);
-    const bool zc = use_zero_copy(c, R.S);
+    const bool zc = use_zero_copy(c, S);
     const int r = R.index;
     MPSW_CU(cudaEventCreate(&e.ev_start[r]));
     MPSW_CU(cudaEventCreate(&e.ev_done[r]));
@@ -130,20 +184,18 @@ void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
         MPSW_CU(cudaStreamWaitEvent(R.d2h, R.last_compute[e.model], 0));
     MPSW_CU(cudaEventRecord(e.ev_start[r], R.d2h));
     if (c->cfg.writeback) {
-        for (int i = 0; i < R.n_chunks; ++i) {
-            const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, R.S - off);
+        for (int i = 0; i < n_chunks; ++i) {
+            const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, S - off);
             if (zc) {
-                launch_zero_copy(dst + off, sl.base + off, n, zc_ctas(c), R.d2h);
+                launch_zero_copy(dst + off, base + off, n, zc_ctas(c), R.d2h);
                 c->launches++;
             } else {
-                MPSW_CU(cudaMemcpyAsync(dst + off, sl.base + off, n, cudaMemcpyDeviceToHost, R.d2h));
+                MPSW_CU(cudaMemcpyAsync(dst + off, base + off, n, cudaMemcpyDeviceToHost, R.d2h));
             }
-            MPSW_CU(cudaEventRecord(sl.chunk_gate[i], R.d2h));   // chunk i may now be overwritten
+            add_gate(R, lo + off, lo + off + n, true, R.d2h);   // these bytes may now be overwritten
         }
-        sl.chunk_gate_valid = true;
     } else {
-        MPSW_CU(cudaEventRecord(sl.whole_gate, R.d2h));
-        sl.whole_gate_valid = true;
+        add_gate(R, lo, lo + S, false, R.d2h);                  // after the victim's last forward
     }
     MPSW_CU(cudaEventRecord(e.ev_done[r], R.d2h));
 }

@@ -25,6 +25,11 @@ class MpswError(RuntimeError):
         self.status = status
 
 
+class OptDims(C.Structure):
+    _fields_ = [("n_layers", C.c_int), ("hidden", C.c_int), ("heads", C.c_int), ("ffn", C.c_int),
+                ("vocab", C.c_int), ("max_pos", C.c_int)]
+
+
 class Config(C.Structure):
     _fields_ = [("n_gpus", C.c_int), ("device_ids", C.POINTER(C.c_int)), ("tp", C.c_int),
                 ("param_budget_bytes_per_gpu", C.c_uint64), ("workspace_bytes_per_gpu", C.c_uint64),
@@ -33,12 +38,7 @@ class Config(C.Structure):
                 ("writeback", C.c_int), ("trace", C.c_int), ("zc_ctas", C.c_int),
                 ("world_size", C.c_int), ("world_rank", C.c_int), ("shm_name", C.c_char_p),
                 ("gemm_impl", C.c_int), ("pp", C.c_int), ("helper_device_ids", C.POINTER(C.c_int)),
-                ("n_helpers", C.c_int)]
-
-
-class OptDims(C.Structure):
-    _fields_ = [("n_layers", C.c_int), ("hidden", C.c_int), ("heads", C.c_int), ("ffn", C.c_int),
-                ("vocab", C.c_int), ("max_pos", C.c_int)]
+                ("n_helpers", C.c_int), ("max_dims", OptDims)]
 
 
 class TensorDesc(C.Structure):
@@ -50,7 +50,8 @@ class Stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("swaps_in", C.c_uint64), ("swaps_out", C.c_uint64), ("batches", C.c_uint64),
                 ("requests", C.c_uint64), ("rejected", C.c_uint64), ("k_slots", C.c_int),
-                ("shard_bytes", C.c_uint64), ("fwd_gpu_us_sum", C.c_uint64), ("fwd_gpu_n", C.c_uint64)]
+                ("shard_bytes", C.c_uint64), ("fwd_gpu_us_sum", C.c_uint64), ("fwd_gpu_n", C.c_uint64),
+                ("region_bytes", C.c_uint64)]
 
 
 _P = C.c_void_p
@@ -149,10 +150,13 @@ class Ctx:
 
     def __init__(self, device_ids=(0,), budget=1 << 30, max_batch=8, max_tokens=8, dtype=BF16,
                  max_inflight=1, swap_mode=SWAP_AUTO, chunk_bytes=0, writeback=1, trace=0, zc_ctas=0,
-                 world_size=1, world_rank=0, shm_name=None, gemm_impl=0, pp=1, helper_device_ids=()):
+                 world_size=1, world_rank=0, shm_name=None, gemm_impl=0, pp=1, helper_device_ids=(),
+                 max_dims=None):
         """Single-process: one ctx over len(device_ids) = tp * pp ranks (global rank
         g = stage * tp + tp_rank). Multi-process (world_size > 1): device_ids = (this process's
-        GPU,), rank world_rank of a TP group of world_size."""
+        GPU,), rank world_rank of a TP group of world_size. max_dims: the largest model shape the
+        forward workspace must hold when models of different sizes are registered (default:
+        the first registered model)."""
         self._ids = (C.c_int * len(device_ids))(*device_ids)
         self.world_size, self.world_rank = world_size, world_rank
         self.pp = pp
@@ -164,12 +168,13 @@ class Ctx:
                      max_inflight, swap_mode, chunk_bytes, writeback, trace, zc_ctas, world_size, world_rank,
                      self._shm, gemm_impl, pp,
                      (C.c_int * max(1, len(helper_device_ids)))(*helper_device_ids) if helper_device_ids else None,
-                     len(helper_device_ids))
+                     len(helper_device_ids), dims_of(max_dims) if max_dims is not None else OptDims())
         h = _P()
         _check(lib().mpsw_init(C.byref(cfg), C.byref(h)))
         self.h = h
         self.dtype = dtype
-        self.vocab = None
+        self.vocab = None        # vocab of the last registered model
+        self.vocabs = {}         # model id -> vocab (logits length)
         self._live = {}          # request id -> output array the library writes into (kept alive)
         self._done = {}          # request id -> (t_arrival, t_done); the library releases ids on OK
 
@@ -197,6 +202,7 @@ class Ctx:
             sizes = (C.c_uint64 * self.nr)(*[0 if a is None else a.nbytes for a in arrs])
             _check(lib().mpsw_register_model(self.h, C.byref(od), self.tp, ptrs, sizes, C.byref(mid)))
         self.vocab = dims.vocab
+        self.vocabs[mid.value] = dims.vocab
         return mid.value
 
     def model_arena(self, model_id, rank):
@@ -234,10 +240,11 @@ class Ctx:
 
     def request(self, model_id, tokens, out=None):
         tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        V = self.vocabs.get(model_id, self.vocab or 1)
         if out is None:
-            out = np.empty(self.vocab, np.float32)
+            out = np.empty(V, np.float32)
         rid = C.c_int64()
-        if out.dtype != np.float32 or out.size < self.vocab or not out.flags.c_contiguous:
+        if out.dtype != np.float32 or out.size < V or not out.flags.c_contiguous:
             raise ValueError("out must be a contiguous float32 array of at least vocab elements")
         _check(lib().mpsw_request(self.h, model_id, tok.ctypes.data_as(C.POINTER(C.c_int32)), tok.size,
                                   out.ctypes.data_as(C.POINTER(C.c_float)), C.byref(rid)))

@@ -13,17 +13,13 @@ from tests.gpu_util import need_gpu
 pytestmark = pytest.mark.gpu
 
 
-def read_trace(path):
-    events, decisions = [], []
-    for line in open(path):
-        o = json.loads(line)
-        (events if "ev" in o else decisions).append(o)
-    return events, decisions
-
-
 def replay_check(path, nm, k, tp, mb, D):
-    events, decisions = read_trace(path)
-    rdecs, eng = S.replay(S.EngineConfig(nm, k, tp, mb, D), events)
+    """Replay the engine's trace through the oracle scheduler, configured from the trace header
+    (region bytes, placement bytes per model); equal-size models: cap // size == k slots."""
+    cfg, events, decisions = S.read_trace(path)
+    assert (cfg.n_models, cfg.tp, cfg.max_batch, cfg.max_inflight) == (nm, tp, mb, D)
+    assert cfg.cap // cfg.sizes[0] == k
+    rdecs, eng = S.replay(cfg, events)
     assert rdecs == decisions
     # per-model FIFO and load-before-batch (in the engine's own order)
     resident = set()

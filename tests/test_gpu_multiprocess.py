@@ -47,10 +47,7 @@ def test_two_process_group(tmp_path):
     assert res[0]["stats"]["swaps_in"] == res[1]["stats"]["swaps_in"] > 0
     # leader trace replays through the oracle scheduler (acks from both processes)
     from oracle import scheduler as S
-    evs, decs = [], []
-    for line in open(out + ".trace"):
-        o = json.loads(line)
-        (evs if "ev" in o else decs).append(o)
-    k = res[0]["stats"]["k_slots"]
-    rdecs, _ = S.replay(S.EngineConfig(3, k, 2, 4, 1), evs)
+    cfg, evs, decs = S.read_trace(out + ".trace")
+    assert cfg.n_models == 3 and cfg.tp == 2 and cfg.cap // cfg.sizes[0] == res[0]["stats"]["k_slots"]
+    rdecs, _ = S.replay(cfg, evs)
     assert rdecs == decs

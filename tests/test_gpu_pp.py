@@ -74,11 +74,9 @@ def test_pp_engine_replay(tmp_path):
         p = str(tmp_path / "t.ndjson")
         ctx.trace_dump(p)
         st = ctx.stats()
-    evs, decs = [], []
-    for line in open(p):
-        o = json.loads(line)
-        (evs if "ev" in o else decs).append(o)
-    rdecs, _ = S.replay(S.EngineConfig(2, st["k_slots"], tp * pp, 2, 1), evs)
+    cfg, evs, decs = S.read_trace(p)
+    assert cfg.tp == tp * pp and cfg.cap // cfg.sizes[0] == st["k_slots"]
+    rdecs, _ = S.replay(cfg, evs)
     assert rdecs == decs
     assert sum(1 for e in evs if e["ev"] == "ack") == tp * pp * (st["swaps_in"] + st["swaps_out"])
 

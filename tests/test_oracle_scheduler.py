@@ -71,7 +71,7 @@ def test_capacity1_swap_order():
     load_resident(e, 0)
     out = e.step(ev("arrival", 1.0, rid=0, model=1))
     assert [d["dec"] for d in out] == ["offload", "load"]
-    assert out[0]["model"] == 0 and out[1]["model"] == 1 and out[0]["slot"] == out[1]["slot"]
+    assert out[0]["model"] == 0 and out[1]["model"] == 1 and out[0]["off"] == out[1]["off"]
     assert e.step(ev("ack", 1.5, entry=out[0]["id"], rank=0)) == []
     b = e.step(ev("ack", 1.6, entry=out[1]["id"], rank=0))
     assert [d["dec"] for d in b] == ["batch"] and b[0]["model"] == 1

@@ -52,8 +52,8 @@ def test_exhaustive_sequences():
                                 evs.append({"ev": "ack", "t": t, "entry": d["id"], "rank": 0})
                             elif d["dec"] == "batch":
                                 # a batch runs only on a fully resident, bit-exact model
-                                assert sm.owner[eng.slot_of[d["model"]]] == d["model"]
-                                assert checksum.checksum(sm.slot[0][eng.slot_of[d["model"]]]) == ref[d["model"]][0]
+                                assert sm.owner[eng.off_of[d["model"]]] == d["model"]
+                                assert checksum.checksum(sm.slot[0][eng.off_of[d["model"]]]) == ref[d["model"]][0]
                                 evs.append({"ev": "batch_done", "t": t, "batch": d["id"]})
                     assert sum(o is not None for o in sm.owner) <= k
                 for m, hs in sm.expected_slot_hashes().items():

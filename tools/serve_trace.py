@@ -113,11 +113,8 @@ def main():
     res["fwd_ms_total"] = tot
     res["fwd_overlapped_with_swapin_frac"] = ov / tot if tot else 0.0
     # replay parity of the engine's decisions (oracle C1)
-    evs, decs = [], []
-    for line in open(tpath):
-        o = json.loads(line)
-        (evs if "ev" in o else decs).append(o)
-    rdecs, _ = S.replay(S.EngineConfig(P["n"], st["k_slots"], tp, P["max_batch"], 1), evs)
+    rcfg, evs, decs = S.read_trace(tpath)
+    rdecs, _ = S.replay(rcfg, evs)
     res["replay_identical"] = rdecs == decs
     # logits parity on sampled requests (oracle C5, bf16-emulating) where the oracle is fast enough
     n_check = args.check_logits if args.check_logits >= 0 else (len(outs) if P["model"] == "opt-125m" else 0)
