@@ -7,7 +7,7 @@ log through the oracle scheduler (decisions must be identical) and checks the lo
 requests against the oracle forward when the model is small enough for the oracle.
 
 usage: python tools/serve_trace.py PRESET [--cv 4] [--seed 0] [--out results.json]
-presets: cfg1 | cfg2 | cfg2-t1 | cfg4-analog
+presets: cfg1 | cfg2 | cfg2-t1 | cfg4-analog | hetero
 """
 import argparse
 import json
@@ -35,6 +35,11 @@ PRESETS = {
     # OPT-1.3B-shaped models at TP1 (one GPU / 196 GB host cannot hold 6 x OPT-30B)
     "cfg4-analog": dict(model="opt-1.3b", n=6, tp=1, k=4, max_batch=32, L=8, kind="gamma",
                         rates=zipf_rates(6, 10.0, 1.0), duration=30.0),
+    # NEXT-4 (§6): models of different sizes in one 30 GB region (first-fit placement):
+    # 1 x OPT-13B, 3 x OPT-1.3B, 2 x OPT-125M; Gamma CV=1, 30 s, L=8, max batch 8
+    "hetero": dict(models=["opt-13b", "opt-1.3b", "opt-1.3b", "opt-1.3b", "opt-125m", "opt-125m"], tp=1,
+                   budget=30 * 10**9, max_batch=8, L=8, kind="gamma", rates=[0.5, 3.0, 3.0, 3.0, 6.0, 6.0],
+                   duration=30.0),
 }
 
 
@@ -47,21 +52,25 @@ def main():
     ap.add_argument("--check-logits", type=int, default=-1, help="requests to check vs the oracle (-1 = auto)")
     args = ap.parse_args()
     P = dict(PRESETS[args.preset])
-    d = opt_dims(P["model"])
+    names = P.get("models") or [P["model"]] * P["n"]
+    P["n"] = len(names)
+    dims = [opt_dims(nm) for nm in names]
+    d = max(dims, key=lambda x: layout.shard_bytes(x, P["tp"]))     # workspace dims (max_dims)
     tp = P["tp"]
-    S_r = layout.shard_bytes(d, tp)
+    S_r = layout.shard_bytes(dims[0], tp)
+    sizes_r = [layout.shard_bytes(x, tp) for x in dims]
     cv = args.cv if args.cv is not None else (4.0 if "cfg4" in args.preset else 1.0)
     if P["kind"] == "alternating":
-        trace = alternating_blocking(P["n_req"], args.seed, P["L"], d.vocab)
+        trace = alternating_blocking(P["n_req"], args.seed, P["L"], min(x.vocab for x in dims))
     else:
-        trace = gamma_trace(P["rates"], cv, P["duration"], args.seed, P["L"], d.vocab)
-    budget = P["k"] * ((S_r + 4095) // 4096 * 4096)
-    res = {"preset": args.preset, "model": P["model"], "tp": tp, "k": P["k"], "cv": cv, "seed": args.seed,
-           "requests": len(trace), "shard_bytes": S_r}
+        trace = gamma_trace(P["rates"], cv, P["duration"], args.seed, P["L"], min(x.vocab for x in dims))
+    budget = P["budget"] if "budget" in P else P["k"] * ((S_r + 4095) // 4096 * 4096)
+    res = {"preset": args.preset, "models": names, "tp": tp, "k": P.get("k"), "budget": budget, "cv": cv,
+           "seed": args.seed, "requests": len(trace), "shard_bytes": sizes_r}
     t_setup = time.perf_counter()
     with M.Ctx(device_ids=(0,) * tp, budget=budget, max_batch=P["max_batch"], max_tokens=P["L"], trace=1,
-               writeback=0) as ctx:
-        ids = [ctx.register_model(d) for _ in range(P["n"])]
+               writeback=0, max_dims=d) as ctx:
+        ids = [ctx.register_model(x) for x in dims]
         for m in ids:
             ctx.synth_fill(m, 7000 + m)
         res["setup_s"] = time.perf_counter() - t_setup
@@ -76,11 +85,12 @@ def main():
             outs.append((rid, r, out))
             if r.warmup or P["kind"] == "alternating":
                 ctx.wait_request(rid, 600)
-        lat = []
+        lat, lat_by = [], {}
         for rid, r, out in outs:
             ta, td = ctx.wait_request(rid, 600)
             if not r.warmup:
                 lat.append(td - ta)
+                lat_by.setdefault(names[r.model], []).append(td - ta)
         tpath = "/tmp/serve_trace.ndjson"
         ctx.trace_dump(tpath)
         ctx.timeline_dump("/tmp/serve_timeline.ndjson")
@@ -89,12 +99,15 @@ def main():
         h2d = []   # host-observed swap-in latency (submit -> last rank's ack), ms: virtual ranks share
         for ld in loads:  # one GPU and one link, so per-rank device spans would overlap-count
             ts, td = ctx.wait(ld["id"])
-            h2d.append((max(td) - ts) * 1e3)
+            h2d.append(((max(td) - ts) * 1e3, sizes_r[ld["model"]]))
     if P["kind"] == "alternating":
         lat = lat[1:]                       # cold first load reported separately
     res["latency_s"] = metrics.summary(lat)
     res["swaps_in"] = st["swaps_in"]
-    res["swap_in_GBps_median"] = float(np.median([tp * S_r / (ms / 1e3) / 1e9 for ms in h2d])) if h2d else None
+    res["swap_in_GBps_median"] = float(np.median([tp * n / (ms / 1e3) / 1e9 for ms, n in h2d])) if h2d else None
+    if len(set(names)) > 1:
+        res["latency_by_model_s"] = {k: metrics.summary(v) for k, v in lat_by.items()}
+        res["swaps_in_by_model"] = {k: sum(1 for ld in loads if names[ld["model"]] == k) for k in set(names)}
     res["batches"] = st["batches"]
     res["fwd_ms_mean"] = st["fwd_gpu_us_sum"] / 1e3 / max(1, st["fwd_gpu_n"])
     # device timeline: how much forward time ran while a swap-in was streaming on the same GPU
@@ -117,14 +130,15 @@ def main():
     rdecs, _ = S.replay(rcfg, evs)
     res["replay_identical"] = rdecs == decs
     # logits parity on sampled requests (oracle C5, bf16-emulating) where the oracle is fast enough
-    n_check = args.check_logits if args.check_logits >= 0 else (len(outs) if P["model"] == "opt-125m" else 0)
+    small = [(rid, r, out) for rid, r, out in outs if names[r.model] == "opt-125m"]
+    n_check = args.check_logits if args.check_logits >= 0 else (len(small) if args.preset == "cfg1" else min(8, len(small)))
     if n_check:
         errs = []
         Ws = {}
-        for rid, r, out in outs[:: max(1, len(outs) // n_check)][:n_check]:
+        for rid, r, out in small[:: max(1, len(small) // n_check)][:n_check]:
             if r.model not in Ws:
-                Ws[r.model] = layout.full_tensors(d, 7000 + r.model)
-            ref = forward.forward_bf16_emulated(d, Ws[r.model], r.tokens[None])[0]
+                Ws[r.model] = layout.full_tensors(dims[r.model], 7000 + r.model)
+            ref = forward.forward_bf16_emulated(dims[r.model], Ws[r.model], r.tokens[None])[0]
             errs.append(forward.rel_l2(out, ref))
         res["logits_checked"] = len(errs)
         res["logits_max_rel_l2"] = max(errs)
