@@ -91,6 +91,8 @@ typedef struct {
                                   /* heterogeneous models (NEXT-4): the forward workspace is     */
                                   /* sized for hidden/ffn/vocab up to these; all zero = the dims */
                                   /* of the first registered model (later ones must not exceed)  */
+    int prefetch;                 /* 1 = prefetch predicted models into free space while no swap  */
+                                  /* is in flight (NEXT-3, reading #29); never evicts  */
 } mpsw_config;
 
 typedef struct {
@@ -205,10 +207,11 @@ mpsw_status mpsw_peek(mpsw_ctx* ctx, int model_id, int rank, uint64_t offset, ui
 mpsw_status mpsw_residency(mpsw_ctx* ctx, int model_id, int* state);
 
 /* Write the recorded events and decisions, in engine order, as NDJSON (trace = 1). The first
- * line is {"cfg": {"cap", "sizes", "acks", "max_batch", "D"}}: the state machine's
+ * line is {"cfg": {"cap", "sizes", "acks", "max_batch", "D", "prefetch"}}: the state machine's
  * configuration (region bytes, placement bytes per model, acks per entry), enough to replay
  * the log through the oracle scheduler. Decisions: {"dec": "load"|"offload", "id", "model",
- * "off"} (byte offset in every rank's region), {"dec": "batch"|"complete", "id", "rids"}, ... */
+ * "off"} (byte offset in every rank's region; prefetch loads add "prefetch": true),
+ * {"dec": "batch"|"complete", "id", "rids"}, ... */
 mpsw_status mpsw_trace_dump(mpsw_ctx* ctx, const char* ndjson_path);
 
 /* Write this process's device timeline as NDJSON (trace = 1): one line per finished entry per
@@ -229,6 +232,7 @@ typedef struct {
     uint64_t fwd_gpu_us_sum;      /* sum of per-batch forward device time (first local rank) */
     uint64_t fwd_gpu_n;           /* batches in that sum                                    */
     uint64_t region_bytes;        /* parameter region per rank (budget rounded down to 4 KiB) */
+    uint64_t prefetches;          /* load entries issued by the prefetch policy               */
 } mpsw_stats;
 
 mpsw_status mpsw_get_stats(mpsw_ctx* ctx, mpsw_stats* out);

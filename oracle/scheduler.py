@@ -16,7 +16,11 @@ of different sizes (NEXT-4, §6): each rank's region holds `cap` bytes, mo
 [off, off + size[m]) on every rank, loads go to the lowest-address free range that fits (first
 fit); with no fit, eligible victims are removed in victim-key order until a first fit exists and
 only the victims overlapping that range are offloaded. Equal sizes reduce to k slots
-(cap = k, size 1: off is the slot index).
+(cap = k, size 1: off is the slot index); #29 prefetch (NEXT-3, "more sophisticated
+fetching algorithms"): when enabled and no load/offload is pending, after SCHEDULE the EVICTED
+model with an empty queue that appears most often among the last 32 arrivals (ties: latest
+arrival, then registration order) is loaded into the lowest free range that fits it; it never
+evicts, and candidates that do not fit are skipped.
 
 `Engine` is a deterministic state machine.  `step(event)` applies one event and returns the
 decisions it caused.  Two drivers use it:
@@ -41,6 +45,7 @@ class EngineConfig:
     max_inflight: int = 1       # D (reading #26)
     cap: int = None             # region bytes per rank (reading #28); None: k_slots unit slots
     sizes: list = None          # placement bytes per model; None: 1 each
+    prefetch: bool = False      # reading #29
 
     def region(self):
         return self.k_slots if self.cap is None else self.cap
@@ -52,7 +57,8 @@ class EngineConfig:
 def config_from_trace(cfg):
     """EngineConfig from the {"cfg": ...} header line of the engine's trace (mpsw_trace_dump)."""
     c = cfg["cfg"]
-    return EngineConfig(len(c["sizes"]), 0, c["acks"], c["max_batch"], c["D"], cap=c["cap"], sizes=list(c["sizes"]))
+    return EngineConfig(len(c["sizes"]), 0, c["acks"], c["max_batch"], c["D"], cap=c["cap"], sizes=list(c["sizes"]),
+                        prefetch=bool(c.get("prefetch", False)))
 
 
 def read_trace(path):
@@ -86,9 +92,12 @@ class Engine:
     batches: dict = field(init=False)        # batch id -> (model, rids)
     inflight: int = 0
     next_id: int = 0
+    HISTORY = 32                             # arrivals remembered by the prefetch policy
 
     def __post_init__(self):
         n = self.cfg.n_models
+        self.recent = deque(maxlen=self.HISTORY)
+        self.last_arrival = [float("-inf")] * n
         self.queue = [deque() for _ in range(n)]
         self.state = [EVICTED] * n
         self.last_use = [float("-inf")] * n
@@ -139,6 +148,7 @@ class Engine:
         while True:
             cands = [m for m in range(self.cfg.n_models) if self.queue[m] and m not in blocked]
             if not cands:
+                self._prefetch(out)
                 return
             m = min(cands, key=self._head_key)
             st = self.state[m]
@@ -179,6 +189,21 @@ class Engine:
                         break
                 blocked.add(m)
 
+    def _prefetch(self, out):
+        """Reading #29: one prefetch load into free space when the link is idle."""
+        if not self.cfg.prefetch or self.pending:
+            return
+        count = {}
+        for m in self.recent:
+            count[m] = count.get(m, 0) + 1
+        cands = [m for m in count if self.state[m] == EVICTED and not self.queue[m]]
+        for m in sorted(cands, key=lambda m: (-count[m], -self.last_arrival[m], m)):
+            o = self._first_fit(self.cfg.size(m))
+            if o is not None:
+                self._load(m, o, out)
+                out[-1]["prefetch"] = True
+                return
+
     # ---- events ----------------------------------------------------------------------------
     def step(self, ev):
         """Apply one event dict; return the list of decision dicts it caused."""
@@ -191,6 +216,8 @@ class Engine:
                 out.append({"dec": "reject", "rid": ev["rid"], "status": "ENOENT"})
                 return out
             self.queue[m].append((ev["rid"], now))
+            self.recent.append(m)
+            self.last_arrival[m] = now
         elif kind == "ack":
             e, r = ev["entry"], ev["rank"]
             if e not in self.pending:

@@ -95,6 +95,7 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     c->sm.tp = c->nr;              // acks per entry: one per worker
     c->sm.max_batch = cfg->max_batch;
     c->sm.D = c->D;
+    c->sm.prefetch = cfg->prefetch != 0;
     for (auto& b : c->stage_barrier) b.n = mp ? 1 : c->tp;
     c->models.reserve(kMaxModels);
     for (auto& x : c->local_of) x = -1;
@@ -639,7 +640,8 @@ mpsw_status mpsw_trace_dump(mpsw_ctx* c, const char* path) {
         std::lock_guard<std::mutex> sl(c->sm_mu);
         f << "{\"cfg\":{\"cap\":" << c->sm.cap << ",\"sizes\":[";
         for (int m = 0; m < c->sm.n_models; ++m) f << (m ? "," : "") << c->sm.size[m];
-        f << "],\"acks\":" << c->sm.tp << ",\"max_batch\":" << c->sm.max_batch << ",\"D\":" << c->sm.D << "}}\n";
+        f << "],\"acks\":" << c->sm.tp << ",\"max_batch\":" << c->sm.max_batch << ",\"D\":" << c->sm.D
+          << ",\"prefetch\":" << (c->sm.prefetch ? "true" : "false") << "}}\n";
     }
     for (const auto& l : c->trace_lines) f << l << "\n";
     return MPSW_OK;
@@ -672,6 +674,7 @@ mpsw_status mpsw_get_stats(mpsw_ctx* c, mpsw_stats* o) {
     o->k_slots = c->models.empty() ? 0 : (int)(c->cap / c->models[0]->size);
     o->shard_bytes = c->models.empty() ? 0 : c->models[0]->rank_S[0];
     o->region_bytes = c->cap;
+    o->prefetches = c->prefetches.load();
     o->fwd_gpu_us_sum = c->fwd_us_sum.load();
     o->fwd_gpu_n = c->fwd_n.load();
     return MPSW_OK;

@@ -124,7 +124,10 @@ void log_decisions(mpsw_ctx* c, const std::vector<Decision>& ds) {
     for (const auto& d : ds) {
         std::ostringstream o;
         switch (d.kind) {
-            case 0: o << "{\"dec\":\"load\",\"id\":" << d.id << ",\"model\":" << d.model << ",\"off\":" << d.off << "}"; break;
+            case 0:
+                o << "{\"dec\":\"load\",\"id\":" << d.id << ",\"model\":" << d.model << ",\"off\":" << d.off
+                  << (d.prefetch ? ",\"prefetch\":true}" : "}");
+                break;
             case 1: o << "{\"dec\":\"offload\",\"id\":" << d.id << ",\"model\":" << d.model << ",\"off\":" << d.off << "}"; break;
             case 2:
             case 3: {
@@ -164,6 +167,7 @@ void publish(mpsw_ctx* c, const Entry& e) {
 void dispatch(mpsw_ctx* c, const std::vector<Decision>& ds, double now) {
     for (const auto& d : ds) {
         if (d.kind > 2) continue;
+        if (d.prefetch) c->prefetches++;
         auto e = std::make_shared<Entry>();
         e->id = d.id;
         e->kind = d.kind;

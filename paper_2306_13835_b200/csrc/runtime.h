@@ -242,7 +242,7 @@ struct mpsw_ctx {
     std::mutex sm_mu;
     std::unordered_map<int64_t, std::shared_ptr<mpsw::ReqRec>> eng_reqs;   // engine-private
     std::atomic<uint64_t> launches{0}, h2d_bytes{0}, d2h_bytes{0}, swaps_in{0}, swaps_out{0}, n_batches{0},
-        n_requests{0}, rejected{0}, fwd_us_sum{0}, fwd_n{0};
+        n_requests{0}, rejected{0}, fwd_us_sum{0}, fwd_n{0}, prefetches{0};
 };
 
 namespace mpsw {

@@ -26,6 +26,7 @@ struct Decision {
     uint64_t off = 0;  // load / offload: byte offset of the model's range in every rank's region
     std::vector<int64_t> rids;
     const char* status = "";
+    bool prefetch = false;  // load issued by the prefetch policy (reading #29), not by a request
 };
 
 // Deterministic engine state machine. Placement (reading #28, NEXT-4):
@@ -47,6 +48,11 @@ struct StateMachine {
     std::map<uint64_t, std::pair<int, std::vector<int64_t>>> batches;
     int inflight = 0;
     uint64_t next_id = 0;
+    // prefetch (NEXT-3, reading #29): the last kHist arrivals, last arrival time per model
+    static constexpr int kHist = 32;
+    bool prefetch = false;
+    std::deque<int> recent;
+    std::vector<double> last_arr;
 
     void add_model(uint64_t bytes) {
         queue.emplace_back();
@@ -55,6 +61,7 @@ struct StateMachine {
         off_of.push_back(-1);
         last_use.push_back(-INFINITY);
         size.push_back(bytes);
+        last_arr.push_back(-INFINITY);
         ++n_models;
     }
     bool head_less(int a, int b) const {  // (head t_arr, reg order)
@@ -95,7 +102,7 @@ struct StateMachine {
             int m = -1;
             for (int i = 0; i < n_models; ++i)
                 if (!queue[i].empty() && !blocked[i] && (m < 0 || head_less(i, m))) m = i;
-            if (m < 0) return;
+            if (m < 0) break;
             const int st = state[m];
             if (st == ST_RESIDENT) {
                 if (inflight < D) {
@@ -151,9 +158,36 @@ struct StateMachine {
                 blocked[m] = 1;
             }
         }
+        prefetch_step(out);
     }
+
     // events ------------------------------------------------------------------------------
+    // Prefetch into free space while no load / offload is in flight: among EVICTED models with
+    // an empty queue and at least one of the last kHist arrivals, by (count desc, last arrival
+    // desc, registration order), the first whose size fits a free range is loaded. Never evicts.
+    void prefetch_step(std::vector<Decision>& out) {
+        if (!prefetch || !pending.empty()) return;
+        std::vector<int> cnt(n_models, 0), cand;
+        for (int m : recent) ++cnt[m];
+        for (int m = 0; m < n_models; ++m)
+            if (state[m] == ST_EVICTED && queue[m].empty() && cnt[m] > 0) cand.push_back(m);
+        std::sort(cand.begin(), cand.end(), [&](int a, int b) {
+            if (cnt[a] != cnt[b]) return cnt[a] > cnt[b];
+            if (last_arr[a] != last_arr[b]) return last_arr[a] > last_arr[b];
+            return a < b;
+        });
+        for (int m : cand) {
+            const int64_t o = free_range(m);
+            if (o < 0) continue;
+            load(m, (uint64_t)o, out);
+            out.back().prefetch = true;
+            return;
+        }
+    }
     void arrival(int64_t rid, int m, double t, std::vector<Decision>& out) {
+        recent.push_back(m);
+        if ((int)recent.size() > kHist) recent.pop_front();
+        last_arr[m] = t;
         queue[m].push_back({rid, t});
         schedule(t, out);
     }

@@ -38,7 +38,7 @@ class Config(C.Structure):
                 ("writeback", C.c_int), ("trace", C.c_int), ("zc_ctas", C.c_int),
                 ("world_size", C.c_int), ("world_rank", C.c_int), ("shm_name", C.c_char_p),
                 ("gemm_impl", C.c_int), ("pp", C.c_int), ("helper_device_ids", C.POINTER(C.c_int)),
-                ("n_helpers", C.c_int), ("max_dims", OptDims)]
+                ("n_helpers", C.c_int), ("max_dims", OptDims), ("prefetch", C.c_int)]
 
 
 class TensorDesc(C.Structure):
@@ -51,7 +51,7 @@ class Stats(C.Structure):
                 ("swaps_in", C.c_uint64), ("swaps_out", C.c_uint64), ("batches", C.c_uint64),
                 ("requests", C.c_uint64), ("rejected", C.c_uint64), ("k_slots", C.c_int),
                 ("shard_bytes", C.c_uint64), ("fwd_gpu_us_sum", C.c_uint64), ("fwd_gpu_n", C.c_uint64),
-                ("region_bytes", C.c_uint64)]
+                ("region_bytes", C.c_uint64), ("prefetches", C.c_uint64)]
 
 
 _P = C.c_void_p
@@ -151,12 +151,13 @@ class Ctx:
     def __init__(self, device_ids=(0,), budget=1 << 30, max_batch=8, max_tokens=8, dtype=BF16,
                  max_inflight=1, swap_mode=SWAP_AUTO, chunk_bytes=0, writeback=1, trace=0, zc_ctas=0,
                  world_size=1, world_rank=0, shm_name=None, gemm_impl=0, pp=1, helper_device_ids=(),
-                 max_dims=None):
+                 max_dims=None, prefetch=0):
         """Single-process: one ctx over len(device_ids) = tp * pp ranks (global rank
         g = stage * tp + tp_rank). Multi-process (world_size > 1): device_ids = (this process's
         GPU,), rank world_rank of a TP group of world_size. max_dims: the largest model shape the
         forward workspace must hold when models of different sizes are registered (default:
-        the first registered model)."""
+        the first registered model). prefetch: load predicted models into free space while no
+        swap is in flight (reading #29)."""
         self._ids = (C.c_int * len(device_ids))(*device_ids)
         self.world_size, self.world_rank = world_size, world_rank
         self.pp = pp
@@ -168,7 +169,7 @@ class Ctx:
                      max_inflight, swap_mode, chunk_bytes, writeback, trace, zc_ctas, world_size, world_rank,
                      self._shm, gemm_impl, pp,
                      (C.c_int * max(1, len(helper_device_ids)))(*helper_device_ids) if helper_device_ids else None,
-                     len(helper_device_ids), dims_of(max_dims) if max_dims is not None else OptDims())
+                     len(helper_device_ids), dims_of(max_dims) if max_dims is not None else OptDims(), prefetch)
         h = _P()
         _check(lib().mpsw_init(C.byref(cfg), C.byref(h)))
         self.h = h

@@ -1,5 +1,5 @@
 """NEXT-4: models of different sizes share one region per rank, placed
-first-fit (reading #28). On the GPU: decisions replay identically through the oracle
+first-fit (reading #28), with and without the NEXT-3 prefetch policy (reading #29). On the GPU: decisions replay identically through the oracle
 scheduler, every resident model's range is bit-exact on every rank after arbitrary swap traffic,
 the byte-level oracle (RegionSwapModel) predicts every resident hash, host arenas round-trip,
 and logits match the oracle forward."""
@@ -24,8 +24,9 @@ def placement_bytes(d, tp):
     return (layout.shard_bytes(d, tp) + 4095) // 4096 * 4096
 
 
-@pytest.mark.parametrize("tp,writeback,mode", [(1, 0, 0), (1, 1, 1), (2, 1, 1), (2, 0, 2)])
-def test_heterogeneous_models(tmp_path, tp, writeback, mode):
+@pytest.mark.parametrize("tp,writeback,mode,prefetch", [(1, 0, 0, 0), (1, 1, 1, 1), (2, 1, 1, 0), (2, 0, 2, 1),
+                                                        (1, 0, 0, 1)])
+def test_heterogeneous_models(tmp_path, tp, writeback, mode, prefetch):
     M = need_gpu()
     sizes = [placement_bytes(d, tp) for d in DIMS]
     budget = sizes[0] + sizes[1] + sizes[5] + 3 * 4096        # one mid + two smaller ones
@@ -35,7 +36,7 @@ def test_heterogeneous_models(tmp_path, tp, writeback, mode):
     rnd = random.Random(tp * 100 + writeback * 10 + mode)
     outs = []
     with M.Ctx(device_ids=(0,) * tp, budget=budget, max_batch=4, max_tokens=8, trace=1, writeback=writeback,
-               swap_mode=mode, chunk_bytes=1 << 20, max_dims=opt_dims("mid")) as ctx:
+               swap_mode=mode, chunk_bytes=1 << 20, max_dims=opt_dims("mid"), prefetch=prefetch) as ctx:
         ids = [ctx.register_model(d) for d in DIMS]
         for m in ids:
             ctx.synth_fill(m, seeds[m])
@@ -62,8 +63,11 @@ def test_heterogeneous_models(tmp_path, tp, writeback, mode):
         host = {m: [ctx.checksum(ids[m], r, on_device=False) for r in range(tp)] for m in range(len(DIMS))}
     cfg, evs, decs = S.read_trace(p)
     assert cfg.sizes == sizes and cfg.cap == budget // 4096 * 4096 and st["region_bytes"] == cfg.cap
+    assert cfg.prefetch == bool(prefetch)
     rdecs, _ = S.replay(cfg, evs)
     assert rdecs == decs
+    n_pf = sum(1 for d in decs if d.get("prefetch"))
+    assert n_pf == st["prefetches"] and (n_pf > 0) == bool(prefetch)
     offs = {d["off"] for d in decs if d["dec"] == "load"}
     assert len(offs) > 1 and st["swaps_in"] > len(DIMS)          # real placement traffic
     # byte-level oracle: the decisions applied to the images predict every resident hash

@@ -220,3 +220,83 @@ def test_region_swap_bytes(writeback):
     for m, ims in sm.host.items():
         for r in range(tp):
             assert np.array_equal(ims[r], images[m][r])
+
+
+# ---- prefetch (NEXT-3, reading #29) --------------------------------------------------------
+def test_prefetch_worked_example():
+    # cap 10: B(3)@0, C(3)@3; A(7) evicts both (LRU prefix B, C) and loads at 0; once every swap
+    # is acked, the policy prefetches C (same count as B, later arrival) into the free [7, 10);
+    # the next request for C then needs no swap
+    for pf in (False, True):
+        e = S.Engine(S.EngineConfig(3, 0, 1, 4, 1, cap=10, sizes=[7, 3, 3], prefetch=pf))
+        assert swaps(drive_resident(e, 1, 1.0)) == [("load", 1, 0)]
+        assert swaps(drive_resident(e, 2, 2.0)) == [("load", 2, 3)]
+        decs = drive_resident(e, 0, 3.0)
+        got = swaps(decs)
+        assert got[:3] == [("offload", 1, 0), ("offload", 2, 3), ("load", 0, 0)]
+        if pf:
+            assert got[3:] == [("load", 2, 7)]
+            assert [(d["model"], d["off"]) for d in decs if d.get("prefetch")] == [(2, 7)]
+            assert swaps(drive_resident(e, 2, 4.0)) == []              # prefetched: no swap
+        else:
+            assert got[3:] == []
+            assert swaps(drive_resident(e, 2, 4.0)) == [("load", 2, 7)]
+
+
+def test_prefetch_skips_candidates_that_do_not_fit():
+    # the most frequent evicted model (A, 8) does not fit the free space; the next one (B, 2) does
+    e = S.Engine(S.EngineConfig(3, 0, 1, 4, 1, cap=10, sizes=[8, 2, 9], prefetch=True))
+    drive_resident(e, 0, 1.0)
+    drive_resident(e, 0, 1.5)
+    drive_resident(e, 1, 2.0)          # B(2) fits beside A at 8
+    decs = drive_resident(e, 2, 3.0)   # C(9) evicts A and B; free [9, 10) is too small for anyone
+    assert swaps(decs) == [("offload", 0, 0), ("offload", 1, 8), ("load", 2, 0)]
+    assert not any(d.get("prefetch") for d in decs)
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_prefetch_random_traces(seed):
+    """With prefetch on: invariants, completion and per-model FIFO hold; a prefetch load is the
+    only swap decision of its step (the link was idle) and never comes with an eviction."""
+    rng = random.Random(500 + seed)
+    n = rng.randint(2, 6)
+    sizes = [rng.randint(1, 5) for _ in range(n)]
+    cap = rng.randint(max(sizes), 14)
+    tp = rng.choice([1, 2])
+    e = S.Engine(S.EngineConfig(n, 0, tp, rng.choice([1, 2, 4]), rng.choice([1, 2]), cap=cap, sizes=sizes,
+                                prefetch=True))
+    arrivals = sorted((rng.uniform(0, 10), rng.choices(range(n), weights=[i + 1 for i in range(n)])[0])
+                      for _ in range(30))
+    rid_model, done, pend, n_pf = {}, [], [], 0
+    t, ai = 0.0, 0
+    while ai < len(arrivals) or pend:
+        if ai < len(arrivals) and (not pend or rng.random() < 0.5):
+            t = max(t, arrivals[ai][0])
+            rid_model[ai] = arrivals[ai][1]
+            out = e.step(ev("arrival", t, rid=ai, model=arrivals[ai][1]))
+            ai += 1
+        else:
+            i = rng.randrange(len(pend))
+            if pend[i]["dec"] == "batch":
+                i = next(j for j, x in enumerate(pend) if x["dec"] == "batch")
+            d = pend.pop(i)
+            t += 0.01
+            if d["dec"] == "batch":
+                out = e.step(ev("batch_done", t, batch=d["id"]))
+            else:
+                out = []
+                for r in range(tp):
+                    out += e.step(ev("ack", t, entry=d["id"], rank=r))
+        sw = [d for d in out if d["dec"] in ("load", "offload")]
+        if any(d.get("prefetch") for d in sw):
+            n_pf += 1
+            assert len(sw) == 1
+        for d in out:
+            if d["dec"] in ("load", "offload", "batch"):
+                pend.append(d)
+            if d["dec"] == "complete":
+                done += d["rids"]
+    assert sorted(done) == list(range(len(arrivals)))
+    for m in range(n):
+        mine = [r for r in done if rid_model[r] == m]
+        assert mine == sorted(mine)

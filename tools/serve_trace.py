@@ -50,6 +50,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--out", default="")
     ap.add_argument("--check-logits", type=int, default=-1, help="requests to check vs the oracle (-1 = auto)")
+    ap.add_argument("--prefetch", type=int, default=0, help="1 = NEXT-3 prefetch policy (reading #29)")
     args = ap.parse_args()
     P = dict(PRESETS[args.preset])
     names = P.get("models") or [P["model"]] * P["n"]
@@ -65,11 +66,11 @@ def main():
     else:
         trace = gamma_trace(P["rates"], cv, P["duration"], args.seed, P["L"], min(x.vocab for x in dims))
     budget = P["budget"] if "budget" in P else P["k"] * ((S_r + 4095) // 4096 * 4096)
-    res = {"preset": args.preset, "models": names, "tp": tp, "k": P.get("k"), "budget": budget, "cv": cv,
+    res = {"preset": args.preset, "prefetch": args.prefetch, "models": names, "tp": tp, "k": P.get("k"), "budget": budget, "cv": cv,
            "seed": args.seed, "requests": len(trace), "shard_bytes": sizes_r}
     t_setup = time.perf_counter()
     with M.Ctx(device_ids=(0,) * tp, budget=budget, max_batch=P["max_batch"], max_tokens=P["L"], trace=1,
-               writeback=0, max_dims=d) as ctx:
+               writeback=0, max_dims=d, prefetch=args.prefetch) as ctx:
         ids = [ctx.register_model(x) for x in dims]
         for m in ids:
             ctx.synth_fill(m, 7000 + m)
@@ -104,6 +105,7 @@ def main():
         lat = lat[1:]                       # cold first load reported separately
     res["latency_s"] = metrics.summary(lat)
     res["swaps_in"] = st["swaps_in"]
+    res["prefetches"] = st["prefetches"]
     res["swap_in_GBps_median"] = float(np.median([tp * n / (ms / 1e3) / 1e9 for ms, n in h2d])) if h2d else None
     if len(set(names)) > 1:
         res["latency_by_model_s"] = {k: metrics.summary(v) for k, v in lat_by.items()}
