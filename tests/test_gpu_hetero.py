@@ -1,8 +1,9 @@
 """NEXT-4: models of different sizes share one region per rank, placed
-first-fit (reading #28), with and without the NEXT-3 prefetch policy (reading #29). On the GPU: decisions replay identically through the oracle
-scheduler, every resident model's range is bit-exact on every rank after arbitrary swap traffic,
-the byte-level oracle (RegionSwapModel) predicts every resident hash, host arenas round-trip,
-and logits match the oracle forward."""
+first-fit (reading #28), with and without the NEXT-3 prefetch policy (reading #29).
+On the GPU: decisions replay identically through the oracle scheduler, every resident model's
+range is bit-exact on every rank after arbitrary swap traffic, the byte-level oracle
+(RegionSwapModel) predicts every resident hash, host arenas round-trip, and logits match the
+oracle forward."""
 import random
 
 import numpy as np
