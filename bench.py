@@ -314,7 +314,7 @@ def main():
         print(json.dumps({"impl": "reference", "metric": metric, "value": cb["value"], "unit": "GB/s",
                           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                           "ms_per_step": cb["seconds_per_step_scaled"] * 1e3, "higher_is_better": True,
-                          "scaling": "weak", "vs_baseline": None, "dtype": "u8 (swap) / f64 (forward)",
+                          "scaling": "strong", "vs_baseline": None, "dtype": "u8 (swap) / f64 (forward)",
                           "data": "synthetic", "config": config,
                           "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                           "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -338,7 +338,7 @@ def main():
     line = {
         "metric": metric, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_s_max / steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8 (bf16 weights moved as bytes); forward bf16/fp32-acc",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8 (bf16 weights moved as bytes); forward bf16/fp32-acc",
         "data": "synthetic (counter-based random-init OPT weights, DESIGN.md §Inputs)", "config": config,
         "swap_in_latency_ms": {"p50": 1e3 * OM.nearest_rank(r["swapin_lat_s"], 50),
                                "p99": 1e3 * OM.nearest_rank(r["swapin_lat_s"], 99),
