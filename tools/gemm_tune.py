@@ -1,7 +1,7 @@
 """GEMM microbenchmark sweep (dev): per-layer GEMM shapes of OPT-13B / OPT-1.3B at TP1 x M, for
 tuning knobs given by env vars. Each configuration runs in a fresh process (knobs are read once).
 
-usage: python tools/gemm_tune.py [default|ext|grid|l2pf]"""
+usage: python tools/gemm_tune.py [default|ext|grid|l2pf|smem]"""
 import json, os, subprocess, sys
 MODELS = {"opt-13b": {"qkv": (15360, 5120), "out": (5120, 5120), "fc1": (20480, 5120), "fc2": (5120, 20480)},
           "opt-1.3b": {"qkv": (6144, 2048), "out": (2048, 2048), "fc1": (8192, 2048), "fc2": (2048, 8192)}}
@@ -30,6 +30,9 @@ if mode == "ext":
 elif mode == "l2pf":
     models = "opt-13b,opt-1.3b"
     configs = [("2", {"MPSW_TC_L2PF": v}) for v in ("0", "4", "8", "16", "32")]
+elif mode == "smem":
+    models = "opt-13b,opt-1.3b"
+    configs = [("2", {"MPSW_TC_SMEM_KB": v}) for v in ("56", "72", "88", "104")]
 elif mode == "grid":
     models = "opt-13b,opt-1.3b"
     configs = [("2", {}), ("2", {"MPSW_TC_CPS": "1", "MPSW_TC_SMEM_KB": "200"}),

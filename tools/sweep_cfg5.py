@@ -3,7 +3,7 @@
 For each target size a synthetic OPT-shaped model whose per-rank arena is ~that size is
 registered twice (budget = one slot); swap-in device time (CUDA events on the H2D stream) and
 host-observed latency are measured for the copy-engine and zero-copy paths, clean eviction and
-writeback (paired chunk pipeline). Also the paper's alpha-beta ablation: T separate
+writeback (paired chunk pipeline); with writeback also the D2H of the swap-out alone. Also the paper's alpha-beta ablation: T separate
 per-tensor copies vs one flat copy of the same bytes (torch copy engine), fitting alpha.
 
 usage: python tools/sweep_cfg5.py [--max-gb 8] [--out gpurun_out/cfg5.ndjson]
@@ -46,10 +46,12 @@ def measure(d, mode, writeback, zc_ctas=0, reps=5):
         ctx.synth_fill(a, 1)
         ctx.synth_fill(b, 2)
         ctx.wait(ctx.swap_in(a))
-        dev, host = [], []
+        dev, host, d2h = [], [], []
         cur, other = a, b
         for _ in range(reps + 1):
-            ctx.wait(ctx.swap_out(cur))
+            to = ctx.swap_out(cur)
+            ctx.wait(to)
+            d2h.append(ctx.entry_gpu_ms(to)[2][0])     # D2H alone (writeback) / gate only (clean)
             t = ctx.swap_in(other)
             ts, td = ctx.wait(t)
             dev.append(ctx.entry_gpu_ms(t)[2][0])
@@ -63,8 +65,8 @@ def measure(d, mode, writeback, zc_ctas=0, reps=5):
             rid, _ = ctx.request(a if i % 2 == 0 else b, tok)
             ctx.wait_request(rid, 120)
             pair.append((time.perf_counter() - t0) * 1e3)
-    dev, host = dev[1:], host[1:]
-    return S, float(np.median(dev)), float(np.median(host)), float(np.median(pair[1:]))
+    dev, host, d2h = dev[1:], host[1:], d2h[1:]
+    return S, float(np.median(dev)), float(np.median(host)), float(np.median(pair[1:])), float(np.median(d2h))
 
 
 def alpha_ablation(n_tensors_list=(1, 196, 644, 2000), total=1 << 30):
@@ -106,11 +108,14 @@ def main():
         for mode, zc, wb in [(1, 0, 0), (2, 32, 0), (2, 148, 0), (1, 0, 1)]:
             if mode == 2 and target > (1 << 31):
                 continue
-            S, dev_ms, host_ms, pair_ms = measure(d, mode, wb, zc)
+            S, dev_ms, host_ms, pair_ms, d2h_ms = measure(d, mode, wb, zc)
             r = {"target": target, "S_r": S, "mode": ["", "copy_engine", "zero_copy"][mode], "zc_ctas": zc,
                  "writeback": wb, "swapin_dev_ms": dev_ms, "swapin_host_ms": host_ms,
                  "GBps_dev": S / (dev_ms / 1e3) / 1e9, "GBps_host": S / (host_ms / 1e3) / 1e9,
                  "frac_of_64": S / (dev_ms / 1e3) / 1e9 / 64.0, "request_with_swap_ms": pair_ms}
+            if wb:
+                r["swapout_dev_ms"] = d2h_ms
+                r["GBps_d2h"] = S / (d2h_ms / 1e3) / 1e9
             print(json.dumps(r), flush=True)
             rows.append(r)
     ab = alpha_ablation()
