@@ -35,8 +35,7 @@ elif mode == "smem":
     configs = [("2", {"MPSW_TC_SMEM_KB": v}) for v in ("56", "72", "88", "104")]
 elif mode == "grid":
     models = "opt-13b,opt-1.3b"
-    configs = [("2", {}), ("2", {"MPSW_TC_CPS": "1", "MPSW_TC_SMEM_KB": "200"}),
-               ("2", {"MPSW_TC_CPS": "1", "MPSW_TC_SMEM_KB": "200", "MPSW_TC_EXT_MIN": "32"})]
+    configs = [("2", {}), ("2", {"MPSW_TC_CPS": "1", "MPSW_TC_SMEM_KB": "200"}), ("1", {})]
 for impl, env in configs:
     e = dict(os.environ); e.update(env)
     subprocess.run([sys.executable, __file__, "child", impl, models], env=e)
