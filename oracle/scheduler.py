@@ -1,4 +1,5 @@
 """C1 — engine scheduling semantics (oracle side): per-model FIFO queues, oldest-head batch
+TEST INFRASTRUCTURE (oracle side; see oracle/__init__.py), not product code.
 scheduling, LRU replacement with load/offload entries, ack-based completion.
 
 Paper: P:74 (per-model queues with timestamps; "repeatedly picks a queue to pop oldest request
