@@ -1,4 +1,5 @@
 """C4 — order-independent, position-sensitive 64-bit hash of a byte buffer (oracle side).
+
 TEST INFRASTRUCTURE (oracle side; see oracle/__init__.py), not product code.
 
 Not in the paper; fixed by DESIGN.md (north star: "resident parameters ... bit-exact ...

@@ -1,4 +1,5 @@
 """Alpha-beta transfer cost model (oracle side; virtual-time durations).
+
 TEST INFRASTRUCTURE (oracle side; see oracle/__init__.py), not product code.
 
 P:129: lower bound S/B per GPU (24/32 = 0.75 s), "inversely decrease" with #GPUs.

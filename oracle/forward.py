@@ -1,4 +1,5 @@
 """C5 — OPT forward pass (oracle side), plain definition.
+
 TEST INFRASTRUCTURE (oracle side; see oracle/__init__.py), not product code.
 
 The paper serves OPT-13B and never restates the architecture; the external pin is

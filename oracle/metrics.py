@@ -1,4 +1,5 @@
 """C7 — metrics (oracle side).
+
 TEST INFRASTRUCTURE (oracle side; see oracle/__init__.py), not product code.
 
 * Swap latency window: "we measure from when the offload entry is submitted to

@@ -1,6 +1,7 @@
 """C1 — engine scheduling semantics (oracle side): per-model FIFO queues, oldest-head batch
-TEST INFRASTRUCTURE (oracle side; see oracle/__init__.py), not product code.
 scheduling, LRU replacement with load/offload entries, ack-based completion.
+
+TEST INFRASTRUCTURE (oracle side; see oracle/__init__.py), not product code.
 
 Paper: P:74 (per-model queues with timestamps; "repeatedly picks a queue to pop oldest request
 objects, then packs and submits them ... as a single batch entry"), P:94 (load entries load or

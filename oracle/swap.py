@@ -1,4 +1,5 @@
 """C3 — swap data semantics at byte/chunk level, and the memory budget (oracle side).
+
 TEST INFRASTRUCTURE (oracle side; see oracle/__init__.py), not product code.
 
 P:94: a load entry loads or offloads "the parameters of an instance"; loading and

@@ -1,4 +1,5 @@
 """C0 — synthetic OPT weights from a counter-based generator (oracle side).
+
 TEST INFRASTRUCTURE (oracle side; see oracle/__init__.py), not product code.
 
 Not in the paper (P:127 uses trained OPT-13B; there are no weights here, so random-init
