@@ -32,7 +32,7 @@ def sources():
 def build(verbose=False, force=False):
     os.makedirs(BUILD, exist_ok=True)
     srcs = sources()
-    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".h")]
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     hdrs.append(os.path.join(HERE, "..", "include", "mpsw.h"))
     newest_hdr = max(os.path.getmtime(h) for h in hdrs)
     jobs, objs = [], []

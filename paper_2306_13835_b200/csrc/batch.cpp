@@ -3,6 +3,8 @@
 #include "runtime.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 namespace mpsw {
 
@@ -62,7 +64,18 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
                             R.ws.x, R.ws.a, cs);
         point = 1;
     }
-    for (int l = 0; l < s.n_layers; ++l) {
+    // All layers in one persistent kernel when eligible (bf16, TP = 1, M <= 48, the only rank on
+    // its GPU); it returns 0 otherwise and the per-op kernels below run. Both paths give the same
+    // bits (fwd_fused.cu).
+    bool sole = t == 1;
+    for (const auto& o : c->ranks)
+        if (o.get() != &R && o->device == R.device) sole = false;
+    if (!sole && getenv("MPSW_FUSED_DEBUG")) fprintf(stderr, "[mpsw] fused layers kernel not used: shared GPU / tp\n");
+    const int fused = sole ? fwd_layers_fused(s, Wt, R.ws, B, M, last ? Wt.lnf_w : Wt.layers.back().ln2_w,
+                                              last ? Wt.lnf_b : Wt.layers.back().ln2_b, cs)
+                           : 0;
+    nl += fused;
+    for (int l = 0; l < (fused ? 0 : s.n_layers); ++l) {
         const auto& L = Wt.layers[l];
         nl += fwd_qkv(s, L, R.ws, M, cs);
         nl += fwd_attention(s, R.ws, B, cs);

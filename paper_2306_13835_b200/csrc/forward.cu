@@ -12,7 +12,7 @@
 // (arithmetic intensity ~M flop/B << ridge ~212), so they run on CUDA cores with 128-bit
 // coalesced weight loads; the per-element reduction order depends only on (n, K) — never on
 // M or on the batch composition — so a request's logits are bitwise batch-invariant.
-#include "internal.h"
+#include "fwd_common.cuh"
 
 #include <cuda_bf16.h>
 
@@ -24,7 +24,7 @@ namespace mpsw {
 
 namespace {
 
-using bf16 = __nv_bfloat16;
+using namespace fc;
 
 template <typename T> struct Vec;
 template <> struct Vec<bf16> {
@@ -47,12 +47,6 @@ template <> struct Vec<float> {
         f[0] = u.x; f[1] = u.y; f[2] = u.z; f[3] = u.w;
     }
 };
-
-__device__ __forceinline__ float to_f(bf16 v) { return __bfloat162float(v); }
-__device__ __forceinline__ float to_f(float v) { return v; }
-template <typename T> __device__ __forceinline__ T from_f(float v);
-template <> __device__ __forceinline__ bf16 from_f<bf16>(float v) { return __float2bfloat16_rn(v); }
-template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
 
 // ------------------------------------------------------------------ GEMM (weight streaming)
 enum Epi { EPI_F32 = 0, EPI_RELU_T = 1 };
@@ -235,33 +229,22 @@ struct Peers {
     int n;
 };
 
+
+// Row sum of a 512-thread CTA: warp butterflies, then the 16 warp partials in warp order
+// (fc::ln_red16) — the order the fused layers kernel reproduces with 128 threads.
 __device__ __forceinline__ float block_sum(float v, float* red) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     __syncthreads();
     if (l == 0) red[w] = v;
     __syncthreads();
-    float s = 0.f;
-    for (int i = 0; i < nw; ++i) s += red[i];
-    return s;
+    return ln_red16(red);
 }
 
 // One CTA (512 threads) per row; each thread owns VPT float4 column groups kept in registers,
 // so every global load of the row (t peer partials, residual, bias, position row) is issued
 // before the first use — the kernel is latency-bound at M = 2 rows and this keeps one round
 // trip per operand instead of one per element.
-constexpr int kLnThreads = 512;
-
-template <typename T> __device__ __forceinline__ float4 ld4(const T* p);
-template <> __device__ __forceinline__ float4 ld4<float>(const float* p) { return *reinterpret_cast<const float4*>(p); }
-template <> __device__ __forceinline__ float4 ld4<bf16>(const bf16* p) {
-    const uint2 u = *reinterpret_cast<const uint2*>(p);
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-    return make_float4(a.x, a.y, b.x, b.y);
-}
-
 template <typename T, int VPT>
 __global__ void __launch_bounds__(kLnThreads) reduce_ln_kernel(Peers peers, const float* __restrict__ residual,
                                                               const T* __restrict__ bias, const T* __restrict__ pos_table,
@@ -294,44 +277,30 @@ __global__ void __launch_bounds__(kLnThreads) reduce_ln_kernel(Peers peers, cons
         const int j4 = threadIdx.x + i * kLnThreads;
         if (j4 >= h4) break;
         const int j = 4 * j4;
-        float4 s = *reinterpret_cast<const float4*>(peers.p[0] + row + j);
-#pragma unroll
-        for (int r = 1; r < 8; ++r) {                          // TP all-reduce in rank order
-            if (r < peers.n) {
-                const float4 q = *reinterpret_cast<const float4*>(peers.p[r] + row + j);
-                s.x += q.x; s.y += q.y; s.z += q.z; s.w += q.w;
-            }
-        }
-        if (bias) { s.x = s.x + bi[i].x; s.y = s.y + bi[i].y; s.z = s.z + bi[i].z; s.w = s.w + bi[i].w; }
-        if (prow) { const float4 p = ld4<T>(prow + j); s.x = s.x + p.x; s.y = s.y + p.y; s.z = s.z + p.z; s.w = s.w + p.w; }
-        if (residual) {
-            const float4 q = *reinterpret_cast<const float4*>(residual + row + j);
-            s.x = q.x + s.x; s.y = q.y + s.y; s.z = q.z + s.z; s.w = q.w + s.w;
-        }
+        const float4 s = ln_input4<T>(peers.p, peers.n, row + j, bias != nullptr, bi[i], prow, residual, j);
         x[i] = s;
         *reinterpret_cast<float4*>(x_out + row + j) = s;
-        lsum += (s.x + s.y) + (s.z + s.w);
+        lsum = __fadd_rn(lsum, ln_sum4(s));
     }
-    const float mean = block_sum(lsum, red) / (float)h;
+    const float mean = __fdiv_rn(block_sum(lsum, red), (float)h);
     float lvar = 0.f;
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
         const int j4 = threadIdx.x + i * kLnThreads;
         if (j4 >= h4) break;
-        const float a = x[i].x - mean, b = x[i].y - mean, c = x[i].z - mean, d = x[i].w - mean;
-        lvar += (a * a + b * b) + (c * c + d * d);
+        lvar = __fadd_rn(lvar, ln_var4(x[i], mean));
     }
-    const float var = block_sum(lvar, red) / (float)h;
-    const float den = sqrtf(var + 1e-5f);
+    const float var = __fdiv_rn(block_sum(lvar, red), (float)h);
+    const float den = __fsqrt_rn(__fadd_rn(var, 1e-5f));
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
         const int j4 = threadIdx.x + i * kLnThreads;
         if (j4 >= h4) break;
         T* o = ln_out + row + 4 * j4;
-        o[0] = from_f<T>(((x[i].x - mean) / den) * ga[i].x + be[i].x);
-        o[1] = from_f<T>(((x[i].y - mean) / den) * ga[i].y + be[i].y);
-        o[2] = from_f<T>(((x[i].z - mean) / den) * ga[i].z + be[i].z);
-        o[3] = from_f<T>(((x[i].w - mean) / den) * ga[i].w + be[i].w);
+        o[0] = from_f<T>(ln_norm(x[i].x, mean, den, ga[i].x, be[i].x));
+        o[1] = from_f<T>(ln_norm(x[i].y, mean, den, ga[i].y, be[i].y));
+        o[2] = from_f<T>(ln_norm(x[i].z, mean, den, ga[i].z, be[i].z));
+        o[3] = from_f<T>(ln_norm(x[i].w, mean, den, ga[i].w, be[i].w));
     }
 }
 
@@ -342,49 +311,8 @@ __global__ void __launch_bounds__(128) attention_kernel(const float* __restrict_
     __shared__ float sc[4][128];
     pdl_trigger();
     pdl_wait();
-    const int b = blockIdx.x, head = blockIdx.y;
-    const int s0 = seq_start[b], L = seq_start[b + 1] - s0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int ld = 3 * hl;
-    // lane owns head dims d = lane + 32u (u < 4, d < hd): any hd <= 128
-    for (int i = warp; i < L; i += 4) {
-        const float* q = qkv + (size_t)(s0 + i) * ld + head * hd;
-        float qv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) qv[u] = lane + 32 * u < hd ? q[lane + 32 * u] : 0.f;
-        float mx = -INFINITY;
-        for (int j = 0; j <= i; ++j) {
-            const float* k = qkv + (size_t)(s0 + j) * ld + hl + head * hd;
-            float d = 0.f;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) if (lane + 32 * u < hd) d = fmaf(qv[u], k[lane + 32 * u], d);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
-            if (lane == 0) sc[warp][j] = d;
-            mx = fmaxf(mx, d);
-        }
-        __syncwarp();
-        float sum = 0.f;
-        for (int j = lane; j <= i; j += 32) {
-            const float e = expf(sc[warp][j] - mx);
-            sc[warp][j] = e;
-            sum += e;
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-        __syncwarp();
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int j = 0; j <= i; ++j) {
-            const float p = sc[warp][j] / sum;
-            const float* v = qkv + (size_t)(s0 + j) * ld + 2 * hl + head * hd;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) if (lane + 32 * u < hd) acc[u] = fmaf(p, v[lane + 32 * u], acc[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (lane + 32 * u < hd) o[(size_t)(s0 + i) * hl + head * hd + lane + 32 * u] = from_f<T>(acc[u]);
-        __syncwarp();
-    }
+    attention_item<T>(qkv, seq_start, o, hl, hd, blockIdx.x, blockIdx.y, sc[warp], warp, 4, lane);
 }
 
 inline size_t esz(int dtype) { return dtype == MPSW_BF16 ? 2 : 4; }
@@ -434,6 +362,7 @@ size_t workspace_bytes(const FwdShape& s, int max_rows, int max_batch) {
     b += align_up((3 * (size_t)max_batch + 2 + 2 * M) * 4);     // meta
     b += align_up(tc_ws_floats(s, max_rows) * 4);               // tcgen05 split-K partials
     b += align_up(tc_tiles_max(s) * 4);                         // tile counters
+    b += align_up(fused_bar_count() * 8);                       // fused kernel phase counters
     return b;
 }
 
@@ -454,6 +383,8 @@ void workspace_carve(FwdWorkspace& w, const FwdShape& s, int max_rows, int max_b
     w.meta = (int32_t*)take((3 * (size_t)max_batch + 2 + 2 * M) * 4);
     w.tc_partial = (float*)take(tc_ws_floats(s, max_rows) * 4);
     w.tc_counters = (int*)take(tc_tiles_max(s) * 4);
+    w.fused_bar = (unsigned long long*)take(fused_bar_count() * 8);
+    w.fused_epoch = 0;
     w.bytes = (size_t)(p - (char*)base);
 }
 

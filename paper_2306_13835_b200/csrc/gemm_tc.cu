@@ -14,12 +14,9 @@
 // Split-K over CTAs is chosen from (N, K) only — never from M — and the partial sums are
 // reduced by the last-arriving CTA of each tile in fixed split order, so results are
 // deterministic and bitwise batch-invariant.
-#include "internal.h"
+#include "tc_common.cuh"
 
-#include <cuda.h>
-#include <cudaTypedefs.h>
-#include <cuda_bf16.h>
-
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <unordered_map>
@@ -28,93 +25,7 @@ namespace mpsw {
 
 namespace {
 
-constexpr int kBK = 64;             // K elements per stage (128 bytes of bf16 = one swizzle row)
-constexpr int kBN = 128;            // weight rows per tile (MMA M)
-constexpr int kMaxStages = 12;
-constexpr int kThreads = 256;
-constexpr uint32_t kTileABytes = kBN * kBK * 2;   // 16 KB
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-// Bounded wait: a barrier that never completes (bad tensor map, lost arrive) traps the kernel
-// after ~2^26 polls instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    const uint32_t a = smem_u32(bar);
-    uint32_t done = 0;
-    for (uint32_t it = 0; !done; ++it) {
-        asm volatile(
-            "{\n"
-            ".reg .pred p;\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-            "selp.u32 %0, 1, 0, p;\n"
-            "}\n"
-            : "=r"(done)
-            : "r"(a), "r"(parity)
-            : "memory");
-        if (it > (1u << 26)) __trap();
-    }
-}
-
-__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int c0, int c1) {
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1) : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-            smem_u32(dst)),
-        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-
-// K-major, 128B-swizzled canonical UMMA layout: 8-row x 128 B atoms stacked along rows
-// (SBO = 1024 B), LBO unused (1), descriptor version 1 (sm_100), layout type 2 = SWIZZLE_128B.
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;                 // LBO (ignored for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;       // SBO
-    d |= (uint64_t)1 << 46;                 // version
-    d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
-    return d;
-}
-
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
+using namespace tc;
 
 struct TcSeg {
     int N;              // rows of this segment's weight
@@ -169,11 +80,7 @@ __device__ __forceinline__ const float* partial_run(const TcArgs& g, int cc, int
 __device__ __forceinline__ void epi_store(const TcArgs& g, const TcSeg& seg, int n, int m, float x, float bias_n) {
     const int orow = g.row_of_m ? g.row_of_m[m] : m;
     if (orow < 0) return;
-    if (seg.bias) x = x + bias_n;
-    if (g.epi == 0)
-        reinterpret_cast<float*>(g.out)[(size_t)orow * g.ldo + seg.out_col0 + n] = x * seg.scale;
-    else
-        reinterpret_cast<__nv_bfloat16*>(g.out)[(size_t)orow * g.ldo + seg.out_col0 + n] = __float2bfloat16_rn(fmaxf(x, 0.f));
+    epi_value_store(g.epi, g.out, (size_t)orow * g.ldo + seg.out_col0 + n, x, seg.bias != nullptr, bias_n, seg.scale);
 }
 
 __device__ __forceinline__ int seg_of(const TcArgs& g, int tile) {
@@ -265,17 +172,29 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             stamp(g, c, 2);                        // phase 2: previous kernel complete
             for (int i = 0; i < pre; ++i)
                 tma_load_2d(sb + i * tile_b_bytes, &map_x, &full[i], (int)((u0 + i) % g.kb) * kBK, 0);
-            for (uint64_t u = u0 + pre; u < u1; ++u) {
-                const int i = (int)(u - u0);
-                const int s = i % kStages;
-                const uint32_t ph = (uint32_t)(i / kStages) & 1u;
-                const int tile = (int)(u / g.kb), kbi = (int)(u % g.kb);
-                const int si = seg_of(g, tile);
+            // (tile, k-block, segment, ring slot, parity) advance incrementally: no 64-bit
+            // divisions per unit (the single producer thread's issue rate bounds the stream)
+            uint64_t u = u0 + pre;
+            if (u < u1) {
+                int tile = (int)(u / g.kb), kbi = (int)(u % g.kb), si = seg_of(g, tile);
+                int s = pre % kStages;
+                uint32_t ph = (uint32_t)(pre / kStages) & 1u;
                 const CUtensorMap* mw = si == 0 ? &map_w0 : (si == 1 ? &map_w1 : &map_w2);
-                mbar_wait(&empty[s], ph ^ 1u);
-                mbar_expect_tx(&full[s], kTileABytes + tile_b_bytes);
-                tma_load_2d(sa + s * kTileABytes, mw, &full[s], kbi * kBK, (tile - g.seg[si].tile0) * kBN);
-                tma_load_2d(sb + s * tile_b_bytes, &map_x, &full[s], kbi * kBK, 0);
+                for (; u < u1; ++u) {
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    mbar_expect_tx(&full[s], kTileABytes + tile_b_bytes);
+                    tma_load_2d(sa + s * kTileABytes, mw, &full[s], kbi * kBK, (tile - g.seg[si].tile0) * kBN);
+                    tma_load_2d(sb + s * tile_b_bytes, &map_x, &full[s], kbi * kBK, 0);
+                    if (++s == kStages) { s = 0; ph ^= 1u; }
+                    if (++kbi == g.kb) {
+                        kbi = 0;
+                        ++tile;
+                        if (si + 1 < g.nseg && tile >= g.seg[si + 1].tile0) {
+                            ++si;
+                            mw = si == 1 ? &map_w1 : &map_w2;
+                        }
+                    }
+                }
             }
         }
     } else if (warp == 1) {
@@ -286,12 +205,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                                    ((uint32_t)(kBN >> 4) << 24);
             int run = 0;
             uint32_t tmem_d = tmem_base;
+            int s = 0, kbi = (int)(u0 % g.kb);
+            uint32_t ph = 0;
             for (uint64_t u = u0; u < u1; ++u) {
-                const int i = (int)(u - u0);
-                const int s = i % kStages;
-                const uint32_t ph = (uint32_t)(i / kStages) & 1u;
-                const bool first = u == u0 || u % g.kb == 0;
-                const bool last = u + 1 == u1 || u % g.kb == (uint64_t)g.kb - 1;
+                const bool first = u == u0 || kbi == 0;
+                const bool last = u + 1 == u1 || kbi == g.kb - 1;
                 if (first) {
                     const int b = nacc == 2 ? (run & 1) : 0;
                     const int use = nacc == 2 ? (run >> 1) : run;       // previous uses of buffer b
@@ -311,6 +229,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                     umma_commit(&tmem_full[nacc == 2 ? (run & 1) : 0]);   // accumulator of this run complete
                     ++run;
                 }
+                if (++s == kStages) { s = 0; ph ^= 1u; }
+                if (++kbi == g.kb) kbi = 0;
             }
             stamp(g, c, 4);                        // phase 4: last MMA issued
         }
@@ -456,21 +376,6 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// 2D bf16 tensor map over a row-major [rows, K] matrix, box [box_rows, 64] with 128B swizzle;
-// out-of-bounds rows / K are zero-filled by TMA (ragged N, K and the token padding).
-CUtensorMap make_map(const void* ptr, uint64_t rows, uint64_t K, uint32_t box_rows) {
-    CUtensorMap m;
-    const cuuint64_t dims[2] = {K, rows};
-    const cuuint64_t strides[1] = {K * 2};
-    const cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
-    const cuuint32_t es[2] = {1, 1};
-    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw Error(MPSW_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-    return m;
-}
-
 struct MapKey {
     const void* p;
     uint64_t rows, K;
@@ -489,12 +394,39 @@ const CUtensorMap& cached_map(const void* p, uint64_t rows, uint64_t K, uint32_t
     const MapKey k{p, rows, K, box};
     auto it = cache.find(k);
     if (it != cache.end()) return it->second;
-    return cache.emplace(k, make_map(p, rows, K, box)).first->second;
+    return cache.emplace(k, tc_make_map(p, rows, K, box)).first->second;
 }
 
 }  // namespace
 
-static int sm_count() {
+CUtensorMap tc_make_map(const void* ptr, uint64_t rows, uint64_t K, uint32_t box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {K, rows};
+    const cuuint64_t strides[1] = {K * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(MPSW_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+CUtensorMap tc_make_map_3d(const void* ptr, uint64_t rows, uint64_t K, uint64_t layers, uint64_t layer_stride,
+                           uint32_t box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {K, rows, layers};
+    const cuuint64_t strides[2] = {K * 2, layer_stride};
+    const cuuint32_t box[3] = {(cuuint32_t)kBK, box_rows, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(MPSW_ECUDA, "cuTensorMapEncodeTiled (3d) failed: " + std::to_string((int)r));
+    return m;
+}
+
+int sm_count() {
     static int n = 0;
     if (!n) {
         int dev = 0;
@@ -524,7 +456,7 @@ static int tc_l2_prefetch() {
     return v;
 }
 
-static int tc_ctas_per_sm() {
+int tc_ctas_per_sm() {
     static int v = env_int("MPSW_TC_CPS", 2);
     return v;
 }
@@ -598,7 +530,9 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
     static thread_local size_t attr_set = 0;
     if (attr_set < smem) {
         MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr_set = smem;
+
     }
     g.ext_fixup = Mp >= tc_ext_fixup_min() ? 1 : 0;
     g.trace = g_tc_trace;

@@ -1,0 +1,161 @@
+// Device helpers of the tcgen05 / TMA weight-streaming GEMMs (sm_100a), shared by the per-op
+// GEMM (gemm_tc.cu) and the fused persistent layers kernel (fwd_fused.cu), plus the host-side
+// tensor-map encoders. Included only by .cu files.
+#pragma once
+
+#include "internal.h"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+namespace mpsw {
+namespace tc {
+
+constexpr int kBK = 64;             // K elements per stage (128 bytes of bf16 = one swizzle row)
+constexpr int kBN = 128;            // weight rows per tile (MMA M)
+constexpr int kMaxStages = 12;
+constexpr int kThreads = 256;
+constexpr uint32_t kTileABytes = kBN * kBK * 2;   // 16 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+// Bounded wait: a barrier that never completes (bad tensor map, lost arrive) traps the kernel
+// after ~2^26 polls instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done = 0;
+    for (uint32_t it = 0; !done; ++it) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (it > (1u << 26)) __trap();
+    }
+}
+
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+// K-major, 128B-swizzled canonical UMMA layout: 8-row x 128 B atoms stacked along rows
+// (SBO = 1024 B), LBO unused (1), descriptor version 1 (sm_100), layout type 2 = SWIZZLE_128B.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                 // LBO (ignored for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+    d |= (uint64_t)1 << 46;                 // version
+    d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+
+// Non-blocking probe of an mbarrier phase (true once the phase with this parity completed).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+
+// kind::f16 instruction descriptor: D fp32, A = B = bf16, both K-major, M = 128, N = Mp.
+__device__ __forceinline__ uint32_t umma_idesc(int Mp) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(Mp >> 3) << 17) | ((uint32_t)(kBN >> 4) << 24);
+}
+
+// GEMM epilogue arithmetic, shared by the per-op kernel and the fused layers kernel so both
+// produce the same bits: fp32 out = (acc + bias) * scale, or bf16 out = relu(acc + bias).
+__device__ __forceinline__ void epi_value_store(int epi, void* out, size_t idx, float x, bool has_bias, float bias_n,
+                                                float scale) {
+    if (has_bias) x = __fadd_rn(x, bias_n);
+    if (epi == 0)
+        reinterpret_cast<float*>(out)[idx] = __fmul_rn(x, scale);
+    else
+        reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(fmaxf(x, 0.f));
+}
+
+}  // namespace tc
+
+// Host: 2D bf16 tensor map over a row-major [rows, K] matrix, box [box_rows, 64], 128B swizzle;
+// 3D variant adds a layer dimension of `layers` with byte stride `layer_stride` (equal-stride
+// per-layer tensors of one arena), box [1, box_rows, 64]. Out-of-bounds rows / K are zero-filled.
+CUtensorMap tc_make_map(const void* ptr, uint64_t rows, uint64_t K, uint32_t box_rows);
+int sm_count();
+int tc_ctas_per_sm();
+int tc_stages(int Mp);
+size_t tc_smem_bytes(int Mp);
+CUtensorMap tc_make_map_3d(const void* ptr, uint64_t rows, uint64_t K, uint64_t layers, uint64_t layer_stride,
+                           uint32_t box_rows);
+
+}  // namespace mpsw

@@ -1,6 +1,7 @@
 """Steady-state forward timing through the C-ABI (dev tool): one resident model, back-to-back
-blocking batches, per-batch device time from the library's CUDA events; SIMT vs tcgen05 GEMMs.
-usage: python tools/fwd_bench.py [model=opt-13b] [tc]"""
+blocking batches, per-batch device time from the library's CUDA events.
+impl: 0 auto (= 2 for bf16), 1 SIMT, 2 per-op tcgen05, 3 fused layers kernel (M <= 48, TP 1).
+usage: python tools/fwd_bench.py [model=opt-13b] [tc | impls=0,2] [shapes=1x2,4x8]"""
 import json
 import sys
 import time
@@ -15,8 +16,17 @@ from oracle import layout
 name = sys.argv[1] if len(sys.argv) > 1 else "opt-13b"
 d = opt_dims(name)
 S = layout.shard_bytes(d, 1)
-for B, L in [(1, 2), (8, 8), (32, 8)]:
-    for impl in ((2,) if "tc" in sys.argv[2:] else (1, 2)):
+impls = (1, 2)
+shapes = [(1, 2), (8, 8), (32, 8)]
+for a in sys.argv[2:]:
+    if a == "tc":
+        impls = (2,)
+    elif a.startswith("impls="):
+        impls = tuple(int(x) for x in a[6:].split(","))
+    elif a.startswith("shapes="):
+        shapes = [tuple(int(v) for v in x.split("x")) for x in a[7:].split(",")]
+for B, L in shapes:
+    for impl in impls:
         with M.Ctx(device_ids=(0,), budget=S + 4096, max_batch=B, max_tokens=L, gemm_impl=impl) as ctx:
             m = ctx.register_model(d)
             ctx.synth_fill(m, 1)
@@ -45,6 +55,6 @@ for B, L in [(1, 2), (8, 8), (32, 8)]:
             s1 = ctx.stats()
             nb = s1["fwd_gpu_n"] - s0["fwd_gpu_n"]
             ms = (s1["fwd_gpu_us_sum"] - s0["fwd_gpu_us_sum"]) / 1e3 / max(1, nb)
-            print(json.dumps({"model": name, "B": B, "L": L, "impl": ["", "simt", "tcgen05"][impl], "batches": nb, "batch_rows": B * L,
+            print(json.dumps({"model": name, "B": B, "L": L, "impl": ["auto", "simt", "tcgen05", "fused"][impl], "batches": nb, "batch_rows": B * L,
                               "fwd_ms_device": ms, "GBps": S / (ms / 1e3) / 1e9, "wall_ms_per_round": wall * 1e3}),
                   flush=True)
