@@ -322,10 +322,12 @@ inline size_t esz(int dtype) { return dtype == MPSW_BF16 ? 2 : 4; }
 // ------------------------------------------------------------------ workspace
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-// GEMM shapes of one rank's forward: (n_total, K)
+// GEMM shapes of one rank's forward: (n_total, K). The QKV GEMM tiles each of its three
+// segments separately, so its row count is 3 x hl rounded up to whole 128-row tiles (with
+// hl % 128 != 0, e.g. 1 head of 32 at TP 8, 3 x hl alone undercounts tiles and stream-K CTAs).
 static void gemm_shapes(const FwdShape& s, int out[5][2]) {
     const int hl = s.heads_local * s.head_dim;
-    const int sh[5][2] = {{3 * hl, s.hidden}, {s.hidden, hl}, {s.ffn_local, s.hidden}, {s.hidden, s.ffn_local},
+    const int sh[5][2] = {{3 * ((hl + 127) / 128 * 128), s.hidden}, {s.hidden, hl}, {s.ffn_local, s.hidden}, {s.hidden, s.ffn_local},
                           {s.vocab_local, s.hidden}};
     for (int i = 0; i < 5; ++i) out[i][0] = sh[i][0], out[i][1] = sh[i][1];
 }
@@ -383,6 +385,8 @@ void workspace_carve(FwdWorkspace& w, const FwdShape& s, int max_rows, int max_b
     w.meta = (int32_t*)take((3 * (size_t)max_batch + 2 + 2 * M) * 4);
     w.tc_partial = (float*)take(tc_ws_floats(s, max_rows) * 4);
     w.tc_counters = (int*)take(tc_tiles_max(s) * 4);
+    w.tc_partial_cap = tc_ws_floats(s, max_rows);
+    w.tc_counters_cap = tc_tiles_max(s);
     w.fused_bar = (unsigned long long*)take(fused_bar_count() * 8);
     w.fused_epoch = 0;
     w.bytes = (size_t)(p - (char*)base);
@@ -455,10 +459,16 @@ static void run_gemm(const FwdShape& s, int epi, GemmArgs& g, const FwdWorkspace
         const void* bias[3];
         int N[3], col0[3];
         float sc[3];
+        int tiles = 0;
         for (int i = 0; i < g.nseg; ++i) {
             W[i] = g.seg[i].W; bias[i] = g.seg[i].bias; N[i] = g.seg[i].N; sc[i] = g.seg[i].scale;
             col0[i] = g.seg[i].out_col0;
+            tiles += (N[i] + 127) / 128;
         }
+        // the split-K partials and tile counters live in the rank's workspace: never overrun them
+        const int Mp = std::max(16, (g.M + 15) / 16 * 16);
+        if (tc_partial_floats(tiles * 128, g.K, Mp) > ws.tc_partial_cap || tiles > ws.tc_counters_cap)
+            throw Error(MPSW_EINVARIANT, "tcgen05 GEMM workspace too small for this shape");
         tc_gemm(W, bias, N, sc, col0, g.nseg, g.A, s.max_rows, g.M, g.K, epi, g.out, g.ldo, row_of_m, ws.tc_partial,
                 ws.tc_counters, st);
         return;

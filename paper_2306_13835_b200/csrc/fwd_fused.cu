@@ -752,6 +752,9 @@ int fwd_layers_fused(const FwdShape& s, const TensorPtrs& W, FwdWorkspace& ws, i
         const float sc[1] = {1.0f};
         gemm(g.gm[2], 1, N, b, sc, col0, h, 1, ws.r, ff);
     }
+    for (const FGemm& m : g.gm)                    // split-K partials / counters of the workspace
+        if (tc_partial_floats(m.tiles * kBN, m.K, Mp) > ws.tc_partial_cap || m.tiles > ws.tc_counters_cap)
+            return no("tcgen05 workspace too small");
     g.n_layers = L;
     g.M = M;
     g.Mp = Mp;

@@ -88,6 +88,8 @@ struct FwdWorkspace {        // device buffers of one rank (sized for max_batch*
     int32_t* meta = nullptr;       // seq_start[B+1], last_row[B], pos[M], row_of_m[M]
     float* tc_partial = nullptr;   // tcgen05 split-K partial sums
     int* tc_counters = nullptr;    // per-tile arrival counters (self-resetting)
+    size_t tc_partial_cap = 0;     // floats of tc_partial
+    int tc_counters_cap = 0;       // entries of tc_counters
     unsigned long long* fused_bar = nullptr;   // fused layers kernel: per-phase arrival counters
     uint64_t fused_epoch = 0;      // fused launches so far (host side; counters are monotonic)
     void* base = nullptr;

@@ -1,4 +1,4 @@
-"""Helper for tests: run a 2-rank multi-process TP group on ONE GPU (both processes on cuda:0).
+"""Helper for tests: run a `world`-rank multi-process TP group on ONE GPU (every process on cuda:0).
 Rank 0 (leader) drives requests and explicit swaps; both ranks check their resident shards
 against the oracle image; results are written as JSON by rank 0."""
 import json

@@ -1,5 +1,5 @@
-"""bench.py's N > 1 path end to end: torchrun with 2 processes (one TP=2 group over the shm
-control plane and CUDA IPC), both mapped to cuda:0 (MPSW_BENCH_DEVICE0) with gloo barriers, on a
+"""bench.py's N > 1 path end to end: torchrun with 2 and 4 processes (one TP=N group over the shm
+control plane and CUDA IPC), all mapped to cuda:0 (MPSW_BENCH_DEVICE0) with gloo barriers, on a
 small model; rank 0 prints one JSON line with the contract keys."""
 import json
 import os
@@ -15,17 +15,18 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_bench_torchrun_two_ranks():
+@pytest.mark.parametrize("n", [2, 4])
+def test_bench_torchrun_ranks(n):
     need_gpu()
     env = dict(os.environ, MPSW_BENCH_DEVICE0="1", MPSW_BENCH_BACKEND="gloo")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
-           "127.0.0.1", "--master-port", "29517", "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n), "--master-addr",
+           "127.0.0.1", "--master-port", str(29517 + n), "bench.py", "--gpus", str(n), "--steps", "3", "--warmup", "3",
            "--model", "mid", "--no-cpu-baseline"]
     p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-3000:]
     lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, p.stdout[-2000:]
     o = json.loads(lines[0])
-    assert o["n_gpus"] == 2 and o["config"]["tp"] == 2 and o["steps"] == 3 and o["warmup"] == 3
+    assert o["n_gpus"] == n and o["config"]["tp"] == n and o["steps"] == 3 and o["warmup"] == 3
     assert o["value"] > 0 and o["e2e"]["value"] > 0 and o["gpu_launches"] > 0
     assert o["scaling"] == "strong" and o["roofline"]["bound"] == "pcie"

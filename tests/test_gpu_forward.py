@@ -42,6 +42,23 @@ def test_bf16_logits_parity(tp, name):
     assert st["batches"] >= 1
 
 
+# Per-rank q/k/v widths that are not whole 128-row tiles: small at TP 8 (one 32-wide head per
+# rank) and OPT-125M at TP 4 (hl = 192). The QKV GEMM tiles each segment on its own, so it has
+# more tiles and stream-K CTAs than 3 * hl suggests; the split-K workspace must be sized for that
+# (a regression: it was not, and the partials overran it, giving all-zero logits).
+@pytest.mark.parametrize("name,tp", [("small", 8), ("opt-125m", 4)])
+def test_bf16_parity_ragged_head_tiles(name, tp):
+    M = need_gpu()
+    d = opt_dims(name)
+    toks = [request_tokens(6, 0, i, L, d.vocab) for i, L in enumerate([8, 3, 1, 8])]
+    outs, _ = run_requests(M, d, tp, M.BF16, 23, toks, max_batch=4)
+    W = layout.full_tensors(d, 23, "bf16")
+    for t, y in zip(toks, outs):
+        em = forward.forward_bf16_emulated(d, W, t[None])[0]
+        assert forward.rel_l2(y, em) < 1e-2, forward.rel_l2(y, em)
+        assert int(np.argmax(y)) == int(np.argmax(em))
+
+
 @pytest.mark.parametrize("tp", [1, 2, 4])
 def test_fp32_logits_parity(tp):
     M = need_gpu()

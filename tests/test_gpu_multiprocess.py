@@ -1,4 +1,4 @@
-"""Multi-process TP group (one process per rank; here both on cuda:0): shm control plane,
+"""Multi-process TP group (one process per rank; here all on cuda:0): shm control plane,
 cross-process acks, CUDA-IPC peer partials in the fused all-reduce. Logits vs the oracle and
 resident shards bit-exact on every rank."""
 import json
@@ -26,14 +26,17 @@ def free_port():
     return p
 
 
-def test_two_process_group(tmp_path):
+# 8 processes on one GPU exercise the TP = 8 control plane of cfg4 / `bench.py --gpus 8`: 7 IPC
+# peer mappings per rank, 8-way all-reduce reads, 8 acks per entry
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_process_group(tmp_path, world):
     need_gpu()
     out = str(tmp_path / "mp.json")
     port = free_port()
-    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_group_run.py"), str(r), "2", str(port), out])
-             for r in range(2)]
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_group_run.py"), str(r), str(world), str(port), out])
+             for r in range(world)]
     rcs = [p.wait(timeout=600) for p in procs]
-    assert rcs == [0, 0]
+    assert rcs == [0] * world
     res = json.load(open(out))
     d = opt_dims("small")
     Ws = {m: layout.full_tensors(d, 900 + m) for m in range(3)}
@@ -44,10 +47,11 @@ def test_two_process_group(tmp_path):
     for r in res:
         assert r["checks"] and all(ok for _, ok in r["checks"]), r
         assert r["gpu_ms_local"] > 0
-    assert res[0]["stats"]["swaps_in"] == res[1]["stats"]["swaps_in"] > 0
+    assert len(res) == world
+    assert all(r["stats"]["swaps_in"] == res[0]["stats"]["swaps_in"] for r in res) and res[0]["stats"]["swaps_in"] > 0
     # leader trace replays through the oracle scheduler (acks from both processes)
     from oracle import scheduler as S
     cfg, evs, decs = S.read_trace(out + ".trace")
-    assert cfg.n_models == 3 and cfg.tp == 2 and cfg.cap // cfg.sizes[0] == res[0]["stats"]["k_slots"]
+    assert cfg.n_models == 3 and cfg.tp == world and cfg.cap // cfg.sizes[0] == res[0]["stats"]["k_slots"]
     rdecs, _ = S.replay(cfg, evs)
     assert rdecs == decs
