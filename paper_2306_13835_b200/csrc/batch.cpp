@@ -26,7 +26,8 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
     MPSW_CU(cudaMemcpyAsync(R.ws.meta, ring + c->ring_tok_off + (size_t)c->max_rows * 4, meta_n * 4,
                             cudaMemcpyHostToDevice, cs));
     const int32_t* pos = R.ws.meta + 2 * B + 1;
-    int nl = 0, point = 0;
+    int nl = 0;
+    uint64_t& point = R.ar_point;                  // persistent: parity alternates across batches
     // all-reduce point: record my partial, barrier with the other TP ranks of my stage, wait for
     // every peer's partial on my stream, then the fused reduce + bias + residual + LN kernel
     // reads all t partials directly (peer / IPC mappings over NVLink).
@@ -58,11 +59,12 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
             spin_pause(spins);
         }
         MPSW_CU(cudaStreamWaitEvent(cs, P.ev_stage, 0));
-        MPSW_CU(cudaMemcpyAsync(R.ws.partial[0], P.ws.x, (size_t)M * s.hidden * 4, cudaMemcpyDeviceToDevice, cs));
-        const float* self[1] = {R.ws.partial[0]};
+        float* hop = R.ws.partial[point & 1];
+        MPSW_CU(cudaMemcpyAsync(hop, P.ws.x, (size_t)M * s.hidden * 4, cudaMemcpyDeviceToDevice, cs));
+        const float* self[1] = {hop};
         nl += fwd_reduce_ln(s, M, self, 1, nullptr, nullptr, nullptr, pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b,
                             R.ws.x, R.ws.a, cs);
-        point = 1;
+        ++point;
     }
     // All layers in one persistent kernel when eligible (bf16, TP = 1, M <= 48, the only rank on
     // its GPU); it returns 0 otherwise and the per-op kernels below run. Both paths give the same

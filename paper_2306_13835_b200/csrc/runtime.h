@@ -150,6 +150,10 @@ struct Rank {
     FwdWorkspace ws;
     std::vector<TensorPtrs> wptr;          // per model: pointers into its current range
     cudaEvent_t ev_point[2] = {nullptr, nullptr};   // partial-ready events (interprocess in mp mode)
+    // All-reduce points issued so far by this rank, across batches. Point k uses partial buffer
+    // k & 1; the parity must alternate across batch boundaries too (a batch has an odd number of
+    // points), or with D > 1 a fast peer's next batch overwrites a partial this rank still reads.
+    uint64_t ar_point = 0;
     std::vector<cudaEvent_t> last_compute; // per model
     std::vector<char> last_compute_valid;
     unsigned long long* d_sum = nullptr;
