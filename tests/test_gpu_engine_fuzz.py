@@ -137,3 +137,69 @@ def test_inflight_batches_allreduce_buffers(tp):
     W = layout.full_tensors(d, 9100)
     for t, y in list(zip(toks, res[3]))[::20]:
         assert forward.rel_l2(y, forward.forward_bf16_emulated(d, W, t[None])[0]) < 1e-2
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_engine_fuzz_pipeline(tmp_path, seed):
+    """The same checks with pipeline parallelism (NEXT-1, reading #27): tp x pp ranks (pp 2-4),
+    models of different depths and widths whose stage shards differ in size, D = 1."""
+    M = need_gpu()
+    rnd = random.Random(100 + seed)
+    tp, pp = rnd.choice([(1, 2), (2, 2), (1, 3), (1, 4), (2, 4)])
+    nr = tp * pp
+    dims = []
+    for _ in range(rnd.randint(2, 4)):
+        hd = rnd.choice([32, 64])
+        heads = tp * rnd.randint(1, 4)
+        h = heads * hd
+        dims.append(OptDims(pp * rnd.randint(1, 2), h, heads, 4 * h, vocab=tp * rnd.randint(100, 1500), max_pos=16))
+    big = max(dims, key=lambda d: d.hidden)
+    dmax = OptDims(pp, big.hidden, big.heads, max(d.ffn for d in dims), vocab=max(d.vocab for d in dims), max_pos=16)
+    wb, mode = rnd.choice([0, 1]), rnd.choice([0, 1, 2])
+
+    def img(d, g, s):
+        return layout.shard_image(d, tp, g % tp, s, "bf16", pp, g // tp)
+
+    sizes = [max((layout.shard_bytes(d, tp, "bf16", pp, st) + 4095) // 4096 * 4096 for st in range(pp)) for d in dims]
+    budget = max(sizes) + sum(sorted(sizes)[:-1]) // 2 + 4096
+    seeds = [7500 + 10 * seed + i for i in range(len(dims))]
+    imgs = {m: [img(d, g, seeds[m]) for g in range(nr)] for m, d in enumerate(dims)}
+    ref = {m: [checksum.checksum(a) for a in v] for m, v in imgs.items()}
+    outs = []
+    with M.Ctx(device_ids=(0,) * nr, pp=pp, budget=budget, max_batch=4, max_tokens=8, trace=1, writeback=wb,
+               swap_mode=mode, chunk_bytes=1 << 20, max_dims=dmax) as ctx:
+        ids = [ctx.register_model(d) for d in dims]
+        for m in ids:
+            ctx.synth_fill(m, seeds[m])
+        for step in range(15):
+            pend = []
+            for j in range(rnd.choice([1, 2, 4])):
+                m = rnd.randrange(len(dims))
+                tok = request_tokens(8500 + seed, m, 10 * step + j, rnd.randint(1, 8), dims[m].vocab)
+                rid, out = ctx.request(ids[m], tok)
+                pend.append((rid, m, tok, out))
+            for rid, m, tok, out in pend:
+                ctx.wait_request(rid, 120)
+                outs.append((m, tok, out.copy()))
+            for mm in range(len(dims)):
+                if ctx.residency(ids[mm]) == M.RESIDENT:
+                    for g in range(nr):
+                        assert ctx.checksum(ids[mm], g) == ref[mm][g], (step, mm, g, tp, pp)
+        p = str(tmp_path / "t.ndjson")
+        ctx.trace_dump(p)
+        final_dev = {m: [ctx.checksum(ids[m], g) for g in range(nr)]
+                     for m in range(len(dims)) if ctx.residency(ids[m]) == M.RESIDENT}
+        host = {m: [ctx.checksum(ids[m], g, on_device=False) for g in range(nr)] for m in range(len(dims))}
+    cfg, evs, decs = S.read_trace(p)
+    rdecs, _ = S.replay(cfg, evs)
+    assert rdecs == decs, (tp, pp)
+    sm = RegionSwapModel(imgs, cfg.cap, writeback=bool(wb))
+    sm.apply(decs)
+    assert sm.expected_resident_hashes() == final_dev
+    assert host == ref
+    Ws = {}
+    for m, tok, out in outs[::3]:
+        if m not in Ws:
+            Ws[m] = layout.full_tensors(dims[m], seeds[m])
+        refl = forward.forward_bf16_emulated(dims[m], Ws[m], tok[None])[0]
+        assert forward.rel_l2(out, refl) < 1e-2, (m, tp, pp)
