@@ -203,3 +203,49 @@ def test_engine_fuzz_pipeline(tmp_path, seed):
             Ws[m] = layout.full_tensors(dims[m], seeds[m])
         refl = forward.forward_bf16_emulated(dims[m], Ws[m], tok[None])[0]
         assert forward.rel_l2(out, refl) < 1e-2, (m, tp, pp)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_engine_fuzz_fp32(tmp_path, seed):
+    """fp32 weights (the SIMT parity path, true fp32 FMA) under the same serving fuzz: replay
+    identity, per-burst checksums and logits against the exact oracle at the fp32 bar 1e-5."""
+    M = need_gpu()
+    rnd, dims, dmax, o = random_setup(200 + seed)
+    tp = o["tp"]
+    sizes = [(layout.shard_bytes(d, tp, "fp32") + 4095) // 4096 * 4096 for d in dims]
+    budget = max(sizes) + sum(sorted(sizes)[:-1]) // 2 + 4096
+    seeds = [7700 + 10 * seed + i for i in range(len(dims))]
+    ref = {m: [checksum.checksum(layout.shard_image(d, tp, r, seeds[m], "fp32")) for r in range(tp)]
+           for m, d in enumerate(dims)}
+    outs = []
+    with M.Ctx(device_ids=(0,) * tp, budget=budget, dtype=M.FP32, max_batch=4, max_tokens=8, trace=1,
+               max_inflight=o["D"], writeback=o["writeback"], swap_mode=o["mode"], chunk_bytes=o["chunk"],
+               max_dims=dmax, prefetch=o["prefetch"]) as ctx:
+        ids = [ctx.register_model(d) for d in dims]
+        for m in ids:
+            ctx.synth_fill(m, seeds[m])
+        for step in range(12):
+            pend = []
+            for j in range(rnd.choice([1, 2, 3])):
+                m = rnd.randrange(len(dims))
+                tok = request_tokens(8700 + seed, m, 10 * step + j, rnd.randint(1, 8), dims[m].vocab)
+                rid, out = ctx.request(ids[m], tok)
+                pend.append((rid, m, tok, out))
+            for rid, m, tok, out in pend:
+                ctx.wait_request(rid, 120)
+                outs.append((m, tok, out.copy()))
+            for mm in range(len(dims)):
+                if ctx.residency(ids[mm]) == M.RESIDENT:
+                    for r in range(tp):
+                        assert ctx.checksum(ids[mm], r) == ref[mm][r], (step, mm, r, o)
+        p = str(tmp_path / "t.ndjson")
+        ctx.trace_dump(p)
+    cfg, evs, decs = S.read_trace(p)
+    rdecs, _ = S.replay(cfg, evs)
+    assert rdecs == decs, o
+    Ws = {}
+    for m, tok, out in outs[::3]:
+        if m not in Ws:
+            Ws[m] = layout.full_tensors(dims[m], seeds[m], "fp32")
+        ex = forward.forward_exact(dims[m], Ws[m], tok[None])[0]
+        assert forward.rel_l2(out, ex) < 1e-5, (m, o, forward.rel_l2(out, ex))
