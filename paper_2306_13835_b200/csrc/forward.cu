@@ -272,15 +272,44 @@ __global__ void __launch_bounds__(kLnThreads) reduce_ln_kernel(Peers peers, cons
     float4 x[VPT];
     float lsum = 0.f;
     const T* prow = pos_table ? pos_table + (size_t)pos[m] * h : nullptr;
+    // every load of the row first, then the stores: x_out aliases residual (the residual stream
+    // is updated in place), so a store between two groups' loads would keep the compiler from
+    // issuing the next group's loads early (one dependent L2 round trip per group instead of one)
+    // (the arithmetic is ln_input4's, in its order: peers in rank order, + bias, + position row,
+    // residual + that; peer r's VPT loads are issued together, one round trip per peer)
+    float4 rs[VPT], ps[VPT];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        const int j4 = threadIdx.x + i * kLnThreads;
+        if (j4 < h4) {
+            x[i] = *reinterpret_cast<const float4*>(peers.p[0] + row + 4 * j4);
+            if (residual) rs[i] = *reinterpret_cast<const float4*>(residual + row + 4 * j4);
+            if (prow) ps[i] = ld4<T>(prow + 4 * j4);
+        }
+    }
+    for (int r = 1; r < peers.n; ++r) {
+        float4 q[VPT];
+#pragma unroll
+        for (int i = 0; i < VPT; ++i)
+            if (threadIdx.x + i * kLnThreads < h4)
+                q[i] = *reinterpret_cast<const float4*>(peers.p[r] + row + 4 * (threadIdx.x + i * kLnThreads));
+#pragma unroll
+        for (int i = 0; i < VPT; ++i)
+            if (threadIdx.x + i * kLnThreads < h4) x[i] = add4(x[i], q[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+        if (threadIdx.x + i * kLnThreads >= h4) break;
+        if (bias) x[i] = add4(x[i], bi[i]);
+        if (prow) x[i] = add4(x[i], ps[i]);
+        if (residual) x[i] = add4(rs[i], x[i]);
+    }
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
         const int j4 = threadIdx.x + i * kLnThreads;
         if (j4 >= h4) break;
-        const int j = 4 * j4;
-        const float4 s = ln_input4<T>(peers.p, peers.n, row + j, bias != nullptr, bi[i], prow, residual, j);
-        x[i] = s;
-        *reinterpret_cast<float4*>(x_out + row + j) = s;
-        lsum = __fadd_rn(lsum, ln_sum4(s));
+        *reinterpret_cast<float4*>(x_out + row + 4 * j4) = x[i];
+        lsum = __fadd_rn(lsum, ln_sum4(x[i]));
     }
     const float mean = __fdiv_rn(block_sum(lsum, red), (float)h);
     float lvar = 0.f;
@@ -296,11 +325,9 @@ __global__ void __launch_bounds__(kLnThreads) reduce_ln_kernel(Peers peers, cons
     for (int i = 0; i < VPT; ++i) {
         const int j4 = threadIdx.x + i * kLnThreads;
         if (j4 >= h4) break;
-        T* o = ln_out + row + 4 * j4;
-        o[0] = from_f<T>(ln_norm(x[i].x, mean, den, ga[i].x, be[i].x));
-        o[1] = from_f<T>(ln_norm(x[i].y, mean, den, ga[i].y, be[i].y));
-        o[2] = from_f<T>(ln_norm(x[i].z, mean, den, ga[i].z, be[i].z));
-        o[3] = from_f<T>(ln_norm(x[i].w, mean, den, ga[i].w, be[i].w));
+        store4<T>(ln_out + row + 4 * j4, ln_norm(x[i].x, mean, den, ga[i].x, be[i].x),
+                  ln_norm(x[i].y, mean, den, ga[i].y, be[i].y), ln_norm(x[i].z, mean, den, ga[i].z, be[i].z),
+                  ln_norm(x[i].w, mean, den, ga[i].w, be[i].w));
     }
 }
 
