@@ -727,7 +727,7 @@ int fwd_layers_fused(const FwdShape& s, const TensorPtrs& W, FwdWorkspace& ws, i
         m.K = K;
         m.kb = (K + kBK - 1) / kBK;
         m.units = (uint64_t)tiles * m.kb;
-        m.G = (int)std::min<uint64_t>(m.units, (uint64_t)Gmax);   // = the per-op kernel's grid
+        m.G = tc_grid_tiles(tiles, K);                           // = the per-op kernel's grid
         m.epi = epi;
         m.out = out;
         m.ldo = ldo;

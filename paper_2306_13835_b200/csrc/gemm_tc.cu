@@ -463,9 +463,21 @@ int tc_ctas_per_sm() {
 
 // Persistent grid: a fixed number of CTAs per SM (never a function of M, so the stream-K split
 // and the reduction order are batch-invariant).
+// At least this many (tile, k-block) units (16 KB of weights each) per CTA. Small GEMMs (OPT-125M /
+// 1.3B layers) otherwise run one unit per CTA and split every tile 12-32 ways, so the fix-up
+// chain and per-CTA fixed latency dominate. 8 was the best of 1..32 on B200:
+// OPT-125M M=2 0.59 -> 0.55 ms, M=32 1.40 -> 0.81 ms; OPT-1.3B M=2 1.36 -> 1.14 ms, M=32 2.54 -> 1.98 ms;
+// OPT-13B unchanged (>= 10.8 units per CTA already). Depends on (N, K) only: batch-invariant.
+// MPSW_TC_MINU overrides it (dev).
+static int tc_min_units() {
+    static int v = env_int("MPSW_TC_MINU", 8);
+    return v < 1 ? 1 : v;
+}
+
 static int tc_grid(int tiles, int K) {
     const uint64_t units = (uint64_t)tiles * ((K + kBK - 1) / kBK);
-    return (int)std::min<uint64_t>(units, (uint64_t)tc_ctas_per_sm() * sm_count());
+    const uint64_t mu = (uint64_t)tc_min_units();
+    return (int)std::min<uint64_t>((units + mu - 1) / mu, (uint64_t)tc_ctas_per_sm() * sm_count());
 }
 
 size_t tc_partial_floats(int n_total, int K, int Mp) {
@@ -486,6 +498,7 @@ size_t tc_smem_bytes(int Mp) {
 static unsigned long long* g_tc_trace = nullptr;   // dev instrumentation (mpsw_bench_gemm only)
 void tc_set_trace(unsigned long long* p) { g_tc_trace = p; }
 int tc_grid_for(int n_total, int K) { return tc_grid((n_total + kBN - 1) / kBN, K); }
+int tc_grid_tiles(int tiles, int K) { return tc_grid(tiles, K); }
 
 bool tc_supported(int M, int K) { return M >= 1 && M <= 256 && K % 8 == 0; }
 
