@@ -755,12 +755,18 @@ int fwd_layers_fused(const FwdShape& s, const TensorPtrs& W, FwdWorkspace& ws, i
     for (const FGemm& m : g.gm)                    // split-K partials / counters of the workspace
         if (tc_partial_floats(m.tiles * kBN, m.K, Mp) > ws.tc_partial_cap || m.tiles > ws.tc_counters_cap)
             return no("tcgen05 workspace too small");
+    // Launch only the CTAs that have work: the largest GEMM grid, and 4 per row for the LayerNorm
+    // phases. Every CTA takes part in every phase barrier, so small models (OPT-125M: GEMM grids
+    // of <= 36 CTAs) would otherwise pay 296-way barriers for nothing.
+    int Gl = 4 * M;
+    for (const FGemm& m : g.gm) Gl = std::max(Gl, m.G);
+    Gl = std::min(Gl, Gmax);
     g.n_layers = L;
     g.M = M;
     g.Mp = Mp;
     g.B = B;
     g.stages = tc_stages(Mp);
-    g.Gmax = Gmax;
+    g.Gmax = Gl;
     int nbuf = 32;
     while (nbuf < Mp) nbuf <<= 1;
     g.nbuf = nbuf;
@@ -790,14 +796,14 @@ int fwd_layers_fused(const FwdShape& s, const TensorPtrs& W, FwdWorkspace& ws, i
     // dev instrumentation: MPSW_FUSED_TRACE=path appends the per-CTA phase stamps of one launch
     static const char* trace_path = getenv("MPSW_FUSED_TRACE");
     unsigned long long* dT = nullptr;
-    const size_t nT = (size_t)Gmax * kPhases * L * 2;
+    const size_t nT = (size_t)Gl * kPhases * L * 2;
     if (trace_path) {
         MPSW_CU(cudaMalloc(&dT, nT * 8));
         MPSW_CU(cudaMemsetAsync(dT, 0, nT * 8, st));
     }
     g.trace = dT;
     ws.fused_epoch += 1;
-    g.target = (unsigned long long)Gmax;
+    g.target = (unsigned long long)Gl;
     g.lnflag = ws.fused_bar + kLnFlagOff;
     g.lnx = reinterpret_cast<float*>(ws.fused_bar + kLnxOff);
     g.stamp0 = (unsigned long long)ws.fused_epoch * (2 * kMaxFusedLayers + 2);
@@ -818,11 +824,11 @@ int fwd_layers_fused(const FwdShape& s, const TensorPtrs& W, FwdWorkspace& ws, i
     FusedChain& ch = fused_chain(dev);
     if (ch.last && ch.last != st) MPSW_CU(cudaStreamWaitEvent(st, ch.ev, 0));
     try {
-        launch_pdl(fused_layers_kernel, Gmax, kThreads, smem, st, mq, mk, mv, mo, m1, m2, xa, xo, xr, g);
+        launch_pdl(fused_layers_kernel, Gl, kThreads, smem, st, mq, mk, mv, mo, m1, m2, xa, xo, xr, g);
     } catch (const Error& e) {
         cudaFuncAttributes fa{};
         cudaFuncGetAttributes(&fa, fused_layers_kernel);
-        throw Error(e.status, std::string("fused layers kernel launch (grid ") + std::to_string(Gmax) + ", smem " +
+        throw Error(e.status, std::string("fused layers kernel launch (grid ") + std::to_string(Gl) + ", smem " +
                                   std::to_string(smem) + ", params " + std::to_string(sizeof(FusedArgs) + 9 * sizeof(CUtensorMap)) +
                                   ", max threads " + std::to_string(fa.maxThreadsPerBlock) + ", max dyn smem " +
                                   std::to_string(fa.maxDynamicSharedSizeBytes) + "): " + e.what());
@@ -836,7 +842,7 @@ int fwd_layers_fused(const FwdShape& s, const TensorPtrs& W, FwdWorkspace& ws, i
         MPSW_CU(cudaMemcpy(hv.data(), dT, nT * 8, cudaMemcpyDeviceToHost));
         cudaFree(dT);
         if (FILE* f = fopen(trace_path, "a")) {
-            fprintf(f, "{\"M\":%d,\"L\":%d,\"G\":%d,\"h\":%d,\"t\":[", M, L, Gmax, h);
+            fprintf(f, "{\"M\":%d,\"L\":%d,\"G\":%d,\"h\":%d,\"t\":[", M, L, Gl, h);
             for (size_t i = 0; i < nT; ++i) fprintf(f, "%s%llu", i ? "," : "", hv[i]);
             fprintf(f, "]}\n");
             fclose(f);
