@@ -287,15 +287,33 @@ __global__ void __launch_bounds__(kLnThreads) reduce_ln_kernel(Peers peers, cons
             if (prow) ps[i] = ld4<T>(prow + 4 * j4);
         }
     }
-    for (int r = 1; r < peers.n; ++r) {
-        float4 q[VPT];
+    // the other peers' partials (TP all-reduce over NVLink): one dependent round trip per peer
+    // (all column groups of that peer in flight) or per column group (all peers in flight),
+    // whichever is fewer; the adds stay in rank order either way
+    if (peers.n - 1 <= VPT) {
+        for (int r = 1; r < peers.n; ++r) {
+            float4 q[VPT];
 #pragma unroll
-        for (int i = 0; i < VPT; ++i)
-            if (threadIdx.x + i * kLnThreads < h4)
-                q[i] = *reinterpret_cast<const float4*>(peers.p[r] + row + 4 * (threadIdx.x + i * kLnThreads));
+            for (int i = 0; i < VPT; ++i)
+                if (threadIdx.x + i * kLnThreads < h4)
+                    q[i] = *reinterpret_cast<const float4*>(peers.p[r] + row + 4 * (threadIdx.x + i * kLnThreads));
 #pragma unroll
-        for (int i = 0; i < VPT; ++i)
-            if (threadIdx.x + i * kLnThreads < h4) x[i] = add4(x[i], q[i]);
+            for (int i = 0; i < VPT; ++i)
+                if (threadIdx.x + i * kLnThreads < h4) x[i] = add4(x[i], q[i]);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            if (threadIdx.x + i * kLnThreads >= h4) break;
+            const size_t off = row + 4 * (threadIdx.x + i * kLnThreads);
+            float4 q[7];
+#pragma unroll
+            for (int r = 1; r < 8; ++r)
+                if (r < peers.n) q[r - 1] = *reinterpret_cast<const float4*>(peers.p[r] + off);
+#pragma unroll
+            for (int r = 1; r < 8; ++r)
+                if (r < peers.n) x[i] = add4(x[i], q[r - 1]);
+        }
     }
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
