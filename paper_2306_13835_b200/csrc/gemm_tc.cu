@@ -474,10 +474,31 @@ static int tc_min_units() {
     return v < 1 ? 1 : v;
 }
 
+// Tile-aligned split: G = tiles x s with s | kb, the largest s with G <= 2 x #SMs and
+// kb / s >= tc_min_units(). Every CTA then covers kb / s k-blocks of ONE tile (no CTA straddles
+// two tiles; each tile is reduced from s equal runs). Used only when it keeps >= 80 % of the
+// stream-K grid: with fewer CTAs the large-M GEMMs lose tensor throughput (per shape, M = 2 / 256,
+// profiles/r01_gemm_align.ndjson: OPT-13B QKV, 240 vs 296 CTAs, 31.3 -> 28.4 / 62.6 -> 59.7 us;
+// fc1, 160 vs 296, 38.2 -> 38.4 / 73.6 -> 102.1 us; OPT-125M QKV, 18 vs 27, 16.6 -> 35.6 us at
+// M = 256). Depends on (N, K) only. MPSW_TC_ALIGN=0 restores plain stream-K (dev).
+static int tc_align() {
+    static int v = env_int("MPSW_TC_ALIGN", 1);   // see tc_grid
+    return v;
+}
+
 static int tc_grid(int tiles, int K) {
-    const uint64_t units = (uint64_t)tiles * ((K + kBK - 1) / kBK);
+    const int kb = (K + kBK - 1) / kBK;
+    const uint64_t units = (uint64_t)tiles * kb;
     const uint64_t mu = (uint64_t)tc_min_units();
-    return (int)std::min<uint64_t>((units + mu - 1) / mu, (uint64_t)tc_ctas_per_sm() * sm_count());
+    const uint64_t gmax = (uint64_t)tc_ctas_per_sm() * sm_count();
+    const uint64_t g_sk = std::min<uint64_t>((units + mu - 1) / mu, gmax);
+    if (tc_align() && (uint64_t)tiles < gmax) {
+        int best = 0;
+        for (int sp = 1; sp <= kb; ++sp)
+            if (kb % sp == 0 && (uint64_t)tiles * sp <= gmax && (uint64_t)(kb / sp) >= mu) best = sp;
+        if (best && (uint64_t)tiles * best * 5 >= g_sk * 4) return tiles * best;
+    }
+    return (int)g_sk;
 }
 
 size_t tc_partial_floats(int n_total, int K, int Mp) {

@@ -1,10 +1,11 @@
 """GEMM microbenchmark sweep (dev): per-layer GEMM shapes of OPT-13B / OPT-1.3B at TP1 x M, for
 tuning knobs given by env vars. Each configuration runs in a fresh process (knobs are read once).
 
-usage: python tools/gemm_tune.py [default|ext|grid|l2pf|smem]"""
+usage: python tools/gemm_tune.py [default|ext|grid|l2pf|smem|align]"""
 import json, os, subprocess, sys
 MODELS = {"opt-13b": {"qkv": (15360, 5120), "out": (5120, 5120), "fc1": (20480, 5120), "fc2": (5120, 20480)},
-          "opt-1.3b": {"qkv": (6144, 2048), "out": (2048, 2048), "fc1": (8192, 2048), "fc2": (2048, 8192)}}
+          "opt-1.3b": {"qkv": (6144, 2048), "out": (2048, 2048), "fc1": (8192, 2048), "fc2": (2048, 8192)},
+          "opt-125m": {"qkv": (2304, 768), "out": (768, 768), "fc1": (3072, 768), "fc2": (768, 3072)}}
 if len(sys.argv) > 1 and sys.argv[1] == "child":
     sys.path.insert(0, ".")
     from paper_2306_13835_b200 import mpsw as M
@@ -33,6 +34,9 @@ elif mode == "l2pf":
 elif mode == "smem":
     models = "opt-13b,opt-1.3b"
     configs = [("2", {"MPSW_TC_SMEM_KB": v}) for v in ("56", "72", "88", "104")]
+elif mode == "align":
+    models = "opt-13b,opt-1.3b,opt-125m"
+    configs = [("2", {"MPSW_TC_ALIGN": v}) for v in ("0", "1")]
 elif mode == "grid":
     models = "opt-13b,opt-1.3b"
     configs = [("2", {}), ("2", {"MPSW_TC_CPS": "1", "MPSW_TC_SMEM_KB": "200"}), ("1", {})]
