@@ -249,3 +249,40 @@ def test_engine_fuzz_fp32(tmp_path, seed):
             Ws[m] = layout.full_tensors(dims[m], seeds[m], "fp32")
         ex = forward.forward_exact(dims[m], Ws[m], tok[None])[0]
         assert forward.rel_l2(out, ex) < 1e-5, (m, o, forward.rel_l2(out, ex))
+
+
+def test_long_run_many_swaps(tmp_path):
+    """3000 requests round-robin over 3 models with room for one, 8 outstanding (batches of two
+    form, so about every fourth request swaps), TP 2, D = 2, writeback: no resource runs out
+    (events, staging ring, request ids, ack slots), every request completes, the decisions
+    replay, and the last resident model is bit-exact on device and in its host arena."""
+    M = need_gpu()
+    d = OptDims(1, 128, 2, 512, vocab=512, max_pos=16)
+    tp = 2
+    S_ = placement_bytes(d, tp)
+    seeds = [9300 + i for i in range(3)]
+    with M.Ctx(device_ids=(0,) * tp, budget=S_ + 4096, max_batch=2, max_tokens=4, trace=1, max_inflight=2,
+               writeback=1, chunk_bytes=1 << 20) as ctx:
+        ids = [ctx.register_model(d) for _ in range(3)]
+        for m in ids:
+            ctx.synth_fill(m, seeds[m])
+        pend = []
+        for i in range(3000):
+            pend.append(ctx.request(ids[i % 3], np.array([1 + i % 7, 2, 3], np.int32))[0])
+            if len(pend) >= 8:
+                ctx.wait_request(pend.pop(0), 120)
+        for rid in pend:
+            ctx.wait_request(rid, 120)
+        st = ctx.stats()
+        p = str(tmp_path / "t.ndjson")
+        ctx.trace_dump(p)
+        res = [m for m in range(3) if ctx.residency(ids[m]) == M.RESIDENT]
+        assert len(res) == 1
+        m = res[0]
+        for r in range(tp):
+            assert ctx.checksum(ids[m], r) == checksum.checksum(layout.shard_image(d, tp, r, seeds[m]))
+            assert ctx.checksum(ids[m], r, on_device=False) == checksum.checksum(layout.shard_image(d, tp, r, seeds[m]))
+    assert st["swaps_in"] >= 500
+    cfg, evs, decs = S.read_trace(p)
+    rdecs, _ = S.replay(cfg, evs)
+    assert rdecs == decs
