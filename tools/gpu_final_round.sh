@@ -24,6 +24,8 @@ python tools/tc_trace.py show $O/tc_trace.ndjson > $O/tc_trace.txt 2>&1
 timeout 900 python tools/fwd_bench.py opt-13b > $O/fwd_bench.txt 2>&1
 timeout 600 python tools/fwd_bench.py opt-1.3b tc >> $O/fwd_bench.txt 2>&1
 timeout 900 python tools/gemm_tune.py grid > $O/gemm_tune.txt 2>&1
+timeout 1500 python tools/gemm_tune.py align > $O/gemm_align.txt 2>&1
+for cfg in "opt-13b 2 1 2" "opt-13b 8 1 2" "opt-1.3b 8 1 2"; do timeout 600 python tools/fwd_tp.py $cfg >> $O/fwd_tp.txt 2>&1; done
 rm -f $O/serve.ndjson
 timeout 300 python tools/serve_trace.py cfg1 --out $O/serve.ndjson
 for seed in 0 1 2; do
