@@ -28,6 +28,25 @@ mpsw_status mpsw_test_gemm(int device, int dtype, int impl, const void* W, const
  * allocated, filled with a constant and freed inside. */
 mpsw_status mpsw_bench_gemm(int device, int impl, int M, int N, int K, int reps, float* us);
 
+/* Intermediate-value tap of the TP forward (a6), for element-by-element parity with the oracle's
+ * per-layer values (oracle/forward.py `taps`). Arms a ONE-SHOT tap on `ctx`: the next batch the
+ * engine dispatches runs the same kernels as a normal batch (per-op path: the fused layers kernel
+ * is bypassed) but stops early, and global rank `rank`'s worker copies one workspace buffer into
+ * `dst` before the batch completes. The batch's logits are undefined (lm_head does not run).
+ *   what = MPSW_TAP_X   : fp32 residual stream [M, h] after `n_layers` complete decoder layers
+ *                         (n_layers = 0: the embedding sum E_tok[x] + E_pos[pos], C5 step 1);
+ *          MPSW_TAP_A   : LN output [M, h] (the next GEMM's A operand: LN1 of layer n_layers, or
+ *                         the final LN when n_layers = L_m), in the ctx dtype (bf16 bits / fp32);
+ *          MPSW_TAP_QKV : fp32 [M, 3*h/t] = [q | k | v] of layer n_layers on that rank (q scaled
+ *                         by hd^-0.5 after its bias, HF:opt.py:151);
+ *          MPSW_TAP_O   : attention output [M, h/t] of layer n_layers (ctx dtype);
+ *          MPSW_TAP_R   : ReLU(fc1) output [M, ff/t] of layer n_layers (ctx dtype).
+ * Rows are the batch's packed token rows (requests in batch order). At most `bytes` bytes are
+ * written; dst is host memory that must stay valid until the batch completes.
+ * Single-process ctx with pp = 1 only. Errors: EINVAL (bad argument, mp mode, pp > 1). */
+enum { MPSW_TAP_X = 0, MPSW_TAP_A = 1, MPSW_TAP_QKV = 2, MPSW_TAP_O = 3, MPSW_TAP_R = 4 };
+mpsw_status mpsw_test_tap(mpsw_ctx* ctx, int n_layers, int what, int rank, void* dst, uint64_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -52,36 +52,53 @@ def _attention(q, k, v, heads, dt):
     return o.transpose(0, 2, 1, 3).reshape(B, L, H).astype(dt)
 
 
-def _run(d, W, tokens, dt, rnd):
+def _run(d, W, tokens, dt, rnd, taps=None, n_layers=None):
+    """taps: optional dict filled with the intermediate values, keyed (name, layer):
+    ("x", l) residual stream after l layers [B, L, h]; ("a", l) the LN output feeding layer l
+    (l = L_m: the final LN over all positions); ("qkv", l) = [q | k | v] [B, L, 3h] (q scaled);
+    ("o", l) attention output [B, L, h]; ("r", l) ReLU output [B, L, ff]. Recording only: the
+    arithmetic is the same with or without it. n_layers: stop after that many layers (returns
+    None; for taps)."""
     tokens = np.asarray(tokens)
     B, L = tokens.shape
     hd = d.hidden // d.heads
     g = lambda n: W[n].astype(dt)
+    rec = (lambda k, l, v: taps.__setitem__((k, l), v)) if taps is not None else (lambda k, l, v: None)
     h = g("decoder.embed_tokens.weight")[tokens] + g("decoder.embed_positions.weight")[np.arange(L) + 2][None]
+    rec("x", 0, h)
     scale = dt(hd ** -0.5)
-    for i in range(d.n_layers):
+    for i in range(d.n_layers if n_layers is None else n_layers):
         p = f"decoder.layers.{i}."
         a = rnd(layer_norm(h, W[p + "self_attn_layer_norm.weight"], W[p + "self_attn_layer_norm.bias"], dt))
+        rec("a", i, a)
         q = (a @ g(p + "self_attn.q_proj.weight").T + g(p + "self_attn.q_proj.bias")) * scale
         k = a @ g(p + "self_attn.k_proj.weight").T + g(p + "self_attn.k_proj.bias")
         v = a @ g(p + "self_attn.v_proj.weight").T + g(p + "self_attn.v_proj.bias")
+        rec("qkv", i, np.concatenate([q, k, v], axis=-1))
         o = rnd(_attention(q, k, v, d.heads, dt))
+        rec("o", i, o)
         h = h + (o @ g(p + "self_attn.out_proj.weight").T + g(p + "self_attn.out_proj.bias"))
         f = rnd(layer_norm(h, W[p + "final_layer_norm.weight"], W[p + "final_layer_norm.bias"], dt))
         r = rnd(np.maximum(f @ g(p + "fc1.weight").T + g(p + "fc1.bias"), dt(0)))
+        rec("r", i, r)
         h = h + (r @ g(p + "fc2.weight").T + g(p + "fc2.bias"))
+        rec("x", i + 1, h)
+    if n_layers is not None and n_layers < d.n_layers:
+        return None
+    if taps is not None:
+        rec("a", d.n_layers, rnd(layer_norm(h, W["decoder.final_layer_norm.weight"], W["decoder.final_layer_norm.bias"], dt)))
     x = rnd(layer_norm(h[:, L - 1], W["decoder.final_layer_norm.weight"], W["decoder.final_layer_norm.bias"], dt))
     return x @ g("decoder.embed_tokens.weight").T
 
 
-def forward_exact(d, W, tokens):
+def forward_exact(d, W, tokens, taps=None, n_layers=None):
     """float64 logits [B, V] of the last position.  W: dict name -> full tensor values."""
-    return _run(d, W, tokens, np.float64, lambda x: x)
+    return _run(d, W, tokens, np.float64, lambda x: x, taps, n_layers)
 
 
-def forward_bf16_emulated(d, W, tokens):
+def forward_bf16_emulated(d, W, tokens, taps=None, n_layers=None):
     """float32 logits [B, V], bf16 rounding at the GEMM A-operand storage points."""
-    return _run(d, W, tokens, np.float32, lambda x: round_bf16(x.astype(np.float32)))
+    return _run(d, W, tokens, np.float32, lambda x: round_bf16(x.astype(np.float32)), taps, n_layers)
 
 
 def forward_tp_simulated(d, shards, tokens, dt=np.float64):

@@ -1,6 +1,7 @@
 // Batch entries (a6 / a7): the TP (x PP) forward of one rank, with the all-reduce fused into the
 // LayerNorm kernel over peer memory, and the logits slice returned to the pinned staging ring.
 #include "runtime.h"
+#include "../../include/mpsw_testing.h"
 
 #include <algorithm>
 #include <cstdio>
@@ -69,7 +70,19 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
     // All layers in one persistent kernel when eligible (bf16, TP = 1, M <= 48, the only rank on
     // its GPU); it returns 0 otherwise and the per-op kernels below run. Both paths give the same
     // bits (fwd_fused.cu).
-    bool sole = t == 1;
+    // verification tap (mpsw_test_tap): stop after e.tap.n_layers layers (X / A) or inside layer
+    // n_layers (QKV / O / R); every rank stops at the same point, so the all-reduce points match
+    const Tap& tap = e.tap;
+    const bool tapping = tap.dst != nullptr;
+    bool tapped = false;
+    auto tap_copy = [&](const void* src, size_t bytes) {
+        if (R.index == tap.rank)
+            MPSW_CU(cudaMemcpyAsync(tap.dst, src, std::min<size_t>(bytes, tap.bytes), cudaMemcpyDeviceToHost, cs));
+        tapped = true;
+    };
+    const size_t esz = s.dtype == MPSW_BF16 ? 2 : 4;
+    const int hl = s.heads_local * s.head_dim;
+    bool sole = t == 1 && !tapping;
     for (const auto& o : c->ranks)
         if (o.get() != &R && o->device == R.device) sole = false;
     if (!sole && getenv("MPSW_FUSED_DEBUG")) fprintf(stderr, "[mpsw] fused layers kernel not used: shared GPU / tp\n");
@@ -78,12 +91,17 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
                            : 0;
     nl += fused;
     for (int l = 0; l < (fused ? 0 : s.n_layers); ++l) {
+        if (tapping && l == tap.n_layers && tap.what <= MPSW_TAP_A) break;
+        const bool tap_here = tapping && l == tap.n_layers;
         const auto& L = Wt.layers[l];
         nl += fwd_qkv(s, L, R.ws, M, cs);
+        if (tap_here && tap.what == MPSW_TAP_QKV) { tap_copy(R.ws.qkv, (size_t)M * 3 * hl * 4); break; }
         nl += fwd_attention(s, R.ws, B, cs);
+        if (tap_here && tap.what == MPSW_TAP_O) { tap_copy(R.ws.o, (size_t)M * hl * esz); break; }
         nl += fwd_out_proj(s, L, R.ws, M, R.ws.partial[point & 1], cs);
         allreduce_ln(R.ws.x, L.o_b, nullptr, L.ln2_w, L.ln2_b);
         nl += fwd_fc1(s, L, R.ws, M, cs);
+        if (tap_here && tap.what == MPSW_TAP_R) { tap_copy(R.ws.r, (size_t)M * s.ffn_local * esz); break; }
         nl += fwd_fc2(s, L, R.ws, M, R.ws.partial[point & 1], cs);
         const bool lastl = l + 1 == s.n_layers;
         // after a non-final stage's last layer only the residual stream matters; the LN output
@@ -92,12 +110,16 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
         const void* nb = lastl ? (last ? Wt.lnf_b : L.ln2_b) : Wt.layers[l + 1].ln1_b;
         allreduce_ln(R.ws.x, L.fc2_b, nullptr, ng, nb);
     }
-    if (last) {
+    if (tapping && !tapped) {
+        if (tap.what == MPSW_TAP_X) tap_copy(R.ws.x, (size_t)M * s.hidden * 4);
+        else if (tap.what == MPSW_TAP_A) tap_copy(R.ws.a, (size_t)M * s.hidden * esz);
+    }
+    if (last && !tapping) {
         nl += fwd_lm_head(s, Wt, R.ws, B, M, cs);
         float* logits_host = (float*)(ring) + (size_t)R.trank * s.vocab_local;
         MPSW_CU(cudaMemcpy2DAsync(logits_host, (size_t)s.vocab * 4, R.ws.logits, (size_t)s.vocab_local * 4,
                                   (size_t)s.vocab_local * 4, B, cudaMemcpyDeviceToHost, cs));
-    } else {
+    } else if (!last) {
         MPSW_CU(cudaEventRecord(R.ev_stage, cs));
         R.stage_out.store(e.id + 1, std::memory_order_release);
     }

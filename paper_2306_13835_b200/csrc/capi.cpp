@@ -1,6 +1,7 @@
 // The C-ABI entry points of include/mpsw.h (argument checking, ctx construction / teardown, and
 // the thin request / swap / query calls into the engine).
 #include "runtime.h"
+#include "../../include/mpsw_testing.h"
 
 #include <sys/mman.h>
 #include <unistd.h>
@@ -624,6 +625,18 @@ mpsw_status mpsw_peek(mpsw_ctx* c, int model_id, int rank, uint64_t offset, uint
     MPSW_CU(cudaSetDevice(R.device));
     MPSW_CU(cudaMemcpyAsync(dst, R.region + off + offset, bytes, cudaMemcpyDeviceToHost, R.aux));
     MPSW_CU(cudaStreamSynchronize(R.aux));
+    return MPSW_OK;
+    API_END
+}
+
+mpsw_status mpsw_test_tap(mpsw_ctx* c, int n_layers, int what, int rank, void* dst, uint64_t bytes) {
+    API_BEGIN
+    if (!c || !dst || !bytes) return set_error(MPSW_EINVAL, "NULL argument");
+    if (c->mp || c->pp != 1) return set_error(MPSW_EINVAL, "tap: single-process ctx with pp = 1 only");
+    if (what < MPSW_TAP_X || what > MPSW_TAP_R || n_layers < 0 || rank < 0 || rank >= c->nr)
+        return set_error(MPSW_EINVAL, "tap: bad what / n_layers / rank");
+    std::lock_guard<std::mutex> lk(c->tap_mu);
+    c->tap_next = Tap{n_layers, what, rank, dst, bytes};
     return MPSW_OK;
     API_END
 }

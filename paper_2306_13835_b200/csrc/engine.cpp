@@ -201,6 +201,11 @@ void dispatch(mpsw_ctx* c, const std::vector<Decision>& ds, double now) {
             for (int b = 0; b < B; ++b) row_of_m[meta[B + 1 + b]] = b;
             e->B = B;
             e->M = M;
+            std::lock_guard<std::mutex> lk(c->tap_mu);
+            if (c->tap_next.dst) {
+                e->tap = c->tap_next;
+                c->tap_next = Tap{};
+            }
         } else {
             std::lock_guard<std::mutex> lk(c->done_mu);
             c->entries[e->id] = e;

@@ -89,7 +89,15 @@ struct ReqRec {
     std::atomic<int> done{0};
 };
 
+// One-shot forward tap (include/mpsw_testing.h, mpsw_test_tap): copied into the next batch entry.
+struct Tap {
+    int n_layers = -1, what = 0, rank = 0;
+    void* dst = nullptr;
+    uint64_t bytes = 0;
+};
+
 struct Entry {
+    Tap tap;                                     // batch: verification tap (dst == nullptr: none)
     uint64_t id = 0;
     int kind = 0, model = -1;
     uint64_t off = 0;                            // load / offload: byte offset in the region
@@ -233,6 +241,8 @@ struct mpsw_ctx {
     std::atomic<int64_t> next_rid{0};
     int ring_next = 0;
     std::mutex api_mu;
+    std::mutex tap_mu;
+    mpsw::Tap tap_next;        // armed by mpsw_test_tap, taken by the next dispatched batch
     // follower-local view of residency (mp followers)
     std::vector<int64_t> f_off_of;
     std::vector<int> f_state;

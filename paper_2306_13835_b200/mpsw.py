@@ -16,6 +16,7 @@ STATUS_NAMES = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "EBUSY", -4: "ENOENT", 
 BF16, FP32 = 0, 1
 SWAP_AUTO, SWAP_COPY_ENGINE, SWAP_ZERO_COPY, SWAP_HYBRID = 0, 1, 2, 3
 EVICTED, LOADING, RESIDENT, OFFLOADING = 0, 1, 2, 3
+TAP_X, TAP_A, TAP_QKV, TAP_O, TAP_R = 0, 1, 2, 3, 4
 NOOP_TICKET = (1 << 64) - 1
 
 
@@ -80,6 +81,7 @@ _SIGS = {
     "mpsw_bench_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)],
     "mpsw_test_gemm": [C.c_int, C.c_int, C.c_int, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float,
                        C.POINTER(C.c_float)],
+    "mpsw_test_tap": [_P, C.c_int, C.c_int, C.c_int, _P, C.c_uint64],
 }
 
 _lib = None
@@ -272,6 +274,14 @@ class Ctx:
         self._live.pop(rid, None)
         self._done[rid] = (a.value, d.value)
         return a.value, d.value
+
+    def tap(self, n_layers, what, rank, nbytes):
+        """Arm the one-shot forward tap (include/mpsw_testing.h) and return the host buffer the
+        next dispatched batch fills (uint8, nbytes); valid once that batch's request completed."""
+        buf = np.zeros(nbytes, np.uint8)
+        _check(lib().mpsw_test_tap(self.h, n_layers, what, rank, buf.ctypes.data, nbytes))
+        self._tap_buf = buf
+        return buf
 
     def checksum(self, model_id, rank, on_device=True):
         h = C.c_uint64()

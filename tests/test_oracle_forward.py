@@ -7,6 +7,22 @@ from synth import opt_dims, request_tokens
 from oracle import layout, forward
 
 
+def _hf_model(d, W, dtype):
+    torch = pytest.importorskip("torch")
+    tr = pytest.importorskip("transformers")
+    cfg = tr.OPTConfig(vocab_size=d.vocab, hidden_size=d.hidden, num_hidden_layers=d.n_layers,
+                       ffn_dim=d.ffn, num_attention_heads=d.heads, max_position_embeddings=d.max_pos,
+                       word_embed_proj_dim=d.hidden, dropout=0.0, attention_dropout=0.0,
+                       pad_token_id=1, attn_implementation="eager")
+    m = tr.OPTForCausalLM(cfg).to(dtype).eval()
+    npdt = np.float64 if dtype == torch.float64 else np.float32
+    sd = {"model." + k: torch.from_numpy(np.asarray(v, npdt)) for k, v in W.items()}
+    sd["lm_head.weight"] = sd["model.decoder.embed_tokens.weight"]
+    missing, unexpected = m.load_state_dict(sd, strict=False)
+    assert not unexpected and all("lm_head" in k for k in missing)
+    return m
+
+
 def _hf_logits(d, W, tokens):
     torch = pytest.importorskip("torch")
     tr = pytest.importorskip("transformers")
@@ -77,3 +93,54 @@ def test_causality():
     tok2 = tok.copy(); tok2[0, 4] = (tok2[0, 4] + 1) % d.vocab
     b = forward.forward_exact(d, W, tok2[:, :3])
     assert np.array_equal(a, b)
+
+
+def _hf_bf16_at_linear_inputs(d, W, tokens, skip_in=(), extra_out_round=()):
+    """HF OPTForCausalLM in float32 with a forward-pre-hook on EVERY nn.Linear that rounds the
+    Linear's input to bf16 (torch's own RNE conversion): the plain definition of "bf16 rounding
+    exactly at the GEMM A-operands" (reading #20) written with library code. The
+    residual stream, LayerNorm statistics, q/k/v, softmax and partial sums stay float32.
+    Mutations: skip_in = Linear names whose input is NOT rounded; extra_out_round = Linear names
+    whose OUTPUT is also rounded."""
+    torch = pytest.importorskip("torch")
+    m = _hf_model(d, W, torch.float32)
+    rb = lambda t: t.to(torch.bfloat16).to(torch.float32)
+    for name, mod in m.named_modules():
+        if isinstance(mod, torch.nn.Linear):
+            if not any(name.endswith(x) for x in skip_in):
+                mod.register_forward_pre_hook(lambda _m, args: (rb(args[0]),) + tuple(args[1:]))
+            if any(name.endswith(x) for x in extra_out_round):
+                mod.register_forward_hook(lambda _m, _a, out: rb(out))
+    with torch.no_grad():
+        out = m(input_ids=torch.from_numpy(np.asarray(tokens, np.int64)),
+                attention_mask=torch.ones(tokens.shape, dtype=torch.long))
+    return out.logits[:, -1].double().numpy()
+
+
+PIN_BAR = 2e-5
+
+
+def test_bf16_emulation_storage_points_match_hf_hooks():
+    """Pins forward_bf16_emulated's storage points (reading #20) against an independent
+    construction: HF's OPT forward with bf16 rounding hooked onto every Linear input. Only fp32
+    summation order differs, so the two agree far inside PIN_BAR. Each plausible storage-point
+    mistake (q/k/v rounded; attention output, ReLU output or final-LN output left unrounded; no
+    rounding at all) moves the HF construction by well over PIN_BAR, so an oracle with that
+    mistake would fail the first assertion."""
+    d = opt_dims("small")
+    W = layout.full_tensors(d, 6)
+    tok = np.stack([request_tokens(3, 0, i, 8, d.vocab) for i in range(3)])
+    em = forward.forward_bf16_emulated(d, W, tok)
+    hf = _hf_bf16_at_linear_inputs(d, W, tok)
+    err = forward.rel_l2(em, hf)
+    assert err < PIN_BAR, err
+    mutants = {
+        "qkv rounded": dict(extra_out_round=("q_proj", "k_proj", "v_proj")),
+        "o unrounded": dict(skip_in=("out_proj",)),
+        "relu unrounded": dict(skip_in=("fc2",)),
+        "final LN unrounded": dict(skip_in=("lm_head",)),
+    }
+    for what, kw in mutants.items():
+        mut = _hf_bf16_at_linear_inputs(d, W, tok, **kw)
+        assert forward.rel_l2(mut, em) > 5 * PIN_BAR, what
+    assert forward.rel_l2(forward.forward_exact(d, W, tok), em) > 50 * PIN_BAR
