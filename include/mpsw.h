@@ -165,9 +165,18 @@ mpsw_status mpsw_swap_in(mpsw_ctx* ctx, int model_id, uint64_t* ticket);
  * OK no-op if EVICTED/OFFLOADING. */
 mpsw_status mpsw_swap_out(mpsw_ctx* ctx, int model_id, uint64_t* ticket);
 
+/* Offload semantics of the offload decisions the engine makes from now on (explicit and LRU):
+ * 1 = writeback (D2H copy of the range into the arena, chunk-paired with the next load, reading
+ * #5/#6), 0 = clean eviction (no copy; weights are immutable, NEXT-3). Initial
+ * value: mpsw_config.writeback. Entries already dispatched keep theirs; the flag travels with
+ * each offload entry to every rank (shm record in multi-process mode). Leader only (EINVAL). */
+mpsw_status mpsw_set_writeback(mpsw_ctx* ctx, int writeback);
+
 /* Block until every rank acked `ticket` ("completed when every worker finishes").
  * t_submit: engine time of the decision; t_done_per_rank: array of tp ack times (may be
  * NULL). Times are seconds since mpsw_init (steady clock). timeout_s < 0 waits forever.
+ * A completed ticket stays queryable (here and in mpsw_entry_gpu_ms) until 4096 newer swap
+ * entries have completed; older tickets are released (ENOENT), bounding the entry history.
  * Errors: ENOENT unknown ticket, ETIMEDOUT. */
 mpsw_status mpsw_wait(mpsw_ctx* ctx, uint64_t ticket, double timeout_s, double* t_submit,
                       double* t_done_per_rank);
@@ -198,7 +207,9 @@ mpsw_status mpsw_wait_request(mpsw_ctx* ctx, int64_t request_id, double timeout_
 
 /* 64-bit order-independent checksum (C4) of (model, rank)'s bytes:
  * on_device = 1 hashes the resident range with the sm_100a checksum kernel (EINVAL unless
- * RESIDENT); on_device = 0 hashes the pinned host arena on the host. */
+ * RESIDENT); on_device = 0 hashes the pinned host arena on the host. EAGAIN (retry) if a swap
+ * entry was dispatched while the device range was being read: the bytes may have been changing,
+ * so no hash is returned. (mpsw_peek: same rule.) */
 mpsw_status mpsw_checksum(mpsw_ctx* ctx, int model_id, int rank, int on_device, uint64_t* out);
 
 /* Copy `bytes` at `offset` of a RESIDENT model's device range (rank) into host `dst`

@@ -40,12 +40,21 @@ mpsw_status mpsw_bench_gemm(int device, int impl, int M, int N, int K, int reps,
  *          MPSW_TAP_QKV : fp32 [M, 3*h/t] = [q | k | v] of layer n_layers on that rank (q scaled
  *                         by hd^-0.5 after its bias, HF:opt.py:151);
  *          MPSW_TAP_O   : attention output [M, h/t] of layer n_layers (ctx dtype);
- *          MPSW_TAP_R   : ReLU(fc1) output [M, ff/t] of layer n_layers (ctx dtype).
+ *          MPSW_TAP_R   : ReLU(fc1) output [M, ff/t] of layer n_layers (ctx dtype);
+ *          MPSW_TAP_XM  : fp32 residual stream [M, h] of layer n_layers after its attention block
+ *                         (x + all-reduced out_proj + bias);
+ *          MPSW_TAP_F   : LN2 output [M, h] of layer n_layers (fc1's A operand, ctx dtype).
  * Rows are the batch's packed token rows (requests in batch order). At most `bytes` bytes are
  * written; dst is host memory that must stay valid until the batch completes.
  * Single-process ctx with pp = 1 only. Errors: EINVAL (bad argument, mp mode, pp > 1). */
-enum { MPSW_TAP_X = 0, MPSW_TAP_A = 1, MPSW_TAP_QKV = 2, MPSW_TAP_O = 3, MPSW_TAP_R = 4 };
+enum { MPSW_TAP_X = 0, MPSW_TAP_A = 1, MPSW_TAP_QKV = 2, MPSW_TAP_O = 3, MPSW_TAP_R = 4, MPSW_TAP_XM = 5, MPSW_TAP_F = 6 };
 mpsw_status mpsw_test_tap(mpsw_ctx* ctx, int n_layers, int what, int rank, void* dst, uint64_t bytes);
+
+/* Fault injection (runtime robustness tests): global rank `rank`'s worker throws at its next
+ * all-reduce point, as a CUDA failure inside a batch would. The ctx is poisoned: the other ranks
+ * leave their TP barrier (no hang), pending requests fail with ECUDA and mpsw_shutdown returns.
+ * Single-process ctx only. Errors: EINVAL. */
+mpsw_status mpsw_test_inject_fault(mpsw_ctx* ctx, int rank);
 
 #ifdef __cplusplus
 }

@@ -101,6 +101,44 @@ def forward_bf16_emulated(d, W, tokens, taps=None, n_layers=None):
     return _run(d, W, tokens, np.float32, lambda x: round_bf16(x.astype(np.float32)), taps, n_layers)
 
 
+def layer_ops(d, W, i, dt=np.float64, rnd=lambda x: x):
+    """The steps of C5 for decoder layer i (i = d.n_layers: the final LN / lm_head) as separate
+    functions, each computing ONE step from given inputs, in the order and arithmetic of `_run`
+    (composing them in that order reproduces forward_exact / forward_bf16_emulated exactly,
+    tests/test_oracle_forward.py). Used for teacher-forced parity: each GPU stage is checked
+    against this step applied to the GPU's own inputs of that stage.
+      ln1(x) -> a;  qkv(a) -> [q|k|v];  attn(qkv, heads) -> o;  attn_block(x, o) -> xm;
+      ln2(xm) -> f;  fc1(f) -> r;  mlp_block(xm, r) -> x';  lnf(x) -> a_f;  lm_head(a_f) -> logits.
+    Arrays are [..., features]; attn takes [B, L, 3*n*hd] with n local heads."""
+    g = lambda n: W[n].astype(dt)
+    p = f"decoder.layers.{i}."
+    hd = d.hidden // d.heads
+    scale = dt(hd ** -0.5)
+    ops = {}
+    if i < d.n_layers:
+        def qkv(a):
+            q = (a @ g(p + "self_attn.q_proj.weight").T + g(p + "self_attn.q_proj.bias")) * scale
+            k = a @ g(p + "self_attn.k_proj.weight").T + g(p + "self_attn.k_proj.bias")
+            v = a @ g(p + "self_attn.v_proj.weight").T + g(p + "self_attn.v_proj.bias")
+            return np.concatenate([q, k, v], axis=-1)
+
+        def attn(qkv_, heads):
+            n = qkv_.shape[-1] // 3
+            return rnd(_attention(qkv_[..., :n], qkv_[..., n:2 * n], qkv_[..., 2 * n:], heads, dt))
+
+        ops["ln1"] = lambda x: rnd(layer_norm(x, W[p + "self_attn_layer_norm.weight"], W[p + "self_attn_layer_norm.bias"], dt))
+        ops["qkv"] = qkv
+        ops["attn"] = attn
+        ops["attn_block"] = lambda x, o: x + (o @ g(p + "self_attn.out_proj.weight").T + g(p + "self_attn.out_proj.bias"))
+        ops["ln2"] = lambda xm: rnd(layer_norm(xm, W[p + "final_layer_norm.weight"], W[p + "final_layer_norm.bias"], dt))
+        ops["fc1"] = lambda f: rnd(np.maximum(f @ g(p + "fc1.weight").T + g(p + "fc1.bias"), dt(0)))
+        ops["mlp_block"] = lambda xm, r: xm + (r @ g(p + "fc2.weight").T + g(p + "fc2.bias"))
+    else:
+        ops["lnf"] = lambda x: rnd(layer_norm(x, W["decoder.final_layer_norm.weight"], W["decoder.final_layer_norm.bias"], dt))
+        ops["lm_head"] = lambda a: a @ g("decoder.embed_tokens.weight").T
+    return ops
+
+
 def forward_tp_simulated(d, shards, tokens, dt=np.float64):
     """Megatron-sharded forward: shards[r] = dict name -> rank-r shard values.
     Partials of row-parallel GEMMs (and of the vocab-parallel embedding) are summed

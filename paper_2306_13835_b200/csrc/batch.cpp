@@ -36,6 +36,9 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
                             const void* b) {
         const int pb = point & 1;
         const float* peers[kMaxRanks];
+        int fr = r;
+        if (c->fault_rank.load() == r && c->fault_rank.compare_exchange_strong(fr, -1))
+            throw Error(MPSW_ECUDA, "injected fault (mpsw_test_inject_fault) at an all-reduce point");
         if (t > 1) {
             MPSW_CU(cudaEventRecord(R.ev_point[pb], cs));
             group_barrier(c, R.stage);
@@ -100,6 +103,8 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
         if (tap_here && tap.what == MPSW_TAP_O) { tap_copy(R.ws.o, (size_t)M * hl * esz); break; }
         nl += fwd_out_proj(s, L, R.ws, M, R.ws.partial[point & 1], cs);
         allreduce_ln(R.ws.x, L.o_b, nullptr, L.ln2_w, L.ln2_b);
+        if (tap_here && tap.what == MPSW_TAP_XM) { tap_copy(R.ws.x, (size_t)M * s.hidden * 4); break; }
+        if (tap_here && tap.what == MPSW_TAP_F) { tap_copy(R.ws.a, (size_t)M * s.hidden * esz); break; }
         nl += fwd_fc1(s, L, R.ws, M, cs);
         if (tap_here && tap.what == MPSW_TAP_R) { tap_copy(R.ws.r, (size_t)M * s.ffn_local * esz); break; }
         nl += fwd_fc2(s, L, R.ws, M, R.ws.partial[point & 1], cs);

@@ -28,6 +28,36 @@ static int local_index(mpsw_ctx* c, int rank) {
     return c->local_of[rank];
 }
 
+// Frees what a partially constructed ctx holds (mpsw_init error paths, before any thread runs):
+// per-rank streams, events and device allocations, fan-in helpers, the shm control segment.
+static void release_init_resources(mpsw_ctx* c) {
+    for (auto& R : c->ranks) {
+        cudaSetDevice(R->device);
+        for (cudaStream_t s : {R->compute, R->h2d, R->d2h, R->aux, R->h2d_zc})
+            if (s) cudaStreamDestroy(s);
+        if (R->ev_zc) cudaEventDestroy(R->ev_zc);
+        if (R->ev_base) {
+            for (auto& Q : c->ranks)
+                if (Q.get() != R.get() && Q->ev_base == R->ev_base) Q->ev_base = nullptr;
+            cudaEventDestroy(R->ev_base);
+        }
+        if (R->region) cudaFree(R->region);
+        if (R->d_sum) cudaFree(R->d_sum);
+    }
+    for (auto& H : c->helpers) {
+        cudaSetDevice(H->device);
+        if (H->stream) cudaStreamDestroy(H->stream);
+        if (H->staging) cudaFree(H->staging);
+        for (auto ev : H->free_ev)
+            if (ev) cudaEventDestroy(ev);
+    }
+    if (c->ctl) {
+        munmap((void*)c->ctl, sizeof(ShmCtl));
+        if (c->leader) shm_unlink(c->shm_name.c_str());
+    }
+    cudaGetLastError();
+}
+
 extern "C" {
 
 const char* mpsw_last_error(void) { return tls_error().c_str(); }
@@ -73,12 +103,29 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     if (cfg->swap_mode < 0 || cfg->swap_mode > 3) return set_error(MPSW_EINVAL, "bad swap_mode");
     if (cfg->param_budget_bytes_per_gpu == 0) return set_error(MPSW_EINVAL, "param budget is 0");
     if (cfg->gemm_impl < 0 || cfg->gemm_impl > 3) return set_error(MPSW_EINVAL, "bad gemm_impl");
+    if (cfg->n_helpers < 0 || cfg->n_helpers > kMaxHelpers || (cfg->n_helpers && !cfg->helper_device_ids))
+        return set_error(MPSW_EINVAL, "n_helpers must be 0..8 with helper_device_ids");
+    if (mp && cfg->n_helpers) return set_error(MPSW_EINVAL, "fan-in helpers are single-process only");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
         cudaGetLastError();
         return set_error(MPSW_ECUDA, "no CUDA device");
     }
+    // every argument that can be checked without allocating is checked above / here; past this
+    // point an error return frees what was allocated (guard), so a failed init leaks nothing
+    for (int l = 0; l < cfg->n_gpus; ++l)
+        if (cfg->device_ids[l] < 0 || cfg->device_ids[l] >= ndev) return set_error(MPSW_EINVAL, "device id out of range");
+    for (int h = 0; h < cfg->n_helpers; ++h)
+        if (cfg->helper_device_ids[h] < 0 || cfg->helper_device_ids[h] >= ndev)
+            return set_error(MPSW_EINVAL, "helper device id out of range");
     auto c = std::make_unique<mpsw_ctx>();
+    struct Guard {
+        mpsw_ctx* c;
+        bool armed = true;
+        ~Guard() {
+            if (armed) release_init_resources(c);
+        }
+    } guard{c.get()};
     c->cfg = *cfg;
     c->cfg.shm_name = nullptr;
     c->t0 = std::chrono::steady_clock::now();
@@ -89,6 +136,7 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     c->pp = pp;
     c->nr = mp ? cfg->world_size : cfg->n_gpus;
     c->D = cfg->max_inflight_batches > 0 ? cfg->max_inflight_batches : 1;
+    c->writeback_now.store(cfg->writeback != 0);
     c->chunk = cfg->chunk_bytes ? cfg->chunk_bytes : (64ull << 20);
     c->trace = cfg->trace != 0 && c->leader;
     c->timeline_on = cfg->trace != 0;
@@ -103,7 +151,8 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     for (int l = 0; l < cfg->n_gpus; ++l) {
         const int dev = c->device_ids[l];
         if (dev < 0 || dev >= ndev) return set_error(MPSW_EINVAL, "device id out of range");
-        auto R = std::make_unique<Rank>();
+        c->ranks.push_back(std::make_unique<Rank>());
+        Rank* R = c->ranks.back().get();
         R->index = mp ? cfg->world_rank : l;
         R->stage = R->index / cfg->tp;
         R->trank = R->index % cfg->tp;
@@ -139,15 +188,12 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
                 MPSW_CU(cudaEventSynchronize(R->ev_base));
             }
         }
-        c->ranks.push_back(std::move(R));
     }
-    if (cfg->n_helpers < 0 || cfg->n_helpers > kMaxHelpers || (cfg->n_helpers && !cfg->helper_device_ids))
-        return set_error(MPSW_EINVAL, "n_helpers must be 0..8 with helper_device_ids");
-    if (mp && cfg->n_helpers) return set_error(MPSW_EINVAL, "fan-in helpers are single-process only");
     for (int h = 0; h < cfg->n_helpers; ++h) {
         const int dev = cfg->helper_device_ids[h];
         if (dev < 0 || dev >= ndev) return set_error(MPSW_EINVAL, "helper device id out of range");
-        auto H = std::make_unique<Helper>();
+        c->helpers.push_back(std::make_unique<Helper>());
+        Helper* H = c->helpers.back().get();
         H->device = dev;
         MPSW_CU(cudaSetDevice(dev));
         MPSW_CU(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
@@ -167,7 +213,6 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
             if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) MPSW_CU(pe);
             cudaGetLastError();
         }
-        c->helpers.push_back(std::move(H));
     }
     if (!mp) {
         // peer access between distinct devices of the group (TP all-reduce reads peer partials)
@@ -212,6 +257,7 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
             std::this_thread::sleep_for(std::chrono::milliseconds(5));
         }
     }
+    guard.armed = false;
     mpsw_ctx* raw = c.release();
     for (auto& R : raw->ranks) R->th = std::thread(worker_main, raw, R.get());
     raw->engine = std::thread(raw->leader ? engine_main : follower_main, raw);
@@ -597,6 +643,7 @@ mpsw_status mpsw_checksum(mpsw_ctx* c, int model_id, int rank, int on_device, ui
         *out = host_checksum(c->models[model_id]->arena[li].p, S, 0);
         return MPSW_OK;
     }
+    const uint64_t gen0 = c->swap_gen.load();
     const int64_t off = resident_off(c, model_id);
     if (off < 0) return set_error(MPSW_EINVAL, "model not RESIDENT");
     Rank& R = *c->ranks[li];
@@ -607,6 +654,8 @@ mpsw_status mpsw_checksum(mpsw_ctx* c, int model_id, int rank, int on_device, ui
     unsigned long long h = 0;
     MPSW_CU(cudaMemcpyAsync(&h, R.d_sum, 8, cudaMemcpyDeviceToHost, R.aux));
     MPSW_CU(cudaStreamSynchronize(R.aux));
+    // a swap dispatched while the kernel read the range may have overwritten it: retry
+    if (c->swap_gen.load() != gen0) return set_error(MPSW_EAGAIN, "swap activity during the read; retry");
     *out = h;
     return MPSW_OK;
     API_END
@@ -619,12 +668,31 @@ mpsw_status mpsw_peek(mpsw_ctx* c, int model_id, int rank, uint64_t offset, uint
     const int li = local_index(c, rank);
     if (li < 0 || offset + bytes > c->models[model_id]->rank_S[c->ranks[li]->index])
         return set_error(MPSW_EINVAL, "rank or range");
+    const uint64_t gen0 = c->swap_gen.load();
     const int64_t off = resident_off(c, model_id);
     if (off < 0) return set_error(MPSW_EINVAL, "model not RESIDENT");
     Rank& R = *c->ranks[li];
     MPSW_CU(cudaSetDevice(R.device));
     MPSW_CU(cudaMemcpyAsync(dst, R.region + off + offset, bytes, cudaMemcpyDeviceToHost, R.aux));
     MPSW_CU(cudaStreamSynchronize(R.aux));
+    if (c->swap_gen.load() != gen0) return set_error(MPSW_EAGAIN, "swap activity during the read; retry");
+    return MPSW_OK;
+    API_END
+}
+
+mpsw_status mpsw_set_writeback(mpsw_ctx* c, int writeback) {
+    API_BEGIN
+    if (!c) return set_error(MPSW_EINVAL, "NULL ctx");
+    if (need_leader(c) != MPSW_OK) return MPSW_EINVAL;
+    c->writeback_now.store(writeback != 0);
+    return MPSW_OK;
+    API_END
+}
+
+mpsw_status mpsw_test_inject_fault(mpsw_ctx* c, int rank) {
+    API_BEGIN
+    if (!c || c->mp || rank < 0 || rank >= c->nr) return set_error(MPSW_EINVAL, "bad ctx / rank (single-process only)");
+    c->fault_rank.store(rank);
     return MPSW_OK;
     API_END
 }
@@ -633,7 +701,7 @@ mpsw_status mpsw_test_tap(mpsw_ctx* c, int n_layers, int what, int rank, void* d
     API_BEGIN
     if (!c || !dst || !bytes) return set_error(MPSW_EINVAL, "NULL argument");
     if (c->mp || c->pp != 1) return set_error(MPSW_EINVAL, "tap: single-process ctx with pp = 1 only");
-    if (what < MPSW_TAP_X || what > MPSW_TAP_R || n_layers < 0 || rank < 0 || rank >= c->nr)
+    if (what < MPSW_TAP_X || what > MPSW_TAP_F || n_layers < 0 || rank < 0 || rank >= c->nr)
         return set_error(MPSW_EINVAL, "tap: bad what / n_layers / rank");
     std::lock_guard<std::mutex> lk(c->tap_mu);
     c->tap_next = Tap{n_layers, what, rank, dst, bytes};

@@ -58,7 +58,9 @@ bool group_poisoned(mpsw_ctx* c) { return c->poisoned.load() || (c->ctl && c->ct
 // t processes through the shm segment). Bounded so a dead peer cannot hang the process forever.
 void group_barrier(mpsw_ctx* c, int stage) {
     if (!c->mp) {
-        c->stage_barrier[stage].wait();
+        if (!c->stage_barrier[stage].wait([c] { return c->poisoned.load() != 0; }))
+            throw Error(group_poisoned(c) ? MPSW_ECUDA : MPSW_ETIMEDOUT,
+                        group_poisoned(c) ? "peer rank failed (ctx poisoned)" : "group barrier timed out");
         return;
     }
     ShmCtl* s = c->ctl;
@@ -161,6 +163,7 @@ void publish(mpsw_ctx* c, const Entry& e) {
     rec.ring = e.ring;
     rec.B = e.B;
     rec.M = e.M;
+    rec.writeback = e.writeback;
     s->log_tail.store(tail + 1, std::memory_order_release);
 }
 
@@ -207,6 +210,8 @@ void dispatch(mpsw_ctx* c, const std::vector<Decision>& ds, double now) {
                 c->tap_next = Tap{};
             }
         } else {
+            e->writeback = d.kind == E_OFFLOAD ? c->writeback_now.load() : 0;
+            c->swap_gen.fetch_add(1);
             std::lock_guard<std::mutex> lk(c->done_mu);
             c->entries[e->id] = e;
         }
@@ -293,6 +298,18 @@ int rank_done(mpsw_ctx* c, Entry& e, int r) {
     return c->ctl->ack[e.id % kAckCap][r].load(std::memory_order_acquire) == e.id + 1 ? 1 : 0;
 }
 
+// A completed swap entry stays queryable (mpsw_wait / mpsw_entry_gpu_ms) until kKeepTickets
+// newer swaps have completed; then it is dropped (ENOENT), so a long-running server's entry map
+// stays bounded. Called with done_mu held.
+constexpr size_t kKeepTickets = 4096;
+void retire_ticket(mpsw_ctx* c, uint64_t id) {
+    c->done_tickets.push_back(id);
+    while (c->done_tickets.size() > kKeepTickets) {
+        c->entries.erase(c->done_tickets.front());
+        c->done_tickets.pop_front();
+    }
+}
+
 bool poll_inflight(mpsw_ctx* c) {
     bool progressed = false;
     for (size_t i = 0; i < c->inflight.size();) {
@@ -311,7 +328,7 @@ bool poll_inflight(mpsw_ctx* c) {
                                  ",\"rank\":" + std::to_string(r) + "}");
                 step_and_dispatch(c, [&](std::vector<Decision>& ds) { c->sm.ack(e.id, r, now, ds); }, now);
                 if (e.kind == E_LOAD) c->h2d_bytes += c->models[e.model]->rank_S[r];
-                else if (c->cfg.writeback) c->d2h_bytes += c->models[e.model]->rank_S[r];
+                else if (e.writeback) c->d2h_bytes += c->models[e.model]->rank_S[r];
             }
         }
         if (e.n_acked == c->nr) {
@@ -326,6 +343,7 @@ bool poll_inflight(mpsw_ctx* c) {
                 finish_swap_events(c, e);
                 std::lock_guard<std::mutex> lk(c->done_mu);
                 e.complete.store(1, std::memory_order_release);
+                retire_ticket(c, e.id);
             }
             c->done_cv.notify_all();
             finished = true;
@@ -424,8 +442,10 @@ void follower_main(mpsw_ctx* c) {
             e->ring = rec.ring;
             e->B = rec.B;
             e->M = rec.M;
+            e->writeback = rec.writeback;
             e->t_submit = now_s(c->t0);
             if (e->kind != E_BATCH) {
+                c->swap_gen.fetch_add(1);
                 std::lock_guard<std::mutex> lk(c->done_mu);
                 c->entries[e->id] = e;
             }
@@ -458,10 +478,11 @@ void follower_main(mpsw_ctx* c) {
                 } else {
                     (e.kind == E_LOAD ? c->swaps_in : c->swaps_out)++;
                     if (e.kind == E_LOAD) c->h2d_bytes += c->models[e.model]->rank_S[R.index];
-                    else if (c->cfg.writeback) c->d2h_bytes += c->models[e.model]->rank_S[R.index];
+                    else if (e.writeback) c->d2h_bytes += c->models[e.model]->rank_S[R.index];
                     finish_swap_events(c, e);
                     std::lock_guard<std::mutex> lk(c->done_mu);
                     e.complete.store(1, std::memory_order_release);
+                    retire_ticket(c, e.id);
                 }
                 c->done_cv.notify_all();
                 c->inflight.erase(c->inflight.begin() + i);

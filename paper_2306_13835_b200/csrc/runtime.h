@@ -32,20 +32,31 @@ inline void spin_pause(int& spins) {
     else std::this_thread::yield();
 }
 
+// Barrier of the rank threads of one process. `dead()` is polled while spinning (every 4096
+// spins): a peer thread that failed (ctx poisoned) or a wait beyond the bound ends the wait with
+// false instead of hanging the process (the caller throws, the worker poisons the ctx).
 struct SpinBarrier {
     std::atomic<int> count{0};
     std::atomic<int> gen{0};
     int n = 1;
-    void wait() {
-        if (n <= 1) return;
+    template <typename Dead>
+    bool wait(Dead dead, double timeout_s = 600.0) {
+        if (n <= 1) return true;
         const int g = gen.load(std::memory_order_acquire);
         if (count.fetch_add(1, std::memory_order_acq_rel) + 1 == n) {
             count.store(0, std::memory_order_relaxed);
             gen.fetch_add(1, std::memory_order_acq_rel);
-        } else {
-            int spins = 0;
-            while (gen.load(std::memory_order_acquire) == g) spin_pause(spins);
+            return true;
         }
+        int spins = 0;
+        const auto t0 = std::chrono::steady_clock::now();
+        while (gen.load(std::memory_order_acquire) == g) {
+            spin_pause(spins);
+            if ((spins & 4095) == 0 &&
+                (dead() || std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s))
+                return false;
+        }
+        return true;
     }
 };
 
@@ -58,6 +69,7 @@ struct ShmRec {            // one decision published by the leader
     uint64_t id;
     uint64_t off;          // load / offload: byte offset of the model's range
     int32_t kind, model, ring, B, M;
+    int32_t writeback;     // offload: copy the range back to the arena (else clean eviction)
 };
 
 struct ShmCtl {
@@ -101,6 +113,7 @@ struct Entry {
     uint64_t id = 0;
     int kind = 0, model = -1;
     uint64_t off = 0;                            // load / offload: byte offset in the region
+    int writeback = 0;                           // offload: D2H writeback (else clean eviction)
     std::vector<std::shared_ptr<ReqRec>> reqs;   // leader only
     int ring = 0, B = 0, M = 0;
     double t_submit = 0;
@@ -237,12 +250,16 @@ struct mpsw_ctx {
     std::mutex done_mu;
     std::condition_variable done_cv;
     std::unordered_map<uint64_t, mpsw::EntryP> entries;        // swap entries by ticket
+    std::deque<uint64_t> done_tickets;   // completed swap tickets, oldest first (bounded history)
+    std::atomic<int> writeback_now{0};   // writeback of the next offload decisions (mpsw_set_writeback)
+    std::atomic<uint64_t> swap_gen{0};   // swap entries dispatched so far (checksum / peek consistency)
     std::unordered_map<int64_t, std::shared_ptr<mpsw::ReqRec>> reqs;
     std::atomic<int64_t> next_rid{0};
     int ring_next = 0;
     std::mutex api_mu;
     std::mutex tap_mu;
     mpsw::Tap tap_next;        // armed by mpsw_test_tap, taken by the next dispatched batch
+    std::atomic<int> fault_rank{-1};   // mpsw_test_inject_fault: this rank throws at its next all-reduce point
     // follower-local view of residency (mp followers)
     std::vector<int64_t> f_off_of;
     std::vector<int> f_state;

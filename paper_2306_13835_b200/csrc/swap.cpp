@@ -183,7 +183,7 @@ void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
     if (R.last_compute_valid[e.model] && !event_done(R.last_compute[e.model]))
         MPSW_CU(cudaStreamWaitEvent(R.d2h, R.last_compute[e.model], 0));
     MPSW_CU(cudaEventRecord(e.ev_start[r], R.d2h));
-    if (c->cfg.writeback) {
+    if (e.writeback) {
         for (int i = 0; i < n_chunks; ++i) {
             const uint64_t off = (uint64_t)i * c->chunk, n = std::min<uint64_t>(c->chunk, S - off);
             if (zc) {

@@ -16,7 +16,7 @@ STATUS_NAMES = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "EBUSY", -4: "ENOENT", 
 BF16, FP32 = 0, 1
 SWAP_AUTO, SWAP_COPY_ENGINE, SWAP_ZERO_COPY, SWAP_HYBRID = 0, 1, 2, 3
 EVICTED, LOADING, RESIDENT, OFFLOADING = 0, 1, 2, 3
-TAP_X, TAP_A, TAP_QKV, TAP_O, TAP_R = 0, 1, 2, 3, 4
+TAP_X, TAP_A, TAP_QKV, TAP_O, TAP_R, TAP_XM, TAP_F = 0, 1, 2, 3, 4, 5, 6
 NOOP_TICKET = (1 << 64) - 1
 
 
@@ -82,6 +82,8 @@ _SIGS = {
     "mpsw_test_gemm": [C.c_int, C.c_int, C.c_int, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float,
                        C.POINTER(C.c_float)],
     "mpsw_test_tap": [_P, C.c_int, C.c_int, C.c_int, _P, C.c_uint64],
+    "mpsw_set_writeback": [_P, C.c_int],
+    "mpsw_test_inject_fault": [_P, C.c_int],
 }
 
 _lib = None
@@ -283,14 +285,32 @@ class Ctx:
         self._tap_buf = buf
         return buf
 
+    def inject_fault(self, rank):
+        """Test hook (include/mpsw_testing.h): rank throws at its next all-reduce point."""
+        _check(lib().mpsw_test_inject_fault(self.h, rank))
+
+    def set_writeback(self, writeback):
+        _check(lib().mpsw_set_writeback(self.h, int(writeback)))
+
+    @staticmethod
+    def _retry(fn, tries=200):
+        """Re-issue a verification read that raced a swap (EAGAIN, include/mpsw.h)."""
+        import time
+        for _ in range(tries):
+            st = fn()
+            if st != EAGAIN:
+                return _check(st)
+            time.sleep(0.005)
+        return _check(st)
+
     def checksum(self, model_id, rank, on_device=True):
         h = C.c_uint64()
-        _check(lib().mpsw_checksum(self.h, model_id, rank, int(on_device), C.byref(h)))
+        self._retry(lambda: lib().mpsw_checksum(self.h, model_id, rank, int(on_device), C.byref(h)))
         return h.value
 
     def peek(self, model_id, rank, offset, nbytes):
         buf = np.empty(nbytes, np.uint8)
-        _check(lib().mpsw_peek(self.h, model_id, rank, offset, nbytes, buf.ctypes.data))
+        self._retry(lambda: lib().mpsw_peek(self.h, model_id, rank, offset, nbytes, buf.ctypes.data))
         return buf
 
     def residency(self, model_id):

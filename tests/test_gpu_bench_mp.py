@@ -30,3 +30,22 @@ def test_bench_torchrun_ranks(n):
     assert o["n_gpus"] == n and o["config"]["tp"] == n and o["steps"] == 3 and o["warmup"] == 3
     assert o["value"] > 0 and o["e2e"]["value"] > 0 and o["gpu_launches"] > 0
     assert o["scaling"] == "strong" and o["roofline"]["bound"] == "pcie"
+    assert o["writeback"]["paper_window_ms"]["p50"] >= o["writeback"]["swap_in_latency_ms"]["p50"] * 0.5
+
+
+def test_bench_driver_form_self_launches():
+    """The driver's form `python bench.py --gpus 2` (no torchrun around it) re-launches itself
+    under torch.distributed.run with 2 ranks and reports n_gpus = 2 (ranks on cuda:0 here)."""
+    need_gpu()
+    env = dict(os.environ, MPSW_BENCH_DEVICE0="1", MPSW_BENCH_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--model", "mid",
+           "--no-cpu-baseline", "--wb-steps", "2"]
+    p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    o = json.loads(lines[0])
+    assert o["n_gpus"] == 2 and o["config"]["tp"] == 2
+    assert o["writeback"]["steps"] == 2 and o["writeback"]["d2h_bytes"] > 0
+    assert o["swap_in_latency_ms"]["p50"] > 0

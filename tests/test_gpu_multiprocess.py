@@ -13,6 +13,7 @@ import pytest
 from synth import opt_dims
 from oracle import layout, forward
 from tests.gpu_util import need_gpu
+from tests import parity_util as PU
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -43,7 +44,7 @@ def test_process_group(tmp_path, world):
     for o in res[0]["outs"]:
         tok = np.array(o["tokens"], np.int32)[None]
         ref = forward.forward_bf16_emulated(d, Ws[o["model"]], tok)[0]
-        assert forward.rel_l2(np.array(o["logits"], np.float32), ref) < 1e-2
+        PU.assert_logits(np.array(o["logits"], np.float32), ref, tag="mp")
     for r in res:
         assert r["checks"] and all(ok for _, ok in r["checks"]), r
         assert r["gpu_ms_local"] > 0
@@ -80,7 +81,7 @@ def test_process_group_fuzz(tmp_path, world, seed):
         if m not in Ws:
             Ws[m] = layout.full_tensors(dims[m], res[0]["seeds"][m])
         ref = forward.forward_bf16_emulated(dims[m], Ws[m], np.array(o["tokens"], np.int32)[None])[0]
-        assert forward.rel_l2(np.array(o["logits"], np.float32), ref) < 1e-2, (m, res[0]["opts"])
+        PU.assert_logits(np.array(o["logits"], np.float32), ref, tag=f"mp-fuzz m{m}")
     from oracle import scheduler as S
     cfg, evs, decs = S.read_trace(out + ".trace")
     assert cfg.tp == world

@@ -1,13 +1,15 @@
 """GPU parity of the swap path (a2/a3/a8): resident bytes are bit-exact with the oracle's C0
 image (checksum C4 + sampled element reads), writeback leaves host arenas unchanged, random
 swap sequences match oracle/swap.py, every swap mode and chunk size."""
+import json
+import os
 import random
 
 import numpy as np
 import pytest
 
 from synth import opt_dims
-from oracle import layout, checksum, swap as OS
+from oracle import layout, checksum
 from oracle import scheduler as S
 from tests.gpu_util import need_gpu
 
@@ -48,8 +50,13 @@ def test_register_with_caller_shards_and_fp32():
 
 @pytest.mark.parametrize("writeback", [1, 0])
 @pytest.mark.parametrize("mode", [1, 2])
-def test_random_swap_sequences_match_oracle(writeback, mode):
+def test_random_swap_sequences_match_oracle(writeback, mode, tmp_path):
+    """60 random requests / explicit swap-ins / swap-outs over 4 models with room for 2: after
+    every step each RESIDENT range equals its C0 image; at the end the engine's recorded decisions
+    are applied to the oracle's byte-level swap model (oracle/swap.py RegionSwapModel), whose
+    predicted resident and host-arena hashes must equal the device / host checksums."""
     M = need_gpu()
+    from oracle.swap import RegionSwapModel
     d = opt_dims("tiny")
     tp, nm, k = 2, 4, 2
     S_ = layout.shard_bytes(d, tp)
@@ -57,15 +64,12 @@ def test_random_swap_sequences_match_oracle(writeback, mode):
     ref = {m: [checksum.checksum(a) for a in v] for m, v in imgs.items()}
     rnd = random.Random(writeback * 10 + mode)
     with M.Ctx(device_ids=(0,) * tp, budget=k * ((S_ + 4095) // 4096 * 4096), swap_mode=mode, chunk_bytes=4096,
-               writeback=writeback, max_batch=2, max_tokens=4) as ctx:
+               writeback=writeback, max_batch=2, max_tokens=4, trace=1) as ctx:
         ids = [ctx.register_model(d, shards=imgs[m]) for m in range(nm)]
-        sm = OS.SwapModel(imgs, k, 4096, bool(writeback))
-        owner = [None] * k
         for step in range(60):
             m = rnd.randrange(nm)
             if rnd.random() < 0.6:
-                # a request: the engine swaps via LRU; mirror with the oracle engine decisions below
-                rid, out = ctx.request(ids[m], np.array([1, 2, 3], np.int32))
+                rid, out = ctx.request(ids[m], np.array([1, 2, 3], np.int32))   # LRU swap if needed
                 ctx.wait_request(rid, 60)
             elif rnd.random() < 0.5:
                 try:
@@ -86,6 +90,19 @@ def test_random_swap_sequences_match_oracle(writeback, mode):
                 assert ctx.checksum(ids[mm], r, on_device=False) == ref[mm][r]     # (iv) writeback identity
         st = ctx.stats()
         assert st["k_slots"] == k
+        p = str(tmp_path / "trace.ndjson")
+        ctx.trace_dump(p)
+        cfg, _, decs = S.read_trace(p)
+        sm = RegionSwapModel(imgs, cfg.cap, writeback=bool(writeback))
+        sm.apply(decs)
+        pred = sm.expected_resident_hashes()
+        assert pred, "no model resident at the end"
+        for mm, hs in pred.items():
+            assert ctx.residency(ids[mm]) == M.RESIDENT
+            assert [ctx.checksum(ids[mm], r) for r in range(tp)] == hs
+        for mm in range(nm):
+            assert [checksum.checksum(a) for a in sm.host[mm]] == [ctx.checksum(ids[mm], r, on_device=False)
+                                                                 for r in range(tp)]
 
 
 def test_budget_errors():
@@ -132,3 +149,6 @@ def test_full_size_opt13b_tp1_sampled_and_checksum():
             assert (exp is None and got == 0) or int(exp) == int(got)
         host = ctx.model_arena(m, 0)
         assert ctx.checksum(m, 0) == checksum.checksum_parallel(host)
+        # the full-size image's hash from the oracle alone (tests/golden, tools/gen_golden_hashes.py)
+        gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c0_shard_hashes.json")))
+        assert ctx.checksum(m, 0) == int(gold["opt-13b/tp1/r0/seed9/bf16"], 16)

@@ -144,3 +144,24 @@ def test_bf16_emulation_storage_points_match_hf_hooks():
         mut = _hf_bf16_at_linear_inputs(d, W, tok, **kw)
         assert forward.rel_l2(mut, em) > 5 * PIN_BAR, what
     assert forward.rel_l2(forward.forward_exact(d, W, tok), em) > 50 * PIN_BAR
+
+
+@pytest.mark.parametrize("mode", ["exact", "bf16"])
+def test_layer_ops_compose_to_forward(mode):
+    """layer_ops (the per-step functions used for teacher-forced GPU parity) composed in C5's
+    order reproduce forward_exact / forward_bf16_emulated bit for bit."""
+    from oracle.weights import round_bf16
+    d = opt_dims("small")
+    W = layout.full_tensors(d, 9)
+    tok = np.stack([request_tokens(5, 0, i, 6, d.vocab) for i in range(2)])
+    dt, rnd = (np.float64, lambda x: x) if mode == "exact" else (np.float32, lambda x: round_bf16(x.astype(np.float32)))
+    ref = (forward.forward_exact if mode == "exact" else forward.forward_bf16_emulated)(d, W, tok)
+    L = tok.shape[1]
+    h = W["decoder.embed_tokens.weight"].astype(dt)[tok] + W["decoder.embed_positions.weight"].astype(dt)[np.arange(L) + 2][None]
+    for i in range(d.n_layers):
+        op = forward.layer_ops(d, W, i, dt, rnd)
+        xm = op["attn_block"](h, op["attn"](op["qkv"](op["ln1"](h)), d.heads))
+        h = op["mlp_block"](xm, op["fc1"](op["ln2"](xm)))
+    op = forward.layer_ops(d, W, d.n_layers, dt, rnd)
+    y = op["lm_head"](op["lnf"](h[:, L - 1]))
+    assert np.array_equal(y, ref)
