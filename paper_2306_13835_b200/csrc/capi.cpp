@@ -378,6 +378,14 @@ mpsw_status mpsw_register_model(mpsw_ctx* c, const mpsw_opt_dims* dims, int tp, 
         for (auto& R : c->ranks)
             if (shards[R->index] && shard_bytes[R->index] != m->rank_S[R->index])
                 return set_error(MPSW_EINVAL, "shard_bytes != S_r of the layout");
+    {   // host-memory preflight: pinning more than the host has would fail late (or swap-thrash)
+        uint64_t need = 0;
+        for (auto& R : c->ranks) need += m->rank_S[R->index];
+        const uint64_t avail = host_mem_available();
+        if (avail && need > avail)
+            return set_error(MPSW_ENOMEM, "pinned arenas need " + std::to_string(need) + " B of host memory, " +
+                                              std::to_string(avail) + " B available (MemAvailable)");
+    }
     try {
         for (auto& R : c->ranks) {
             Layout L;

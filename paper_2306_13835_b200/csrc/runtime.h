@@ -280,6 +280,7 @@ namespace mpsw {
 
 // store.cpp
 int gpu_numa_node(int dev);
+uint64_t host_mem_available();
 PinnedBuf pin_alloc(uint64_t bytes, int numa_node);
 void pin_free(PinnedBuf& b);
 void parallel_memcpy(uint8_t* dst, const uint8_t* src, uint64_t n);

@@ -24,6 +24,18 @@ int gpu_numa_node(int dev) {
     return node;
 }
 
+// MemAvailable of /proc/meminfo in bytes (0 if unknown): the register_model preflight.
+uint64_t host_mem_available() {
+    std::ifstream f("/proc/meminfo");
+    std::string key;
+    uint64_t kb = 0;
+    while (f >> key >> kb) {
+        if (key == "MemAvailable:") return kb * 1024;
+        f.ignore(256, '\n');
+    }
+    return 0;
+}
+
 // NUMA-affine page-locked arena: anonymous mmap, transparent huge pages, bound to the
 // GPU's NUMA node when the platform reports one, then registered (portable + mapped so the
 // zero-copy kernel can read it through UVA).

@@ -7,7 +7,7 @@ log through the oracle scheduler (decisions must be identical) and checks the lo
 requests against the oracle forward when the model is small enough for the oracle.
 
 usage: python tools/serve_trace.py PRESET [--cv 4] [--seed 0] [--out results.json]
-presets: cfg1 | cfg2 | cfg2-t1 | cfg4-analog | hetero
+presets: cfg1 | cfg2 | cfg2-t1 | cfg4 | cfg4-slice | cfg4-analog | hetero
 """
 import argparse
 import json
@@ -35,6 +35,16 @@ PRESETS = {
     # OPT-1.3B-shaped models at TP1 (one GPU / 196 GB host cannot hold 6 x OPT-30B)
     "cfg4-analog": dict(model="opt-1.3b", n=6, tp=1, k=4, max_batch=32, L=8, kind="gamma",
                         rates=zipf_rates(6, 10.0, 1.0), duration=30.0),
+    # cfg4 at its real shape: 6 x OPT-30B, TP8 (one GPU per rank), 4 resident,
+    # Zipf lambda_i = 10/i, Gamma CV=4, max batch 32, L=8, 30 s. Needs 8 GPUs and
+    # 6 x 60.2 GB = 361 GB of pinned host memory: the preflight reports what is missing.
+    "cfg4": dict(model="opt-30b", n=6, tp=8, k=4, max_batch=32, L=8, kind="gamma",
+                 rates=zipf_rates(6, 10.0, 1.0), duration=30.0, gpus=8),
+    # the largest slice of cfg4 one B200 + 196 GB host holds: cfg4's per-rank shapes (OPT-30B at
+    # TP8, 7.5 GB per rank, 8 virtual ranks on cuda:0 sharing its one PCIe link), 2 models with
+    # the first two Zipf rates (10, 5 req/s), budget 1 model, CV=4, max batch 32, L=8, 20 s
+    "cfg4-slice": dict(model="opt-30b", n=2, tp=8, k=1, max_batch=32, L=8, kind="gamma",
+                       rates=zipf_rates(6, 10.0, 1.0)[:2], duration=20.0, gpus=1),
     # NEXT-4 (§6): models of different sizes in one 30 GB region (first-fit placement):
     # 1 x OPT-13B, 3 x OPT-1.3B, 2 x OPT-125M; Gamma CV=1, 30 s, L=8, max batch 8
     "hetero": dict(models=["opt-13b", "opt-1.3b", "opt-1.3b", "opt-1.3b", "opt-125m", "opt-125m"], tp=1,
@@ -66,10 +76,25 @@ def main():
     else:
         trace = gamma_trace(P["rates"], cv, P["duration"], args.seed, P["L"], min(x.vocab for x in dims))
     budget = P["budget"] if "budget" in P else P["k"] * ((S_r + 4095) // 4096 * 4096)
+    # preflight: GPUs and pinned host memory (all ranks' shards of every model) before pinning
+    gpus = P.get("gpus", 1)
+    host_need = sum(tp * sz for sz in sizes_r)
+    avail = None
+    for l in open("/proc/meminfo"):
+        if l.startswith("MemAvailable:"):
+            avail = int(l.split()[1]) * 1024
+    import torch
+    ngpu = torch.cuda.device_count()
+    if ngpu < gpus or (avail is not None and host_need > 0.95 * avail):
+        print(json.dumps({"preset": args.preset, "runnable": False, "needs": {
+            "gpus": gpus, "gpus_present": ngpu, "pinned_host_bytes": host_need, "host_bytes_available": avail,
+            "device_param_bytes_per_gpu": budget, "models": names, "tp": tp}}))
+        sys.exit(2)
+    device_ids = tuple(range(tp)) if gpus >= tp else (0,) * tp
     res = {"preset": args.preset, "prefetch": args.prefetch, "models": names, "tp": tp, "k": P.get("k"), "budget": budget, "cv": cv,
            "seed": args.seed, "requests": len(trace), "shard_bytes": sizes_r}
     t_setup = time.perf_counter()
-    with M.Ctx(device_ids=(0,) * tp, budget=budget, max_batch=P["max_batch"], max_tokens=P["L"], trace=1,
+    with M.Ctx(device_ids=device_ids, budget=budget, max_batch=P["max_batch"], max_tokens=P["L"], trace=1,
                writeback=0, max_dims=d, prefetch=args.prefetch) as ctx:
         ids = [ctx.register_model(x) for x in dims]
         for m in ids:
@@ -132,18 +157,27 @@ def main():
     rdecs, _ = S.replay(rcfg, evs)
     res["replay_identical"] = rdecs == decs
     # logits parity on sampled requests (oracle C5, bf16-emulating) where the oracle is fast enough
+    # (OPT-125M requests by default; --check-logits N samples N requests of any model, the large
+    # ones through the oracle's layer-by-layer C0 weights)
     small = [(rid, r, out) for rid, r, out in outs if names[r.model] == "opt-125m"]
     n_check = args.check_logits if args.check_logits >= 0 else (len(small) if args.preset == "cfg1" else min(8, len(small)))
-    if n_check:
-        errs = []
+    pool = small if args.check_logits < 0 or small else [(rid, r, out) for rid, r, out in outs if not r.warmup]
+    if n_check and pool:
+        errs, errs_ex, maxabs = [], [], []
         Ws = {}
-        for rid, r, out in small[:: max(1, len(small) // n_check)][:n_check]:
+        for rid, r, out in pool[:: max(1, len(pool) // n_check)][:n_check]:
             if r.model not in Ws:
-                Ws[r.model] = layout.full_tensors(dims[r.model], 7000 + r.model)
+                big = layout.shard_bytes(dims[r.model], 1) > 2**31
+                Ws[r.model] = (layout.LazyFull if big else layout.full_tensors)(dims[r.model], 7000 + r.model)
             ref = forward.forward_bf16_emulated(dims[r.model], Ws[r.model], r.tokens[None])[0]
+            ex = forward.forward_exact(dims[r.model], Ws[r.model], r.tokens[None])[0]
             errs.append(forward.rel_l2(out, ref))
+            errs_ex.append(forward.rel_l2(out, ex))
+            maxabs.append(float(np.abs(out - ex).max() / np.abs(ex).max()))
         res["logits_checked"] = len(errs)
         res["logits_max_rel_l2"] = max(errs)
+        res["logits_max_rel_l2_vs_exact"] = max(errs_ex)
+        res["logits_max_elementwise_vs_exact"] = max(maxabs)
     print(json.dumps(res), flush=True)
     if args.out:
         with open(args.out, "a") as f:
