@@ -86,7 +86,11 @@ typedef struct {
                                      its GPU runs every decoder layer in ONE persistent tcgen05/TMA
                                      kernel (else as 2). 0, 2 and 3 give bitwise identical logits. */
     int pp;                       /* pipeline stages (0/1 = none); ranks = tp * pp, global rank  */
-                                  /* g = stage * tp + tp_rank; single-process only; needs D = 1  */
+                                  /* g = stage * tp + tp_rank; single-process only. Entries are */
+                                  /* pipelined stage to stage (NEXT-1): the engine feeds */
+                                  /* stage 0; each worker forwards an entry to the next stage   */
+                                  /* right after issuing it (loads without waiting for the copy)*/
+                                  /* and batches overlap across stages for D > 1                 */
     const int* helper_device_ids; /* NVLink fan-in (NEXT-2; single process): GPUs whose PCIe    */
     int n_helpers;                /* links also pull chunks of every swap-in and forward them   */
                                   /* to the owner over NVLink; 0 = off (copy-engine mode only)  */
@@ -96,6 +100,8 @@ typedef struct {
                                   /* of the first registered model (later ones must not exceed)  */
     int prefetch;                 /* 1 = prefetch predicted models into free space while no swap  */
                                   /* is in flight (NEXT-3, reading #29); never evicts  */
+    int pp_broadcast;             /* pp > 1 ablation: 1 = the engine hands every entry to every  */
+                                  /* worker at once (the design P:96 rules out); needs D = 1     */
 } mpsw_config;
 
 typedef struct {

@@ -52,10 +52,21 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
     if (first) {
         nl += fwd_embed(s, Wt, R.ws, M, R.ws.partial[point & 1], cs);
         allreduce_ln(nullptr, nullptr, Wt.embed_pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b);
+    } else if (!c->cfg.pp_broadcast) {
+        // PP hop ("PP communication occurs through FIFO pipes"): this entry came from the
+        // same TP rank of the previous stage after it issued the batch, so its hop event for this
+        // ring slot is already recorded: wait on it and read that rank's residual stream in place
+        // (peer memory over NVLink) into LN1 of my first layer. Slots are reused only after the
+        // batch completed everywhere, so batches of different slots overlap across stages (D > 1).
+        Rank& P = *c->ranks[c->local_of[r - t]];
+        MPSW_CU(cudaStreamWaitEvent(cs, P.ev_hop[e.ring], 0));
+        const float* self[1] = {P.hop[e.ring]};
+        nl += fwd_reduce_ln(s, M, self, 1, nullptr, nullptr, nullptr, pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b,
+                            R.ws.x, R.ws.a, cs);
+        ++point;
     } else {
-        // PP hop ("PP communication occurs through FIFO pipes"): take the residual stream
-        // of the same TP rank of the previous stage (peer copy over NVLink), then LN1 of my
-        // first layer. D = 1 for pp > 1, so batches never overlap on a stage boundary.
+        // broadcast ablation (P:96's ruled-out design, D = 1): the entry reached every stage at
+        // once, so wait on the host until the previous stage has issued this batch
         Rank& P = *c->ranks[c->local_of[r - t]];
         int spins = 0;
         while (P.stage_out.load(std::memory_order_acquire) < e.id + 1) {
@@ -124,6 +135,10 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
         float* logits_host = (float*)(ring) + (size_t)R.trank * s.vocab_local;
         MPSW_CU(cudaMemcpy2DAsync(logits_host, (size_t)s.vocab * 4, R.ws.logits, (size_t)s.vocab_local * 4,
                                   (size_t)s.vocab_local * 4, B, cudaMemcpyDeviceToHost, cs));
+    } else if (!last && !c->cfg.pp_broadcast) {
+        // residual stream out through hop slot e.ring (read in place by the next stage)
+        MPSW_CU(cudaMemcpyAsync(R.hop[e.ring], R.ws.x, (size_t)M * s.hidden * 4, cudaMemcpyDeviceToDevice, cs));
+        MPSW_CU(cudaEventRecord(R.ev_hop[e.ring], cs));
     } else if (!last) {
         MPSW_CU(cudaEventRecord(R.ev_stage, cs));
         R.stage_out.store(e.id + 1, std::memory_order_release);

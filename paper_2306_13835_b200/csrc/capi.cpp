@@ -94,8 +94,8 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     } else if (cfg->tp < 1 || cfg->tp * pp != cfg->n_gpus) {
         return set_error(MPSW_EINVAL, "tp * pp must equal n_gpus (one TP x PP group per ctx)");
     }
-    if (pp > 1 && cfg->max_inflight_batches > 1)
-        return set_error(MPSW_EINVAL, "pp > 1 requires max_inflight_batches = 1");
+    if (pp > 1 && cfg->pp_broadcast && cfg->max_inflight_batches > 1)
+        return set_error(MPSW_EINVAL, "pp_broadcast (ablation) requires max_inflight_batches = 1");
     if (cfg->max_batch < 1 || cfg->max_batch > 256) return set_error(MPSW_EINVAL, "max_batch must be 1..256");
     if (cfg->max_tokens < 1 || cfg->max_tokens > 128) return set_error(MPSW_EINVAL, "max_tokens must be 1..128");
     if (cfg->dtype != MPSW_BF16 && cfg->dtype != MPSW_FP32) return set_error(MPSW_EINVAL, "bad dtype");
@@ -306,6 +306,8 @@ mpsw_status mpsw_shutdown(mpsw_ctx* c) {
         for (auto ev : R->ev_point)
             if (ev) cudaEventDestroy(ev);
         if (R->ev_stage) cudaEventDestroy(R->ev_stage);
+        for (auto ev : R->ev_hop) cudaEventDestroy(ev);
+        if (R->hop_base) cudaFree(R->hop_base);
         if (R->ev_base) {
             for (auto& Q : c->ranks)
                 if (Q.get() != R.get() && Q->ev_base == R->ev_base) Q->ev_base = nullptr;

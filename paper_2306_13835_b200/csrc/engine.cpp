@@ -102,16 +102,28 @@ void worker_main(mpsw_ctx* c, Rank* R) {
             poison(c, err.what());
         }
         e->issued[R->index].store(1, std::memory_order_release);
+        // pipelined entries (NEXT-1): hand the entry to the same TP rank of the next stage
+        // as soon as it is issued here — a load without waiting for its copy, a batch once its
+        // kernels (and the hop event of its residual stream) are on this rank's stream
+        if (c->pp > 1 && !c->cfg.pp_broadcast && R->stage + 1 < c->pp) {
+            const int nxt = c->local_of[R->index + c->tp];
+            if (nxt >= 0) push_to_rank(*c->ranks[nxt], e);
+        }
         c->cmd_cv.notify_all();
     }
 }
 
+void push_to_rank(Rank& R, const EntryP& e) {
+    std::lock_guard<std::mutex> lk(R.mu);
+    R.fifo.push_back(e);
+    R.cv.notify_one();
+}
+
+// The engine hands every entry, in its one global order, to every worker — or, with pipeline
+// stages (default), to the stage-0 workers only: later stages receive it from their predecessor.
 void push_to_workers(mpsw_ctx* c, const EntryP& e) {
-    for (auto& R : c->ranks) {
-        std::lock_guard<std::mutex> lk(R->mu);
-        R->fifo.push_back(e);
-        R->cv.notify_one();
-    }
+    for (auto& R : c->ranks)
+        if (c->pp == 1 || c->cfg.pp_broadcast || R->stage == 0) push_to_rank(*R, e);
 }
 
 // ----------------------------------------------------------------------------- engine (leader)
@@ -554,6 +566,16 @@ void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& dmax) {
         workspace_carve(R.ws, f, c->max_rows, c->cfg.max_batch, R.ws_base);
         for (auto& ev : R.ev_point) MPSW_CU(cudaEventCreateWithFlags(&ev, ev_flags));
         MPSW_CU(cudaEventCreateWithFlags(&R.ev_stage, cudaEventDisableTiming));
+        if (c->pp > 1 && R.stage + 1 < c->pp) {      // hop ring: one [max_rows, h] fp32 slot per ring entry
+            const size_t slot = ((size_t)c->max_rows * dmax.hidden * 4 + 255) & ~size_t(255);
+            MPSW_CU(cudaMalloc(&R.hop_base, slot * (size_t)(c->D + 1)));
+            for (int j = 0; j <= c->D; ++j) {
+                R.hop.push_back((float*)((uint8_t*)R.hop_base + slot * j));
+                cudaEvent_t ev;
+                MPSW_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                R.ev_hop.push_back(ev);
+            }
+        }
         for (int pb = 0; pb < 2; ++pb) {
             c->peer_partial[R.index][pb] = R.ws.partial[pb];
             c->peer_ev[R.index][pb] = R.ev_point[pb];

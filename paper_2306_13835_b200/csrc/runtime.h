@@ -159,9 +159,16 @@ struct Rank {
     int index = 0, local = 0, device = 0, numa = -1;   // index = global rank = stage * tp + trank
     int stage = 0, trank = 0;              // pipeline stage, TP rank inside the stage
     FwdShape fs_max{};                     // workspace shape: elementwise max over the ctx's models
-    cudaEvent_t ev_stage = nullptr;        // PP: residual stream of this stage is ready
     cudaEvent_t ev_base = nullptr;         // timeline origin of this rank's device (trace = 1)
-    std::atomic<uint64_t> stage_out{0};    // PP: id+1 of the last batch whose ev_stage is recorded
+    // PP (stage < pp - 1): the residual stream of batch e leaves through hop slot e.ring (the
+    // staging-ring index: reused only after batch e completed on every rank, so no WAR fence) and
+    // ev_hop[slot] marks it written; the next stage reads it in place (peer memory)
+    std::vector<float*> hop;
+    std::vector<cudaEvent_t> ev_hop;
+    float* hop_base = nullptr;
+    // broadcast ablation (cfg.pp_broadcast): host handshake on the batch id instead of forwarding
+    cudaEvent_t ev_stage = nullptr;
+    std::atomic<uint64_t> stage_out{0};
     cudaStream_t compute = nullptr, h2d = nullptr, d2h = nullptr, aux = nullptr;
     cudaStream_t h2d_zc = nullptr;         // hybrid swap: the zero-copy share of a swap-in
     cudaEvent_t ev_zc = nullptr;
@@ -292,6 +299,7 @@ void poison(mpsw_ctx* c, const std::string& msg);
 bool group_poisoned(mpsw_ctx* c);
 void group_barrier(mpsw_ctx* c, int stage = 0);
 void worker_main(mpsw_ctx* c, Rank* R);
+void push_to_rank(Rank& R, const EntryP& e);
 void engine_main(mpsw_ctx* c);
 void follower_main(mpsw_ctx* c);
 void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& dmax);

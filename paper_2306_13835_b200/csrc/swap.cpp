@@ -180,8 +180,8 @@ void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
     MPSW_CU(cudaEventCreate(&e.ev_done[r]));
     // eviction never races an in-flight request: the D2H stream waits for the last forward
     // that read the victim (the engine also only evicts models with no in-flight batch)
-    if (R.last_compute_valid[e.model] && !event_done(R.last_compute[e.model]))
-        MPSW_CU(cudaStreamWaitEvent(R.d2h, R.last_compute[e.model], 0));
+    const bool fwd_pending = R.last_compute_valid[e.model] && !event_done(R.last_compute[e.model]);
+    if (fwd_pending) MPSW_CU(cudaStreamWaitEvent(R.d2h, R.last_compute[e.model], 0));
     MPSW_CU(cudaEventRecord(e.ev_start[r], R.d2h));
     if (e.writeback) {
         for (int i = 0; i < n_chunks; ++i) {
@@ -194,9 +194,12 @@ void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
             }
             add_gate(R, lo + off, lo + off + n, true, R.d2h);   // these bytes may now be overwritten
         }
-    } else {
+    } else if (fwd_pending) {
         add_gate(R, lo, lo + S, false, R.d2h);                  // after the victim's last forward
     }
+    // (clean eviction of a victim whose forwards have all completed needs no gate: the load that
+    // reuses its bytes would otherwise pay a cross-stream event wait, ~40 us per swap at small
+    // sizes, for an event that orders nothing — DESIGN.md §8 cfg5)
     MPSW_CU(cudaEventRecord(e.ev_done[r], R.d2h));
 }
 
