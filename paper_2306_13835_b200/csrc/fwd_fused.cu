@@ -678,6 +678,7 @@ int fwd_layers_fused(const FwdShape& s, const TensorPtrs& W, FwdWorkspace& ws, i
         if (dbg) fprintf(stderr, "[mpsw] fused layers kernel not used: %s\n", why);
         return 0;
     };
+    if (tc_pair()) return no("CTA-pair GEMM mode (the fused kernel reproduces the single-CTA split only)");
     if (s.dtype != MPSW_BF16 || s.gemm_impl != 3) return no("dtype / gemm_impl (opt-in: 3)");
     if (s.tp != 1) return no("tp > 1");
     if (M < 1 || M > kMaxFusedRows) return no("M out of range");

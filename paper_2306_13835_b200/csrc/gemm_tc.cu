@@ -38,16 +38,16 @@ struct TcSeg {
 struct TcArgs {
     TcSeg seg[3];
     int nseg, tiles, kb, K, M, Mp, stages, G;
-    uint64_t units;              // tiles * kb
+    uint64_t units;              // work units: tiles * kb (single CTA) or pairs * kb (CTA pairs)
     int epi;                     // 0: fp32 out (bias, scale); 1: bf16 out relu(acc + bias)
     void* out;
     int ldo;
     const int32_t* row_of_m;     // optional: output row for token m (-1 = drop); lm_head
-    float* partial;              // [G][2][Mp][128]: a CTA's first / last partial run (row fastest)
+    float* partial;              // [CTAs][2][Mp][128]: a CTA's first / last partial run (row fastest)
     int* counters;               // [tiles], self-resetting
     int ext_fixup;               // 1: split tiles are reduced by tc_fixup_kernel, not in-kernel
     int nacc;                    // TMEM accumulator buffers (2 = epilogue overlaps the next run)
-    unsigned long long* trace;   // dev: [G][8] %globaltimer stamps per CTA phase, or null
+    unsigned long long* trace;   // dev: [CTAs][8] %globaltimer stamps per CTA phase, or null
     int l2_prefetch;             // weight units per CTA prefetched into L2 before griddepcontrol.wait
 };
 
@@ -59,8 +59,9 @@ __device__ __forceinline__ void stamp(const TcArgs& g, int c, int i) {
     }
 }
 
-// Stream-K work split: CTA c owns units [ubeg(c), ubeg(c+1)) of the linearised (tile, k-block)
-// space. Depends only on (tiles, kb, G) — never on M — so it is batch-invariant.
+// Stream-K work split: worker w (a CTA, or a CTA pair) owns units [ubeg(w), ubeg(w+1)) of the
+// linearised (tile or tile pair, k-block) space. Depends only on (units, G) — never on M — so it
+// is batch-invariant.
 __device__ __forceinline__ uint64_t ubeg(const TcArgs& g, int c) { return (uint64_t)c * g.units / (uint64_t)g.G; }
 
 __device__ __forceinline__ int cta_of(const TcArgs& g, uint64_t u) {
@@ -70,11 +71,20 @@ __device__ __forceinline__ int cta_of(const TcArgs& g, uint64_t u) {
     return c;
 }
 
-// Partial run of CTA cc on a split tile: slot 0 if the tile is cc's first tile, else slot 1
-// (a CTA touches at most two split tiles: where its range starts and where it ends).
-__device__ __forceinline__ const float* partial_run(const TcArgs& g, int cc, int c_first, int tile, int row) {
-    const int wh = (cc == c_first && (int)(ubeg(g, c_first) / g.kb) != tile) ? 1 : 0;
-    return g.partial + ((size_t)cc * 2 + wh) * (size_t)g.Mp * kBN + row;
+// Tiles per work unit: 1 (single CTA, MMA M = 128) or 2 (CTA pair, MMA M = 256: CTA rank r of
+// the pair owns tile 2p + r of pair p).
+template <bool kPair> struct TileMap {
+    static constexpr int kT = kPair ? 2 : 1;
+    __device__ static int tile(uint64_t u, int kb, int r) { return (int)(u / kb) * kT + r; }
+    __device__ static int cta(int w, int r) { return w * kT + r; }
+};
+
+// Partial run of worker cc on a split tile: slot 0 if the tile is cc's first tile (pair), else 1
+// (a worker touches at most two split tiles / pairs: where its range starts and where it ends).
+template <bool kPair>
+__device__ __forceinline__ const float* partial_run(const TcArgs& g, int cc, int c_first, int unit_tile, int r, int row) {
+    const int wh = (cc == c_first && (int)(ubeg(g, c_first) / g.kb) != unit_tile) ? 1 : 0;
+    return g.partial + ((size_t)TileMap<kPair>::cta(cc, r) * 2 + wh) * (size_t)g.Mp * kBN + row;
 }
 
 __device__ __forceinline__ void epi_store(const TcArgs& g, const TcSeg& seg, int n, int m, float x, float bias_n) {
@@ -89,13 +99,64 @@ __device__ __forceinline__ int seg_of(const TcArgs& g, int tile) {
     return si;
 }
 
+// ---- CTA-pair (cta_group::2) primitives
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same smem variable in the pair's leader (CTA rank 0)
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(a) : "r"(smem_u32(p)));
+    return a;
+}
+// TMA load into this CTA's smem whose completion bytes count on the LEADER's mbarrier
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_leader, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(bar_leader), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// MMA completion arrives on the mbarrier at this offset in BOTH CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     smem_u32(bar)),
+                 "h"((uint16_t)3)
+                 : "memory");
+}
+
+// One kernel, two work shapes (kPair):
+//  * single CTA: unit = (tile, k-block); the CTA's tcgen05.mma.cta_group::1 M = 128 reads its W
+//    tile [128 x 64] and the whole token tile [Mp x 64] from its own smem;
+//  * CTA pair (cluster of 2, cta_group::2): unit = (tile pair, k-block); each CTA loads its own W
+//    tile and HALF of the token tile (Mp/2 rows), the leader issues one M = 256 MMA that reads
+//    A from both CTAs (rows of each tile) and B split by N across them, D = each CTA's 128 rows
+//    x Mp in its own TMEM. Per SM and unit: 16 KB + Mp x 64 B through smem instead of
+//    16 KB + Mp x 128 B — half the token-tile re-reads, and deeper rings at large M.
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant__ CUtensorMap map_w1,
                const __grid_constant__ CUtensorMap map_w2, const __grid_constant__ CUtensorMap map_x, TcArgs g) {
+    using TM = TileMap<kPair>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024-B alignment for the 128B swizzle atoms
+    // 1024-B alignment for the 128B swizzle atoms (same offset in both CTAs of a pair)
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    const uint32_t tile_b_bytes = (uint32_t)g.Mp * kBK * 2;
+    const int xrows = kPair ? g.Mp / 2 : g.Mp;     // token rows of the B tile this CTA holds
+    const uint32_t tile_b_bytes = (uint32_t)xrows * kBK * 2;
     const int kStages = g.stages;
     uint8_t* sa = smem;
     uint8_t* sb = smem + kStages * kTileABytes;
@@ -107,11 +168,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
     __shared__ int s_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = blockIdx.x;
+    const int r = kPair ? (int)cluster_rank() : 0;           // rank in the pair
+    const bool leader = r == 0;
+    const int c = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // worker (CTA or pair)
+    const int cta = TM::cta(c, r);
     const uint64_t u0 = ubeg(g, c), u1 = ubeg(g, c + 1);
     pdl_trigger();                                 // let the next kernel's CTAs get scheduled
-    if (u0 >= u1) return;                          // uniform for the whole CTA
-    if (threadIdx.x == 0) stamp(g, c, 0);          // phase 0: CTA start
+    if (u0 >= u1) return;                          // uniform for the whole CTA (and pair)
+    if (threadIdx.x == 0) stamp(g, cta, 0);        // phase 0: CTA start
     uint32_t nbuf = 32;                            // TMEM columns per accumulator: pow2 >= max(32, Mp)
     while ((int)nbuf < g.Mp) nbuf <<= 1;
     // double-buffered accumulator while every resident CTA's buffers fit in the 512 TMEM columns
@@ -129,80 +193,85 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tmem_full[b], 1);
-            mbar_init(&tmem_empty[b], 4);          // one arrive per epilogue warp
+            mbar_init(&tmem_empty[b], kPair ? 8 : 4);   // one arrive per epilogue warp (of both CTAs)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(ncols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (kPair) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(ncols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(ncols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    if (kPair) cluster_sync_all();                 // the peer's barriers exist before any remote arrive
+    else __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem_base = *tmem_slot;
+    // leader's stage barriers: TMA bytes of both CTAs land there (pair mode)
+    const uint32_t stage_bytes = kPair ? 2 * (kTileABytes + tile_b_bytes) : kTileABytes + tile_b_bytes;
 
     if (warp == 0) {
         if (lane == 0) {                           // ---- TMA producer: continuous across tiles
-            // Weights do not depend on the previous kernel: the first kStages weight tiles are in
-            // flight before griddepcontrol.wait, overlapping the previous kernel's tail (PDL).
-            stamp(g, c, 1);                        // phase 1: prologue done (barriers, TMEM)
-            const int pre = (int)(u1 - u0 < (uint64_t)kStages ? u1 - u0 : (uint64_t)kStages);
-            for (int i = 0; i < pre; ++i) {
-                const uint64_t u = u0 + i;
-                const int tile = (int)(u / g.kb), kbi = (int)(u % g.kb);
+            auto load_w = [&](int s, uint64_t u, int kbi) {
+                const int tile = TM::tile(u, g.kb, r);
                 const int si = seg_of(g, tile);
                 const CUtensorMap* mw = si == 0 ? &map_w0 : (si == 1 ? &map_w1 : &map_w2);
-                mbar_expect_tx(&full[i], kTileABytes + tile_b_bytes);
-                tma_load_2d(sa + i * kTileABytes, mw, &full[i], kbi * kBK, (tile - g.seg[si].tile0) * kBN);
+                if (kPair)                         // rows past the last tile (odd tile count) are zero-filled
+                    tma_load_2d_pair(sa + s * kTileABytes, mw, leader_addr(&full[s]), kbi * kBK, (tile - g.seg[si].tile0) * kBN);
+                else
+                    tma_load_2d(sa + s * kTileABytes, mw, &full[s], kbi * kBK, (tile - g.seg[si].tile0) * kBN);
+            };
+            auto load_x = [&](int s, int kbi) {
+                if (kPair) tma_load_2d_pair(sb + s * tile_b_bytes, &map_x, leader_addr(&full[s]), kbi * kBK, r * xrows);
+                else tma_load_2d(sb + s * tile_b_bytes, &map_x, &full[s], kbi * kBK, 0);
+            };
+            // Weights do not depend on the previous kernel: the first kStages weight tiles are in
+            // flight before griddepcontrol.wait, overlapping the previous kernel's tail (PDL).
+            stamp(g, cta, 1);                      // phase 1: prologue done (barriers, TMEM)
+            const int pre = (int)(u1 - u0 < (uint64_t)kStages ? u1 - u0 : (uint64_t)kStages);
+            for (int i = 0; i < pre; ++i) {
+                if (leader) mbar_expect_tx(&full[i], stage_bytes);
+                load_w(i, u0 + i, (int)((u0 + i) % g.kb));
             }
             // ...and the next l2_prefetch units go to L2, so the weight stream keeps HBM busy
             // across the kernel boundary (the smem ring alone holds only `stages` units)
             {
                 const uint64_t pe = u0 + pre + (uint64_t)g.l2_prefetch < u1 ? u0 + pre + g.l2_prefetch : u1;
                 for (uint64_t u = u0 + pre; u < pe; ++u) {
-                    const int tile = (int)(u / g.kb), kbi = (int)(u % g.kb);
+                    const int tile = TM::tile(u, g.kb, r), kbi = (int)(u % g.kb);
                     const int si = seg_of(g, tile);
                     const CUtensorMap* mw = si == 0 ? &map_w0 : (si == 1 ? &map_w1 : &map_w2);
                     tma_prefetch_l2(mw, kbi * kBK, (tile - g.seg[si].tile0) * kBN);
                 }
             }
             pdl_wait();
-            stamp(g, c, 2);                        // phase 2: previous kernel complete
-            for (int i = 0; i < pre; ++i)
-                tma_load_2d(sb + i * tile_b_bytes, &map_x, &full[i], (int)((u0 + i) % g.kb) * kBK, 0);
-            // (tile, k-block, segment, ring slot, parity) advance incrementally: no 64-bit
-            // divisions per unit (the single producer thread's issue rate bounds the stream)
+            stamp(g, cta, 2);                      // phase 2: previous kernel complete
+            for (int i = 0; i < pre; ++i) load_x(i, (int)((u0 + i) % g.kb));
             uint64_t u = u0 + pre;
-            if (u < u1) {
-                int tile = (int)(u / g.kb), kbi = (int)(u % g.kb), si = seg_of(g, tile);
-                int s = pre % kStages;
-                uint32_t ph = (uint32_t)(pre / kStages) & 1u;
-                const CUtensorMap* mw = si == 0 ? &map_w0 : (si == 1 ? &map_w1 : &map_w2);
-                for (; u < u1; ++u) {
-                    mbar_wait(&empty[s], ph ^ 1u);
-                    mbar_expect_tx(&full[s], kTileABytes + tile_b_bytes);
-                    tma_load_2d(sa + s * kTileABytes, mw, &full[s], kbi * kBK, (tile - g.seg[si].tile0) * kBN);
-                    tma_load_2d(sb + s * tile_b_bytes, &map_x, &full[s], kbi * kBK, 0);
-                    if (++s == kStages) { s = 0; ph ^= 1u; }
-                    if (++kbi == g.kb) {
-                        kbi = 0;
-                        ++tile;
-                        if (si + 1 < g.nseg && tile >= g.seg[si + 1].tile0) {
-                            ++si;
-                            mw = si == 1 ? &map_w1 : &map_w2;
-                        }
-                    }
-                }
+            int s = pre % kStages;
+            uint32_t ph = (uint32_t)(pre / kStages) & 1u;
+            int kbi = (int)(u % g.kb);
+            for (; u < u1; ++u) {
+                mbar_wait(&empty[s], ph ^ 1u);
+                if (leader) mbar_expect_tx(&full[s], stage_bytes);
+                load_w(s, u, kbi);
+                load_x(s, kbi);
+                if (++s == kStages) { s = 0; ph ^= 1u; }
+                if (++kbi == g.kb) kbi = 0;
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {                           // ---- MMA issuer
+        if (lane == 0 && leader) {                 // ---- MMA issuer (the pair's leader)
             // kind::f16: D fp32 (c_format 1), A = B = bf16 (format 1), both K-major,
-            // N = Mp (n_dim = N >> 3), M = 128 (m_dim = M >> 4)
+            // N = Mp (n_dim = N >> 3), M = 128 / 256 (m_dim = M >> 4)
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(g.Mp >> 3) << 17) |
-                                   ((uint32_t)(kBN >> 4) << 24);
+                                   ((uint32_t)((kBN * TM::kT) >> 4) << 24);
             int run = 0;
             uint32_t tmem_d = tmem_base;
             int s = 0, kbi = (int)(u0 % g.kb);
@@ -219,48 +288,56 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                 }
                 mbar_wait(&full[s], ph);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if (u == u0) stamp(g, c, 3);       // phase 3: first stage landed
+                if (u == u0) stamp(g, cta, 3);     // phase 3: first stage landed
                 const uint32_t a0 = smem_u32(sa + s * kTileABytes), b0 = smem_u32(sb + s * tile_b_bytes);
 #pragma unroll
-                for (int kk = 0; kk < kBK / 16; ++kk)
-                    umma_bf16(tmem_d, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, (!first || kk) ? 1u : 0u);
-                umma_commit(&empty[s]);            // smem stage free once these MMAs have read it
-                if (last) {
-                    umma_commit(&tmem_full[nacc == 2 ? (run & 1) : 0]);   // accumulator of this run complete
+                for (int kk = 0; kk < kBK / 16; ++kk) {
+                    if (kPair) umma_bf16_pair(tmem_d, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, (!first || kk) ? 1u : 0u);
+                    else umma_bf16(tmem_d, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, (!first || kk) ? 1u : 0u);
+                }
+                if (kPair) umma_commit_pair(&empty[s]);   // both CTAs' stage s free once read
+                else umma_commit(&empty[s]);
+                if (last) {                        // accumulator of this run complete (both CTAs)
+                    if (kPair) umma_commit_pair(&tmem_full[nacc == 2 ? (run & 1) : 0]);
+                    else umma_commit(&tmem_full[nacc == 2 ? (run & 1) : 0]);
                     ++run;
                 }
                 if (++s == kStages) { s = 0; ph ^= 1u; }
                 if (++kbi == g.kb) kbi = 0;
             }
-            stamp(g, c, 4);                        // phase 4: last MMA issued
+            stamp(g, cta, 4);                      // phase 4: last MMA issued
         }
     } else if (warp >= 4) {                        // ---- epilogue: TMEM lane = weight row
         pdl_wait();                                // outputs / partials written only after it
         const int q = warp - 4;                    // TMEM lane quarter of this warp
         const int row = q * 32 + lane;             // row within the 128-row tile
-        const int cfirst_run_tile = (int)(u0 / g.kb);
+        const int cfirst_run_ut = (int)(u0 / g.kb);   // first tile (pair) of this worker's range
+        const uint32_t tmem_empty_leader = kPair ? leader_addr(&tmem_empty[0]) : 0;
         int run = 0;
         for (uint64_t u = u0; u < u1; ++run) {
-            const int tile = (int)(u / g.kb);
-            const uint64_t tend = (uint64_t)(tile + 1) * g.kb;
+            const int ut = (int)(u / g.kb);        // unit tile (tile, or tile pair)
+            const int tile = ut * TM::kT + r;
+            const bool phantom = tile >= g.tiles;  // pair mode, odd tile count: zero rows
+            const uint64_t tend = (uint64_t)(ut + 1) * g.kb;
             const uint64_t rend = u1 < tend ? u1 : tend;
-            const int si = seg_of(g, tile);
+            const int si = seg_of(g, phantom ? g.tiles - 1 : tile);
             const TcSeg& seg = g.seg[si];
             const int n = (tile - seg.tile0) * kBN + row;
-            const bool nvalid = n < seg.N;
+            const bool nvalid = !phantom && n < seg.N;
             const float bias_n = (seg.bias && nvalid) ? __bfloat162float(seg.bias[n]) : 0.f;
-            const int c_first = cta_of(g, (uint64_t)tile * g.kb), c_last = cta_of(g, tend - 1);
+            const int c_first = cta_of(g, (uint64_t)ut * g.kb), c_last = cta_of(g, tend - 1);
             const bool whole = c_first == c_last;
-            const int which = tile == cfirst_run_tile ? 0 : 1;
-            float* prow = g.partial + ((size_t)c * 2 + which) * (size_t)g.Mp * kBN + row;
+            const int which = ut == cfirst_run_ut ? 0 : 1;
+            float* prow = g.partial + ((size_t)cta * 2 + which) * (size_t)g.Mp * kBN + row;
             const int b = nacc == 2 ? (run & 1) : 0;
             const int use = nacc == 2 ? (run >> 1) : run;
             mbar_wait(&tmem_full[b], (uint32_t)use & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (row == 0 && rend == u1) stamp(g, c, 5);   // phase 5: last accumulator ready
+            if (row == 0 && rend == u1) stamp(g, cta, 5);   // phase 5: last accumulator ready
             float v[16];
             for (int col = 0; col < g.Mp; col += 16) {
                 tmem_ld16(tmem_base + (uint32_t)b * nbuf + ((uint32_t)(q * 32) << 16) + (uint32_t)col, v);
+                if (phantom) continue;
                 if (!whole) {              // token-major partial: one 128-B store per warp per token
 #pragma unroll
                     for (int j = 0; j < 16; ++j) prow[(size_t)(col + j) * kBN] = v[j];
@@ -272,9 +349,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[b])) : "memory");
-            if (row == 0 && rend == u1) stamp(g, c, 6);   // phase 6: last run drained
-            if (!whole && !g.ext_fixup) {
+            if (lane == 0) {
+                if (kPair)
+                    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(tmem_empty_leader + (uint32_t)b * 8)
+                                 : "memory");
+                else
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[b])) : "memory");
+            }
+            if (row == 0 && rend == u1) stamp(g, cta, 6);   // phase 6: last run drained
+            if (!whole && !g.ext_fixup && !phantom) {
                 // fix-up: the last CTA to finish a run of this tile sums all runs in k order.
                 // bar.sync orders the 128 threads' partial stores before thread 0's gpu-scope
                 // acq_rel atomic (release is cumulative); the acquire + bar.sync orders the
@@ -296,20 +379,20 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                             for (int j = 0; j < 8; ++j) acc[j] = 0.f;
                             int cc = c_first;
                             for (; cc + 1 <= c_last; cc += 2) {
-                                const float* p0 = partial_run(g, cc, c_first, tile, row) + (size_t)m0 * kBN;
-                                const float* p1 = partial_run(g, cc + 1, c_first, tile, row) + (size_t)m0 * kBN;
-                                float a[8], b[8];
+                                const float* p0 = partial_run<kPair>(g, cc, c_first, ut, r, row) + (size_t)m0 * kBN;
+                                const float* p1 = partial_run<kPair>(g, cc + 1, c_first, ut, r, row) + (size_t)m0 * kBN;
+                                float a[8], bb[8];
 #pragma unroll
                                 for (int j = 0; j < 8; ++j) a[j] = __ldcg(p0 + j * kBN);
 #pragma unroll
-                                for (int j = 0; j < 8; ++j) b[j] = __ldcg(p1 + j * kBN);
+                                for (int j = 0; j < 8; ++j) bb[j] = __ldcg(p1 + j * kBN);
 #pragma unroll
                                 for (int j = 0; j < 8; ++j) acc[j] += a[j];
 #pragma unroll
-                                for (int j = 0; j < 8; ++j) acc[j] += b[j];
+                                for (int j = 0; j < 8; ++j) acc[j] += bb[j];
                             }
                             if (cc == c_last) {
-                                const float* p0 = partial_run(g, cc, c_first, tile, row) + (size_t)m0 * kBN;
+                                const float* p0 = partial_run<kPair>(g, cc, c_first, ut, r, row) + (size_t)m0 * kBN;
 #pragma unroll
                                 for (int j = 0; j < 8; ++j) acc[j] += __ldcg(p0 + j * kBN);
                             }
@@ -326,20 +409,26 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) stamp(g, c, 7);          // phase 7: CTA done
-    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
+    if (kPair) cluster_sync_all();                 // no CTA leaves while its peer may still signal it
+    else __syncthreads();
+    if (threadIdx.x == 0) stamp(g, cta, 7);        // phase 7: CTA done
+    if (warp == 2) {
+        if (kPair) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
+        else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
+    }
 }
 
 // Split-tile reduction as its own grid (ext_fixup, large M): CTA (tile, 16-token group), thread =
 // weight row. Same fixed run order as the in-kernel fix-up, so the bits do not depend on which
 // of the two reduces (the choice may follow M; the split itself never does).
+template <bool kPair>
 __global__ void __launch_bounds__(kBN) tc_fixup_kernel(TcArgs g) {
     pdl_wait();                                    // every partial of the GEMM is written
     pdl_trigger();
     const int tile = blockIdx.x, row = threadIdx.x, m0 = blockIdx.y * 16;
-    const uint64_t tend = (uint64_t)(tile + 1) * g.kb;
-    const int c_first = cta_of(g, (uint64_t)tile * g.kb), c_last = cta_of(g, tend - 1);
+    const int ut = tile / TileMap<kPair>::kT, r = tile % TileMap<kPair>::kT;
+    const uint64_t tend = (uint64_t)(ut + 1) * g.kb;
+    const int c_first = cta_of(g, (uint64_t)ut * g.kb), c_last = cta_of(g, tend - 1);
     if (c_first == c_last || m0 >= g.M) return;   // whole tile: stored by the GEMM itself
     const TcSeg& seg = g.seg[seg_of(g, tile)];
     const int n = (tile - seg.tile0) * kBN + row;
@@ -349,7 +438,7 @@ __global__ void __launch_bounds__(kBN) tc_fixup_kernel(TcArgs g) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = 0.f;
     for (int cc = c_first; cc <= c_last; ++cc) {
-        const float* p = partial_run(g, cc, c_first, tile, row) + (size_t)m0 * kBN;
+        const float* p = partial_run<kPair>(g, cc, c_first, ut, r, row) + (size_t)m0 * kBN;
         float t[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) t[j] = __ldcg(p + j * kBN);
@@ -486,42 +575,87 @@ static int tc_align() {
     return v;
 }
 
+// CTA-pair mode (cta_group::2, see tc_gemm_kernel<true>): one process-wide choice, never a
+// function of M, so the split and the reduction order stay batch-invariant. MPSW_TC_PAIR
+// overrides the default (dev / A-B measurement).
+int tc_pair() {
+    static int v = env_int("MPSW_TC_PAIR", 0);
+    return v;
+}
+
+// Workers (CTAs, or CTA pairs in pair mode) of a GEMM with `tiles` 128-row tiles: stream-K over
+// the (tile or pair, k-block) units with at least tc_min_units() units per worker and at most
+// tc_ctas_per_sm() x #SMs CTAs, or the tile-aligned split when it keeps >= 80 % of that grid.
 static int tc_grid(int tiles, int K) {
+    const int kt = tc_pair() ? 2 : 1;
+    const int ut = (tiles + kt - 1) / kt;          // unit tiles (tiles or pairs)
     const int kb = (K + kBK - 1) / kBK;
-    const uint64_t units = (uint64_t)tiles * kb;
+    const uint64_t units = (uint64_t)ut * kb;
     const uint64_t mu = (uint64_t)tc_min_units();
-    const uint64_t gmax = (uint64_t)tc_ctas_per_sm() * sm_count();
+    const uint64_t gmax = (uint64_t)tc_ctas_per_sm() * sm_count() / kt;
     const uint64_t g_sk = std::min<uint64_t>((units + mu - 1) / mu, gmax);
-    if (tc_align() && (uint64_t)tiles < gmax) {
+    if (tc_align() && (uint64_t)ut < gmax) {
         int best = 0;
         for (int sp = 1; sp <= kb; ++sp)
-            if (kb % sp == 0 && (uint64_t)tiles * sp <= gmax && (uint64_t)(kb / sp) >= mu) best = sp;
-        if (best && (uint64_t)tiles * best * 5 >= g_sk * 4) return tiles * best;
+            if (kb % sp == 0 && (uint64_t)ut * sp <= gmax && (uint64_t)(kb / sp) >= mu) best = sp;
+        if (best && (uint64_t)ut * best * 5 >= g_sk * 4) return ut * best;
     }
     return (int)g_sk;
 }
 
 size_t tc_partial_floats(int n_total, int K, int Mp) {
-    return (size_t)tc_grid((n_total + kBN - 1) / kBN, K) * 2 * kBN * Mp;
+    const int kt = tc_pair() ? 2 : 1;
+    return (size_t)tc_grid((n_total + kBN - 1) / kBN, K) * kt * 2 * kBN * Mp;
 }
+
+// Token rows of the B tile one CTA holds: Mp, or Mp / 2 in pair mode (N split across the pair).
+static int tc_xrows(int Mp) { return tc_pair() ? Mp / 2 : Mp; }
 
 // Stages sized so that two CTAs fit per SM (<= ~110 KB each).
 int tc_stages(int Mp) {
     static int budget_kb = env_int("MPSW_TC_SMEM_KB", 104);
-    const size_t per = kTileABytes + (size_t)Mp * kBK * 2;
+    const size_t per = kTileABytes + (size_t)tc_xrows(Mp) * kBK * 2;
     return (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, ((size_t)budget_kb * 1024) / per));
 }
 
 size_t tc_smem_bytes(int Mp) {
-    return 1024 + tc_stages(Mp) * (kTileABytes + (size_t)Mp * kBK * 2) + (2 * kMaxStages + 4) * 8 + 16;
+    return 1024 + tc_stages(Mp) * (kTileABytes + (size_t)tc_xrows(Mp) * kBK * 2) + (2 * kMaxStages + 4) * 8 + 16;
 }
 
 static unsigned long long* g_tc_trace = nullptr;   // dev instrumentation (mpsw_bench_gemm only)
 void tc_set_trace(unsigned long long* p) { g_tc_trace = p; }
-int tc_grid_for(int n_total, int K) { return tc_grid((n_total + kBN - 1) / kBN, K); }
+// CTAs launched for a GEMM (pair mode: 2 per worker)
+int tc_grid_for(int n_total, int K) { return tc_grid((n_total + kBN - 1) / kBN, K) * (tc_pair() ? 2 : 1); }
 int tc_grid_tiles(int tiles, int K) { return tc_grid(tiles, K); }
 
 bool tc_supported(int M, int K) { return M >= 1 && M <= 256 && K % 8 == 0; }
+
+template <bool kPair>
+static void launch_tc(const TcArgs& g, size_t smem, cudaStream_t st, const CUtensorMap& m0, const CUtensorMap& m1,
+                      const CUtensorMap& m2, const CUtensorMap& mx) {
+    static thread_local size_t attr_set = 0;
+    if (attr_set < smem) {
+        MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel<kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel<kPair>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        attr_set = smem;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(g.G * (kPair ? 2 : 1));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = kPair ? 2 : 1;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = kPair ? 2 : 1;
+    MPSW_CU(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<kPair>, m0, m1, m2, mx, g));
+    if (g.ext_fixup) launch_pdl(tc_fixup_kernel<kPair>, dim3(g.tiles, g.Mp / 16), kBN, 0, st, g);
+}
 
 // Launch: W segments (up to 3, each [N_i, K] bf16) times X [M, K] bf16 (rows of a buffer with
 // x_rows rows). epi 0: fp32 out = (acc + bias) * scale at out[(row) * ldo + out_col0 + n];
@@ -530,6 +664,7 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
              int nseg, const void* X, int x_rows, int M, int K, int epi, void* out, int ldo, const int32_t* row_of_m,
              float* partial, int* counters, cudaStream_t st) {
     const int Mp = std::max(16, (M + 15) / 16 * 16);
+    const bool pair = tc_pair() != 0;
     TcArgs g{};
     int tiles = 0, n_total = 0;
     for (int i = 0; i < nseg; ++i) {
@@ -544,7 +679,7 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
     g.nseg = nseg;
     g.tiles = tiles;
     g.kb = (K + kBK - 1) / kBK;
-    g.units = (uint64_t)tiles * g.kb;
+    g.units = (uint64_t)(pair ? (tiles + 1) / 2 : tiles) * g.kb;
     g.G = tc_grid(tiles, K);
     g.K = K;
     g.M = M;
@@ -559,23 +694,16 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
     const CUtensorMap& m0 = cached_map(W[0], N[0], K, kBN);
     const CUtensorMap& m1 = cached_map(W[nseg > 1 ? 1 : 0], N[nseg > 1 ? 1 : 0], K, kBN);
     const CUtensorMap& m2 = cached_map(W[nseg > 2 ? 2 : 0], N[nseg > 2 ? 2 : 0], K, kBN);
-    const CUtensorMap& mx = cached_map(X, (uint64_t)x_rows, K, (uint32_t)Mp);
+    const CUtensorMap& mx = cached_map(X, (uint64_t)x_rows, K, (uint32_t)tc_xrows(Mp));
     const size_t smem = tc_smem_bytes(Mp);
-    static thread_local size_t attr_set = 0;
-    if (attr_set < smem) {
-        MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        attr_set = smem;
-
-    }
     g.ext_fixup = Mp >= tc_ext_fixup_min() ? 1 : 0;
     g.trace = g_tc_trace;
     g.l2_prefetch = tc_l2_prefetch();
     int nbuf = 32;
     while (nbuf < Mp) nbuf <<= 1;
     g.nacc = 2 * nbuf * tc_ctas_per_sm() <= 512 ? 2 : 1;
-    launch_pdl(tc_gemm_kernel, g.G, kThreads, smem, st, m0, m1, m2, mx, g);
-    if (g.ext_fixup) launch_pdl(tc_fixup_kernel, dim3(tiles, Mp / 16), kBN, 0, st, g);
+    if (pair) launch_tc<true>(g, smem, st, m0, m1, m2, mx);
+    else launch_tc<false>(g, smem, st, m0, m1, m2, mx);
     MPSW_CU(cudaGetLastError());
 }
 

@@ -1,7 +1,7 @@
 """GEMM microbenchmark sweep (dev): per-layer GEMM shapes of OPT-13B / OPT-1.3B at TP1 x M, for
 tuning knobs given by env vars. Each configuration runs in a fresh process (knobs are read once).
 
-usage: python tools/gemm_tune.py [default|ext|grid|l2pf|smem|align]"""
+usage: python tools/gemm_tune.py [default|ext|grid|l2pf|smem|align|pair]"""
 import json, os, subprocess, sys
 MODELS = {"opt-13b": {"qkv": (15360, 5120), "out": (5120, 5120), "fc1": (20480, 5120), "fc2": (5120, 20480)},
           "opt-1.3b": {"qkv": (6144, 2048), "out": (2048, 2048), "fc1": (8192, 2048), "fc2": (2048, 8192)},
@@ -37,6 +37,10 @@ elif mode == "smem":
 elif mode == "align":
     models = "opt-13b,opt-1.3b,opt-125m"
     configs = [("2", {"MPSW_TC_ALIGN": v}) for v in ("0", "1")]
+elif mode == "pair":
+    models = "opt-13b,opt-1.3b,opt-125m"
+    configs = [("2", {"MPSW_TC_PAIR": v}) for v in ("0", "1")] + [("2", {"MPSW_TC_PAIR": "1", "MPSW_TC_SMEM_KB": v})
+                                                                 for v in ("88", "112")]
 elif mode == "grid":
     models = "opt-13b,opt-1.3b"
     configs = [("2", {}), ("2", {"MPSW_TC_CPS": "1", "MPSW_TC_SMEM_KB": "200"}), ("1", {})]
