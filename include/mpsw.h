@@ -253,6 +253,9 @@ typedef struct {
     uint64_t fwd_gpu_n;           /* batches in that sum                                    */
     uint64_t region_bytes;        /* parameter region per rank (budget rounded down to 4 KiB) */
     uint64_t prefetches;          /* load entries issued by the prefetch policy               */
+    uint64_t numa_requested;      /* pinned arenas bound (mbind) to their GPU's NUMA node      */
+    uint64_t numa_verified;       /* ...of which sampled pages are resident on that node      */
+                                  /* (move_pages); MPSW_NUMA_NODE=n forces node n (tests)      */
 } mpsw_stats;
 
 mpsw_status mpsw_get_stats(mpsw_ctx* ctx, mpsw_stats* out);

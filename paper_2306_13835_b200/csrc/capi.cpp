@@ -261,6 +261,7 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     mpsw_ctx* raw = c.release();
     for (auto& R : raw->ranks) R->th = std::thread(worker_main, raw, R.get());
     raw->engine = std::thread(raw->leader ? engine_main : follower_main, raw);
+    if (raw->leader) raw->completer = std::thread(completer_main, raw);
     *out = raw;
     return MPSW_OK;
     API_END
@@ -280,6 +281,12 @@ mpsw_status mpsw_shutdown(mpsw_ctx* c) {
     }
     c->cmd_cv.notify_all();
     if (c->engine.joinable()) c->engine.join();
+    {
+        std::lock_guard<std::mutex> lk(c->comp_mu);
+        c->comp_stop = true;
+    }
+    c->comp_cv.notify_all();
+    if (c->completer.joinable()) c->completer.join();
     if (c->mp && c->leader) c->ctl->stop.store(1, std::memory_order_release);
     for (auto& R : c->ranks) {
         { std::lock_guard<std::mutex> lk(R->mu); }
@@ -768,6 +775,12 @@ mpsw_status mpsw_get_stats(mpsw_ctx* c, mpsw_stats* o) {
     o->prefetches = c->prefetches.load();
     o->fwd_gpu_us_sum = c->fwd_us_sum.load();
     o->fwd_gpu_n = c->fwd_n.load();
+    o->numa_requested = o->numa_verified = 0;
+    for (auto& m : c->models)
+        for (auto& a : m->arena) {
+            o->numa_requested += a.numa >= 0;
+            o->numa_verified += a.numa_ok;
+        }
     return MPSW_OK;
     API_END
 }

@@ -194,6 +194,8 @@ void dispatch(mpsw_ctx* c, const std::vector<Decision>& ds, double now) {
             // pack tokens + meta into the pinned ring entry (shm in mp mode: every rank reads it)
             e->ring = c->ring_next;
             c->ring_next = (c->ring_next + 1) % c->ring_n;
+            // the slot's previous batch may still be copying out on the completer thread
+            for (int spins = 0; c->slot_busy[e->ring].load(std::memory_order_acquire);) spin_pause(spins);
             uint8_t* ring = c->stg + (size_t)e->ring * c->ring_stride;
             int32_t* tok = (int32_t*)(ring + c->ring_tok_off);
             int32_t* meta = tok + c->max_rows;
@@ -242,22 +244,45 @@ void step_and_dispatch(mpsw_ctx* c, const std::function<void(std::vector<Decisio
     dispatch(c, ds, now);
 }
 
-void complete_batch(mpsw_ctx* c, Entry& e, double now) {
-    const uint8_t* ring = c->stg + (size_t)e.ring * c->ring_stride;
-    const int V = c->models[e.model]->dims.vocab;
-    for (size_t b = 0; b < e.reqs.size(); ++b) {
-        auto& rq = e.reqs[b];
-        std::memcpy(rq->out, (const float*)ring + b * (size_t)V, (size_t)V * 4);
+// Batch completion on the engine thread: stamp t_done (the last rank's slice has landed, reading
+// #15) and hand the logits copy-out to the completer thread, so [B, V] fp32 memcpys (6.4 MB at
+// cfg4) never stall scheduling or ack processing.
+void complete_batch(mpsw_ctx* c, const EntryP& e, double now) {
+    for (auto& rq : e->reqs) {
         rq->t_done = now;
         c->eng_reqs.erase(rq->rid);
     }
-    {
-        std::lock_guard<std::mutex> lk(c->done_mu);
-        for (auto& rq : e.reqs) rq->done.store(1, std::memory_order_release);
-    }
     c->n_batches++;
-    c->n_requests += e.reqs.size();
-    c->done_cv.notify_all();
+    c->n_requests += e->reqs.size();
+    c->slot_busy[e->ring].store(1, std::memory_order_release);
+    {
+        std::lock_guard<std::mutex> lk(c->comp_mu);
+        c->comp_q.push_back(e);
+    }
+    c->comp_cv.notify_one();
+}
+
+void completer_main(mpsw_ctx* c) {
+    for (;;) {
+        EntryP e;
+        {
+            std::unique_lock<std::mutex> lk(c->comp_mu);
+            c->comp_cv.wait(lk, [&] { return !c->comp_q.empty() || c->comp_stop; });
+            if (c->comp_q.empty()) return;
+            e = c->comp_q.front();
+            c->comp_q.pop_front();
+        }
+        const uint8_t* ring = c->stg + (size_t)e->ring * c->ring_stride;
+        const int V = c->models[e->model]->dims.vocab;
+        for (size_t b = 0; b < e->reqs.size(); ++b)
+            std::memcpy(e->reqs[b]->out, (const float*)ring + b * (size_t)V, (size_t)V * 4);
+        c->slot_busy[e->ring].store(0, std::memory_order_release);
+        {
+            std::lock_guard<std::mutex> lk(c->done_mu);
+            for (auto& rq : e->reqs) rq->done.store(1, std::memory_order_release);
+        }
+        c->done_cv.notify_all();
+    }
 }
 
 // Device time of a finished batch's forward on the first local rank (stats), then free its events.
@@ -326,6 +351,7 @@ bool poll_inflight(mpsw_ctx* c) {
     bool progressed = false;
     for (size_t i = 0; i < c->inflight.size();) {
         Entry& e = *c->inflight[i];
+        const EntryP ep = c->inflight[i];
         bool finished = false;
         for (int r = 0; r < c->nr; ++r) {
             if (e.acked[r] || !rank_done(c, e, r)) continue;
@@ -346,7 +372,7 @@ bool poll_inflight(mpsw_ctx* c) {
         if (e.n_acked == c->nr) {
             const double now = now_s(c->t0);
             if (e.kind == E_BATCH) {
-                complete_batch(c, e, now);
+                complete_batch(c, ep, now);
                 log_event(c, "{\"ev\":\"batch_done\",\"t\":" + fmt_d(now) + ",\"batch\":" + std::to_string(e.id) + "}");
                 step_and_dispatch(c, [&](std::vector<Decision>& ds) { c->sm.batch_done(e.id, now, ds); }, now);
                 record_fwd_time(c, e);
@@ -584,6 +610,8 @@ void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& dmax) {
     const mpsw_opt_dims& d = dmax;
     // staging ring: per entry [max_batch * V] fp32 logits, then tokens [max_rows] + meta
     c->ring_n = c->D + 1;
+    c->slot_busy.reset(new std::atomic<int>[c->ring_n]);
+    for (int j = 0; j < c->ring_n; ++j) c->slot_busy[j].store(0);
     const size_t logits_b = ((size_t)c->cfg.max_batch * d.vocab * 4 + 255) & ~size_t(255);
     c->ring_tok_off = logits_b;
     c->ring_stride = (logits_b + (size_t)(c->max_rows * 3 + 3 * c->cfg.max_batch + 8) * 4 + 4095) & ~size_t(4095);

@@ -25,6 +25,8 @@ struct PinnedBuf {
     uint8_t* p = nullptr;
     uint64_t bytes = 0;
     uint64_t map_bytes = 0;
+    int numa = -1;            // node the arena was bound to (-1: none)
+    bool numa_ok = false;     // sampled pages verified resident on that node
 };
 
 inline void spin_pause(int& spins) {
@@ -264,6 +266,14 @@ struct mpsw_ctx {
     std::atomic<int64_t> next_rid{0};
     int ring_next = 0;
     std::mutex api_mu;
+    // result return (a7) off the engine thread: a completer thread copies each finished batch's
+    // logits from the staging ring into the callers' buffers; the ring slot stays busy until then
+    std::thread completer;
+    std::mutex comp_mu;
+    std::condition_variable comp_cv;
+    std::deque<mpsw::EntryP> comp_q;
+    bool comp_stop = false;
+    std::unique_ptr<std::atomic<int>[]> slot_busy;
     std::mutex tap_mu;
     mpsw::Tap tap_next;        // armed by mpsw_test_tap, taken by the next dispatched batch
     std::atomic<int> fault_rank{-1};   // mpsw_test_inject_fault: this rank throws at its next all-reduce point
@@ -301,6 +311,7 @@ void group_barrier(mpsw_ctx* c, int stage = 0);
 void worker_main(mpsw_ctx* c, Rank* R);
 void push_to_rank(Rank& R, const EntryP& e);
 void engine_main(mpsw_ctx* c);
+void completer_main(mpsw_ctx* c);
 void follower_main(mpsw_ctx* c);
 void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& dmax);
 void check_dims(mpsw_ctx* c, const mpsw_opt_dims& d);   // kernel limits + fits dims_max (after geometry)

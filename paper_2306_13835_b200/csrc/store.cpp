@@ -15,6 +15,7 @@
 namespace mpsw {
 
 int gpu_numa_node(int dev) {
+    if (const char* f = getenv("MPSW_NUMA_NODE")) return atoi(f);   // forced (tests, remote-node runs)
     char bus[64] = {0};
     if (cudaDeviceGetPCIBusId(bus, sizeof(bus), dev) != cudaSuccess) return -1;
     for (char* c = bus; *c; ++c) *c = (char)tolower(*c);
@@ -48,7 +49,7 @@ PinnedBuf pin_alloc(uint64_t bytes, int numa_node) {
     madvise(p, b.map_bytes, MADV_HUGEPAGE);
     if (numa_node >= 0 && numa_node < 64) {
         unsigned long mask = 1ul << numa_node;
-        syscall(SYS_mbind, p, b.map_bytes, 2 /*MPOL_BIND*/, &mask, 64, 0);
+        if (syscall(SYS_mbind, p, b.map_bytes, 2 /*MPOL_BIND*/, &mask, 64, 0) == 0) b.numa = numa_node;
     }
     cudaError_t e = cudaHostRegister(p, b.map_bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
     if (e != cudaSuccess) {
@@ -57,6 +58,17 @@ PinnedBuf pin_alloc(uint64_t bytes, int numa_node) {
         throw Error(MPSW_ENOMEM, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
     }
     b.p = (uint8_t*)p;
+    if (b.numa >= 0) {
+        // registration faulted every page in under the binding policy: check where 16 sampled
+        // pages live (move_pages with no target nodes only reports)
+        void* pages[16];
+        int status[16];
+        const uint64_t step = std::max<uint64_t>(4096, b.map_bytes / 16 / 4096 * 4096);
+        int n = 0;
+        for (uint64_t off = 0; off < b.map_bytes && n < 16; off += step) pages[n++] = (uint8_t*)p + off;
+        b.numa_ok = syscall(SYS_move_pages, 0, n, pages, nullptr, status, 0) == 0 &&
+                    std::all_of(status, status + n, [&](int s) { return s == b.numa; });
+    }
     return b;
 }
 

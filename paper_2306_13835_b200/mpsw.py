@@ -52,7 +52,8 @@ class Stats(C.Structure):
                 ("swaps_in", C.c_uint64), ("swaps_out", C.c_uint64), ("batches", C.c_uint64),
                 ("requests", C.c_uint64), ("rejected", C.c_uint64), ("k_slots", C.c_int),
                 ("shard_bytes", C.c_uint64), ("fwd_gpu_us_sum", C.c_uint64), ("fwd_gpu_n", C.c_uint64),
-                ("region_bytes", C.c_uint64), ("prefetches", C.c_uint64)]
+                ("region_bytes", C.c_uint64), ("prefetches", C.c_uint64), ("numa_requested", C.c_uint64),
+                ("numa_verified", C.c_uint64)]
 
 
 _P = C.c_void_p

@@ -14,3 +14,4 @@ for p in 0 1; do
 done
 timeout 1200 python -m pytest tests/test_gpu_pp.py tests/test_gpu_runtime.py -q --tb=short > $O/pytest_pp_runtime.txt 2>&1
 timeout 1500 python tools/auto_table.py --out $O/auto_table.ndjson > $O/auto_table.log 2>&1
+timeout 300 python -m pytest tests/test_gpu_numa.py -q > $O/pytest_numa.txt 2>&1
