@@ -9,6 +9,16 @@
 
 namespace mpsw {
 
+// Reduce-scatter all-reduce from this many bytes of peer partials per rank and point
+// ((t-1)·M·h·4); MPSW_RS_MIN_BYTES overrides (0 = always, huge = never).
+static uint64_t rs_min_bytes() {
+    static uint64_t v = [] {
+        const char* e = getenv("MPSW_RS_MIN_BYTES");
+        return e ? (uint64_t)atoll(e) : (uint64_t)(2u << 20);
+    }();
+    return v;
+}
+
 void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
     const FwdShape& s = c->models[e.model]->fs[R.local];
     const int B = e.B, M = e.M;
@@ -29,6 +39,15 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
     const int32_t* pos = R.ws.meta + 2 * B + 1;
     int nl = 0;
     uint64_t& point = R.ar_point;                  // persistent: parity alternates across batches
+    // Reduce-scatter all-reduce (large M·h·(t-1)): each rank reduces, adds bias + residual and
+    // normalises only its own slice of the M rows, then writes that slice's bf16 LN output into
+    // every rank's A operand (the all-gather); the fp32 residual stream stays sharded by rows.
+    // Per point and rank that moves (t-1)/t·M·h·(4 + 2) bytes instead of (t-1)·M·h·4. Same adds in
+    // the same order per element, same LN code: bitwise identical to the direct mode (tested), so
+    // the choice may follow M. Not with pipeline stages (the hop needs every row) or taps.
+    const bool rs = t > 1 && c->pp == 1 && e.tap.dst == nullptr &&
+                    (uint64_t)(t - 1) * M * s.hidden * 4 >= rs_min_bytes();
+    const int rs_row0 = (int)((int64_t)M * R.trank / t), rs_rows = (int)((int64_t)M * (R.trank + 1) / t) - rs_row0;
     // all-reduce point: record my partial, barrier with the other TP ranks of my stage, wait for
     // every peer's partial on my stream, then the fused reduce + bias + residual + LN kernel
     // reads all t partials directly (peer / IPC mappings over NVLink).
@@ -46,7 +65,19 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
                 if (g0 + p != r) MPSW_CU(cudaStreamWaitEvent(cs, c->peer_ev[g0 + p][pb], 0));
         }
         for (int p = 0; p < t; ++p) peers[p] = c->peer_partial[g0 + p][pb];
-        nl += fwd_reduce_ln(s, M, peers, t, residual, bias, pos_table, pos, g, b, R.ws.x, R.ws.a, cs);
+        if (!rs) {
+            nl += fwd_reduce_ln(s, M, peers, t, residual, bias, pos_table, pos, g, b, R.ws.x, R.ws.a, cs);
+        } else {
+            void* outs[kMaxRanks];
+            for (int p = 0; p < t; ++p) outs[p] = c->peer_a[g0 + p];
+            nl += fwd_reduce_ln_rows(s, rs_row0, rs_rows, peers, t, residual, bias, pos_table, pos, g, b, R.ws.x, outs, t,
+                                     cs);
+            // every rank's slice must have landed in my A operand before my next GEMM reads it
+            MPSW_CU(cudaEventRecord(R.ev_ag[pb], cs));
+            group_barrier(c, R.stage);
+            for (int p = 0; p < t; ++p)
+                if (g0 + p != r) MPSW_CU(cudaStreamWaitEvent(cs, c->peer_ev_ag[g0 + p][pb], 0));
+        }
         ++point;
     };
     if (first) {

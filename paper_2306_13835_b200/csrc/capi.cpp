@@ -312,6 +312,8 @@ mpsw_status mpsw_shutdown(mpsw_ctx* c) {
         R->gates.clear();
         for (auto ev : R->ev_point)
             if (ev) cudaEventDestroy(ev);
+        for (auto ev : R->ev_ag)
+            if (ev) cudaEventDestroy(ev);
         if (R->ev_stage) cudaEventDestroy(R->ev_stage);
         for (auto ev : R->ev_hop) cudaEventDestroy(ev);
         if (R->hop_base) cudaFree(R->hop_base);

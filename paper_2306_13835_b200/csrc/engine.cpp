@@ -591,6 +591,8 @@ void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& dmax) {
         MPSW_CU(cudaMemset(R.ws_base, 0, wsb));
         workspace_carve(R.ws, f, c->max_rows, c->cfg.max_batch, R.ws_base);
         for (auto& ev : R.ev_point) MPSW_CU(cudaEventCreateWithFlags(&ev, ev_flags));
+        for (auto& ev : R.ev_ag) MPSW_CU(cudaEventCreateWithFlags(&ev, ev_flags));
+        c->peer_a[R.index] = R.ws.a;
         MPSW_CU(cudaEventCreateWithFlags(&R.ev_stage, cudaEventDisableTiming));
         if (c->pp > 1 && R.stage + 1 < c->pp) {      // hop ring: one [max_rows, h] fp32 slot per ring entry
             const size_t slot = ((size_t)c->max_rows * dmax.hidden * 4 + 255) & ~size_t(255);
@@ -605,6 +607,7 @@ void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& dmax) {
         for (int pb = 0; pb < 2; ++pb) {
             c->peer_partial[R.index][pb] = R.ws.partial[pb];
             c->peer_ev[R.index][pb] = R.ev_point[pb];
+            c->peer_ev_ag[R.index][pb] = R.ev_ag[pb];
         }
     }
     const mpsw_opt_dims& d = dmax;
@@ -627,7 +630,9 @@ void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& dmax) {
         for (int pb = 0; pb < 2; ++pb) {
             s->partial_off[R.index][pb] = (uint64_t)((uint8_t*)R.ws.partial[pb] - R.ws_base);
             MPSW_CU(cudaIpcGetEventHandle(&s->ev_handle[R.index][pb], R.ev_point[pb]));
+            MPSW_CU(cudaIpcGetEventHandle(&s->ev_ag_handle[R.index][pb], R.ev_ag[pb]));
         }
+        s->a_off[R.index] = (uint64_t)((uint8_t*)R.ws.a - R.ws_base);
         const std::string stg_name = c->shm_name + "_stg";
         if (c->leader) {
             c->stg = (uint8_t*)shm_map(stg_name, stg_bytes, true);
@@ -653,7 +658,11 @@ void setup_geometry(mpsw_ctx* c, const mpsw_opt_dims& dmax) {
                 MPSW_CU(cudaIpcOpenEventHandle(&ev, s->ev_handle[p][pb]));
                 c->ipc_ev_opened.push_back(ev);
                 c->peer_ev[p][pb] = ev;
+                MPSW_CU(cudaIpcOpenEventHandle(&ev, s->ev_ag_handle[p][pb]));
+                c->ipc_ev_opened.push_back(ev);
+                c->peer_ev_ag[p][pb] = ev;
             }
+            c->peer_a[p] = (uint8_t*)base + s->a_off[p];
         }
         group_barrier(c);
         if (c->leader) shm_unlink(stg_name.c_str());   // mapped everywhere; name no longer needed

@@ -229,6 +229,13 @@ struct Peers {
     int n;
 };
 
+// Destinations of the LN output rows: the local A-operand buffer, or (reduce-scatter mode) every
+// TP rank's, in rank order.
+struct LnDst {
+    void* p[8];
+    int n;
+};
+
 
 // Row sum of a 512-thread CTA: warp butterflies, then the 16 warp partials in warp order
 // (fc::ln_red16) — the order the fused layers kernel reproduces with 128 threads.
@@ -250,10 +257,10 @@ __global__ void __launch_bounds__(kLnThreads) reduce_ln_kernel(Peers peers, cons
                                                               const T* __restrict__ bias, const T* __restrict__ pos_table,
                                                               const int32_t* __restrict__ pos, const T* __restrict__ gamma,
                                                               const T* __restrict__ beta, float* __restrict__ x_out,
-                                                              T* __restrict__ ln_out, int h) {
+                                                              LnDst dst, int h, int row0) {
     __shared__ float red[32];
     pdl_trigger();
-    const int m = blockIdx.x;
+    const int m = row0 + blockIdx.x;
     const size_t row = (size_t)m * h;
     const int h4 = h / 4;
     // parameters (bias, gamma, beta) do not depend on the previous kernel: load them while it
@@ -343,9 +350,9 @@ __global__ void __launch_bounds__(kLnThreads) reduce_ln_kernel(Peers peers, cons
     for (int i = 0; i < VPT; ++i) {
         const int j4 = threadIdx.x + i * kLnThreads;
         if (j4 >= h4) break;
-        store4<T>(ln_out + row + 4 * j4, ln_norm(x[i].x, mean, den, ga[i].x, be[i].x),
-                  ln_norm(x[i].y, mean, den, ga[i].y, be[i].y), ln_norm(x[i].z, mean, den, ga[i].z, be[i].z),
-                  ln_norm(x[i].w, mean, den, ga[i].w, be[i].w));
+        const float o0 = ln_norm(x[i].x, mean, den, ga[i].x, be[i].x), o1 = ln_norm(x[i].y, mean, den, ga[i].y, be[i].y),
+                    o2 = ln_norm(x[i].z, mean, den, ga[i].z, be[i].z), o3 = ln_norm(x[i].w, mean, den, ga[i].w, be[i].w);
+        for (int d = 0; d < dst.n; ++d) store4<T>((T*)dst.p[d] + row + 4 * j4, o0, o1, o2, o3);
     }
 }
 
@@ -452,42 +459,55 @@ int fwd_embed(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, in
 }
 
 template <typename T, int VPT>
-static void launch_ln(int M, const Peers& P, const float* residual, const void* bias, const void* pos_table,
-                      const int32_t* pos, const void* gamma, const void* beta, float* x_out, void* ln_out, int h,
+static void launch_ln(int rows, int row0, const Peers& P, const float* residual, const void* bias, const void* pos_table,
+                      const int32_t* pos, const void* gamma, const void* beta, float* x_out, const LnDst& D, int h,
                       cudaStream_t st) {
-    launch_pdl(reduce_ln_kernel<T, VPT>, M, kLnThreads, 0, st, P, residual, (const T*)bias, (const T*)pos_table, pos,
-               (const T*)gamma, (const T*)beta, x_out, (T*)ln_out, h);
+    launch_pdl(reduce_ln_kernel<T, VPT>, rows, kLnThreads, 0, st, P, residual, (const T*)bias, (const T*)pos_table, pos,
+               (const T*)gamma, (const T*)beta, x_out, D, h, row0);
 }
 
 template <typename T>
-static void launch_ln_t(int M, const Peers& P, const float* residual, const void* bias, const void* pos_table,
-                        const int32_t* pos, const void* gamma, const void* beta, float* x_out, void* ln_out, int h,
-                        cudaStream_t st) {
+static void launch_ln_t(int rows, int row0, const Peers& P, const float* residual, const void* bias,
+                        const void* pos_table, const int32_t* pos, const void* gamma, const void* beta, float* x_out,
+                        const LnDst& D, int h, cudaStream_t st) {
     const int vpt = (h / 4 + kLnThreads - 1) / kLnThreads;
     switch (vpt) {
-        case 1: launch_ln<T, 1>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, h, st); break;
-        case 2: launch_ln<T, 2>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, h, st); break;
-        case 3: launch_ln<T, 3>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, h, st); break;
-        case 4: launch_ln<T, 4>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, h, st); break;
-        case 5: launch_ln<T, 5>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, h, st); break;
-        case 6: launch_ln<T, 6>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, h, st); break;
+        case 1: launch_ln<T, 1>(rows, row0, P, residual, bias, pos_table, pos, gamma, beta, x_out, D, h, st); break;
+        case 2: launch_ln<T, 2>(rows, row0, P, residual, bias, pos_table, pos, gamma, beta, x_out, D, h, st); break;
+        case 3: launch_ln<T, 3>(rows, row0, P, residual, bias, pos_table, pos, gamma, beta, x_out, D, h, st); break;
+        case 4: launch_ln<T, 4>(rows, row0, P, residual, bias, pos_table, pos, gamma, beta, x_out, D, h, st); break;
+        case 5: launch_ln<T, 5>(rows, row0, P, residual, bias, pos_table, pos, gamma, beta, x_out, D, h, st); break;
+        case 6: launch_ln<T, 6>(rows, row0, P, residual, bias, pos_table, pos, gamma, beta, x_out, D, h, st); break;
         default: throw Error(MPSW_EINVAL, "hidden too large for reduce_ln (max 12288)");
     }
+}
+
+int fwd_reduce_ln_rows(const FwdShape& s, int row0, int rows, const float* const* peer_partials, int n_peers,
+                       const float* residual, const void* bias, const void* pos_table, const int32_t* pos,
+                       const void* gamma, const void* beta, float* x_out, void* const* ln_outs, int n_out,
+                       cudaStream_t st) {
+    Peers P{};
+    LnDst D{};
+    if (n_peers < 1 || n_peers > 8 || n_out < 1 || n_out > 8) throw Error(MPSW_EINVAL, "1..8 peers / outputs");
+    for (int i = 0; i < n_peers; ++i) P.p[i] = peer_partials[i];
+    P.n = n_peers;
+    for (int i = 0; i < n_out; ++i) D.p[i] = ln_outs[i];
+    D.n = n_out;
+    if (rows <= 0) return 0;
+    if (s.dtype == MPSW_BF16)
+        launch_ln_t<bf16>(rows, row0, P, residual, bias, pos_table, pos, gamma, beta, x_out, D, s.hidden, st);
+    else
+        launch_ln_t<float>(rows, row0, P, residual, bias, pos_table, pos, gamma, beta, x_out, D, s.hidden, st);
+    MPSW_CU(cudaGetLastError());
+    return 1;
 }
 
 int fwd_reduce_ln(const FwdShape& s, int M, const float* const* peer_partials, int n_peers, const float* residual,
                   const void* bias, const void* pos_table, const int32_t* pos, const void* gamma, const void* beta,
                   float* x_out, void* ln_out, cudaStream_t st) {
-    Peers P{};
-    if (n_peers < 1 || n_peers > 8) throw Error(MPSW_EINVAL, "1..8 peers");
-    for (int i = 0; i < n_peers; ++i) P.p[i] = peer_partials[i];
-    P.n = n_peers;
-    if (s.dtype == MPSW_BF16)
-        launch_ln_t<bf16>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, s.hidden, st);
-    else
-        launch_ln_t<float>(M, P, residual, bias, pos_table, pos, gamma, beta, x_out, ln_out, s.hidden, st);
-    MPSW_CU(cudaGetLastError());
-    return 1;
+    void* outs[1] = {ln_out};
+    return fwd_reduce_ln_rows(s, 0, M, peer_partials, n_peers, residual, bias, pos_table, pos, gamma, beta, x_out, outs,
+                              1, st);
 }
 
 // Route one GEMM to the tcgen05/TMA kernel (bf16, M <= 256) or the SIMT weight-streaming kernel

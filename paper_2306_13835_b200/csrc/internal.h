@@ -115,6 +115,12 @@ int fwd_embed(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, in
 int fwd_reduce_ln(const FwdShape& s, int M, const float* const* peer_partials, int n_peers,
                   const float* residual, const void* bias, const void* pos_table, const int32_t* pos,
                   const void* gamma, const void* beta, float* x_out, void* ln_out, cudaStream_t st);
+// Reduce-scatter variant: rows [row0, row0 + rows) only, the LN output written to every buffer of
+// ln_outs (all TP ranks' A operands: the all-gather of the bf16 LN output).
+int fwd_reduce_ln_rows(const FwdShape& s, int row0, int rows, const float* const* peer_partials, int n_peers,
+                       const float* residual, const void* bias, const void* pos_table, const int32_t* pos,
+                       const void* gamma, const void* beta, float* x_out, void* const* ln_outs, int n_out,
+                       cudaStream_t st);
 int fwd_qkv(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M, cudaStream_t st);
 int fwd_attention(const FwdShape& s, const FwdWorkspace& ws, int B, cudaStream_t st);
 int fwd_out_proj(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M,

@@ -89,6 +89,8 @@ struct ShmCtl {
     cudaIpcMemHandle_t ws_handle[kMaxRanks];
     uint64_t partial_off[kMaxRanks][2];
     cudaIpcEventHandle_t ev_handle[kMaxRanks][2];
+    uint64_t a_off[kMaxRanks];                       // A-operand buffer (reduce-scatter all-gather)
+    cudaIpcEventHandle_t ev_ag_handle[kMaxRanks][2];
     ShmRec log[kLogCap];
     std::atomic<uint64_t> ack[kAckCap][kMaxRanks];
 };
@@ -180,6 +182,7 @@ struct Rank {
     FwdWorkspace ws;
     std::vector<TensorPtrs> wptr;          // per model: pointers into its current range
     cudaEvent_t ev_point[2] = {nullptr, nullptr};   // partial-ready events (interprocess in mp mode)
+    cudaEvent_t ev_ag[2] = {nullptr, nullptr};      // reduce-scatter: my LN rows written to every rank
     // All-reduce points issued so far by this rank, across batches. Point k uses partial buffer
     // k & 1; the parity must alternate across batch boundaries too (a batch has an odd number of
     // points), or with D > 1 a fast peer's next batch overwrites a partial this rank still reads.
@@ -235,6 +238,8 @@ struct mpsw_ctx {
     // TP peers (global rank -> partial buffers / partial-ready events)
     float* peer_partial[mpsw::kMaxRanks][2] = {};
     cudaEvent_t peer_ev[mpsw::kMaxRanks][2] = {};
+    void* peer_a[mpsw::kMaxRanks] = {};              // every rank's A-operand (LN output) buffer
+    cudaEvent_t peer_ev_ag[mpsw::kMaxRanks][2] = {};
     std::vector<void*> ipc_mem_opened;
     std::vector<cudaEvent_t> ipc_ev_opened;
     // logits / tokens staging ring (pinned; shm in mp mode), D + 1 entries

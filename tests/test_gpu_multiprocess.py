@@ -29,12 +29,16 @@ def free_port():
 
 # 8 processes on one GPU exercise the TP = 8 control plane of cfg4 / `bench.py --gpus 8`: 7 IPC
 # peer mappings per rank, 8-way all-reduce reads, 8 acks per entry
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_process_group(tmp_path, world):
+# rs: the reduce-scatter all-reduce forced on every point (its all-gather writes through the CUDA
+# IPC mappings of every rank's A operand, ordered by interprocess events)
+@pytest.mark.parametrize("world,rs", [(2, 0), (4, 0), (8, 0), (4, 1), (8, 1)])
+def test_process_group(tmp_path, world, rs):
     need_gpu()
     out = str(tmp_path / "mp.json")
     port = free_port()
-    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_group_run.py"), str(r), str(world), str(port), out])
+    env = dict(os.environ, MPSW_RS_MIN_BYTES="0" if rs else str(1 << 62))
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_group_run.py"), str(r), str(world), str(port), out],
+                              env=env)
              for r in range(world)]
     rcs = [p.wait(timeout=600) for p in procs]
     assert rcs == [0] * world

@@ -27,5 +27,6 @@ with M.Ctx(device_ids=(0,) * tp, budget=S + 4096, max_batch=B, max_tokens=L) as 
             ctx.wait_request(r, 120)
     s1 = ctx.stats()
     n = s1["fwd_gpu_n"] - s0["fwd_gpu_n"]
-    print(json.dumps({"model": name, "tp": tp, "B": B, "L": L,
+    import os
+    print(json.dumps({"model": name, "tp": tp, "B": B, "L": L, "rs_min_bytes": os.environ.get("MPSW_RS_MIN_BYTES"),
                       "fwd_ms_device": (s1["fwd_gpu_us_sum"] - s0["fwd_gpu_us_sum"]) / 1e3 / max(1, n)}), flush=True)

@@ -15,3 +15,9 @@ done
 timeout 1200 python -m pytest tests/test_gpu_pp.py tests/test_gpu_runtime.py -q --tb=short > $O/pytest_pp_runtime.txt 2>&1
 timeout 1500 python tools/auto_table.py --out $O/auto_table.ndjson > $O/auto_table.log 2>&1
 timeout 300 python -m pytest tests/test_gpu_numa.py -q > $O/pytest_numa.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_allreduce.py -q --tb=short > $O/pytest_allreduce.txt 2>&1
+for rs in 1152921504606846976 0; do
+  MPSW_RS_MIN_BYTES=$rs timeout 900 python tools/fwd_tp.py opt-30b 8 32 8 >> $O/fwd_tp_rs.txt 2>&1
+  MPSW_RS_MIN_BYTES=$rs timeout 900 python tools/fwd_tp.py opt-13b 8 32 8 >> $O/fwd_tp_rs.txt 2>&1
+done
+timeout 900 python -m pytest tests/test_gpu_multiprocess.py -q --tb=short -k test_process_group > $O/pytest_mp_rs.txt 2>&1
