@@ -19,6 +19,14 @@ static uint64_t rs_min_bytes() {
     return v;
 }
 
+static bool graphs_enabled() {
+    static const bool v = [] {
+        const char* e = getenv("MPSW_GRAPHS");
+        return !e || atoi(e) != 0;
+    }();
+    return v;
+}
+
 void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
     const FwdShape& s = c->models[e.model]->fs[R.local];
     const int B = e.B, M = e.M;
@@ -80,41 +88,6 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
         }
         ++point;
     };
-    if (first) {
-        nl += fwd_embed(s, Wt, R.ws, M, R.ws.partial[point & 1], cs);
-        allreduce_ln(nullptr, nullptr, Wt.embed_pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b);
-    } else if (!c->cfg.pp_broadcast) {
-        // PP hop ("PP communication occurs through FIFO pipes"): this entry came from the
-        // same TP rank of the previous stage after it issued the batch, so its hop event for this
-        // ring slot is already recorded: wait on it and read that rank's residual stream in place
-        // (peer memory over NVLink) into LN1 of my first layer. Slots are reused only after the
-        // batch completed everywhere, so batches of different slots overlap across stages (D > 1).
-        Rank& P = *c->ranks[c->local_of[r - t]];
-        MPSW_CU(cudaStreamWaitEvent(cs, P.ev_hop[e.ring], 0));
-        const float* self[1] = {P.hop[e.ring]};
-        nl += fwd_reduce_ln(s, M, self, 1, nullptr, nullptr, nullptr, pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b,
-                            R.ws.x, R.ws.a, cs);
-        ++point;
-    } else {
-        // broadcast ablation (P:96's ruled-out design, D = 1): the entry reached every stage at
-        // once, so wait on the host until the previous stage has issued this batch
-        Rank& P = *c->ranks[c->local_of[r - t]];
-        int spins = 0;
-        while (P.stage_out.load(std::memory_order_acquire) < e.id + 1) {
-            if (group_poisoned(c)) throw Error(MPSW_ECUDA, "peer failed");
-            spin_pause(spins);
-        }
-        MPSW_CU(cudaStreamWaitEvent(cs, P.ev_stage, 0));
-        float* hop = R.ws.partial[point & 1];
-        MPSW_CU(cudaMemcpyAsync(hop, P.ws.x, (size_t)M * s.hidden * 4, cudaMemcpyDeviceToDevice, cs));
-        const float* self[1] = {hop};
-        nl += fwd_reduce_ln(s, M, self, 1, nullptr, nullptr, nullptr, pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b,
-                            R.ws.x, R.ws.a, cs);
-        ++point;
-    }
-    // All layers in one persistent kernel when eligible (bf16, TP = 1, M <= 48, the only rank on
-    // its GPU); it returns 0 otherwise and the per-op kernels below run. Both paths give the same
-    // bits (fwd_fused.cu).
     // verification tap (mpsw_test_tap): stop after e.tap.n_layers layers (X / A) or inside layer
     // n_layers (QKV / O / R); every rank stops at the same point, so the all-reduce points match
     const Tap& tap = e.tap;
@@ -127,42 +100,122 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
     };
     const size_t esz = s.dtype == MPSW_BF16 ? 2 : 4;
     const int hl = s.heads_local * s.head_dim;
-    bool sole = t == 1 && !tapping;
-    for (const auto& o : c->ranks)
-        if (o.get() != &R && o->device == R.device) sole = false;
-    if (!sole && getenv("MPSW_FUSED_DEBUG")) fprintf(stderr, "[mpsw] fused layers kernel not used: shared GPU / tp\n");
-    const int fused = sole ? fwd_layers_fused(s, Wt, R.ws, B, M, last ? Wt.lnf_w : Wt.layers.back().ln2_w,
-                                              last ? Wt.lnf_b : Wt.layers.back().ln2_b, cs)
-                           : 0;
-    nl += fused;
-    for (int l = 0; l < (fused ? 0 : s.n_layers); ++l) {
-        if (tapping && l == tap.n_layers && tap.what <= MPSW_TAP_A) break;
-        const bool tap_here = tapping && l == tap.n_layers;
-        const auto& L = Wt.layers[l];
-        nl += fwd_qkv(s, L, R.ws, M, cs);
-        if (tap_here && tap.what == MPSW_TAP_QKV) { tap_copy(R.ws.qkv, (size_t)M * 3 * hl * 4); break; }
-        nl += fwd_attention(s, R.ws, B, cs);
-        if (tap_here && tap.what == MPSW_TAP_O) { tap_copy(R.ws.o, (size_t)M * hl * esz); break; }
-        nl += fwd_out_proj(s, L, R.ws, M, R.ws.partial[point & 1], cs);
-        allreduce_ln(R.ws.x, L.o_b, nullptr, L.ln2_w, L.ln2_b);
-        if (tap_here && tap.what == MPSW_TAP_XM) { tap_copy(R.ws.x, (size_t)M * s.hidden * 4); break; }
-        if (tap_here && tap.what == MPSW_TAP_F) { tap_copy(R.ws.a, (size_t)M * s.hidden * esz); break; }
-        nl += fwd_fc1(s, L, R.ws, M, cs);
-        if (tap_here && tap.what == MPSW_TAP_R) { tap_copy(R.ws.r, (size_t)M * s.ffn_local * esz); break; }
-        nl += fwd_fc2(s, L, R.ws, M, R.ws.partial[point & 1], cs);
-        const bool lastl = l + 1 == s.n_layers;
-        // after a non-final stage's last layer only the residual stream matters; the LN output
-        // (computed with this layer's LN2 parameters) is unused
-        const void* ng = lastl ? (last ? Wt.lnf_w : L.ln2_w) : Wt.layers[l + 1].ln1_w;
-        const void* nb = lastl ? (last ? Wt.lnf_b : L.ln2_b) : Wt.layers[l + 1].ln1_b;
-        allreduce_ln(R.ws.x, L.fc2_b, nullptr, ng, nb);
+    // The compute of this batch (embedding or hop, layers, lm_head kernel). At TP = 1 / PP = 1 it is
+    // captured once per (model, range offset, M, B) into a CUDA graph and replayed: one launch
+    // instead of ~7 per layer, so small models are not bound by the worker's launch rate. The
+    // graph holds device pointers only (weights at the model's range offset, the rank's workspace,
+    // tokens / meta already copied in), so a replay computes exactly the captured kernels.
+    auto compute = [&]() {
+        if (first) {
+            nl += fwd_embed(s, Wt, R.ws, M, R.ws.partial[point & 1], cs);
+            allreduce_ln(nullptr, nullptr, Wt.embed_pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b);
+        } else if (!c->cfg.pp_broadcast) {
+            // PP hop ("PP communication occurs through FIFO pipes"): this entry came from the
+            // same TP rank of the previous stage after it issued the batch, so its hop event for this
+            // ring slot is already recorded: wait on it and read that rank's residual stream in place
+            // (peer memory over NVLink) into LN1 of my first layer. Slots are reused only after the
+            // batch completed everywhere, so batches of different slots overlap across stages (D > 1).
+            Rank& P = *c->ranks[c->local_of[r - t]];
+            MPSW_CU(cudaStreamWaitEvent(cs, P.ev_hop[e.ring], 0));
+            const float* self[1] = {P.hop[e.ring]};
+            nl += fwd_reduce_ln(s, M, self, 1, nullptr, nullptr, nullptr, pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b,
+                                R.ws.x, R.ws.a, cs);
+            ++point;
+        } else {
+            // broadcast ablation (P:96's ruled-out design, D = 1): the entry reached every stage at
+            // once, so wait on the host until the previous stage has issued this batch
+            Rank& P = *c->ranks[c->local_of[r - t]];
+            int spins = 0;
+            while (P.stage_out.load(std::memory_order_acquire) < e.id + 1) {
+                if (group_poisoned(c)) throw Error(MPSW_ECUDA, "peer failed");
+                spin_pause(spins);
+            }
+            MPSW_CU(cudaStreamWaitEvent(cs, P.ev_stage, 0));
+            float* hop = R.ws.partial[point & 1];
+            MPSW_CU(cudaMemcpyAsync(hop, P.ws.x, (size_t)M * s.hidden * 4, cudaMemcpyDeviceToDevice, cs));
+            const float* self[1] = {hop};
+            nl += fwd_reduce_ln(s, M, self, 1, nullptr, nullptr, nullptr, pos, Wt.layers[0].ln1_w, Wt.layers[0].ln1_b,
+                                R.ws.x, R.ws.a, cs);
+            ++point;
+        }
+        // All layers in one persistent kernel when eligible (bf16, TP = 1, M <= 48, the only rank on
+        // its GPU); it returns 0 otherwise and the per-op kernels below run. Both paths give the same
+        // bits (fwd_fused.cu).
+        bool sole = t == 1 && !tapping;
+        for (const auto& o : c->ranks)
+            if (o.get() != &R && o->device == R.device) sole = false;
+        if (!sole && getenv("MPSW_FUSED_DEBUG")) fprintf(stderr, "[mpsw] fused layers kernel not used: shared GPU / tp\n");
+        const int fused = sole ? fwd_layers_fused(s, Wt, R.ws, B, M, last ? Wt.lnf_w : Wt.layers.back().ln2_w,
+                                                  last ? Wt.lnf_b : Wt.layers.back().ln2_b, cs)
+                               : 0;
+        nl += fused;
+        for (int l = 0; l < (fused ? 0 : s.n_layers); ++l) {
+            if (tapping && l == tap.n_layers && tap.what <= MPSW_TAP_A) break;
+            const bool tap_here = tapping && l == tap.n_layers;
+            const auto& L = Wt.layers[l];
+            nl += fwd_qkv(s, L, R.ws, M, cs);
+            if (tap_here && tap.what == MPSW_TAP_QKV) { tap_copy(R.ws.qkv, (size_t)M * 3 * hl * 4); break; }
+            nl += fwd_attention(s, R.ws, B, cs);
+            if (tap_here && tap.what == MPSW_TAP_O) { tap_copy(R.ws.o, (size_t)M * hl * esz); break; }
+            nl += fwd_out_proj(s, L, R.ws, M, R.ws.partial[point & 1], cs);
+            allreduce_ln(R.ws.x, L.o_b, nullptr, L.ln2_w, L.ln2_b);
+            if (tap_here && tap.what == MPSW_TAP_XM) { tap_copy(R.ws.x, (size_t)M * s.hidden * 4); break; }
+            if (tap_here && tap.what == MPSW_TAP_F) { tap_copy(R.ws.a, (size_t)M * s.hidden * esz); break; }
+            nl += fwd_fc1(s, L, R.ws, M, cs);
+            if (tap_here && tap.what == MPSW_TAP_R) { tap_copy(R.ws.r, (size_t)M * s.ffn_local * esz); break; }
+            nl += fwd_fc2(s, L, R.ws, M, R.ws.partial[point & 1], cs);
+            const bool lastl = l + 1 == s.n_layers;
+            // after a non-final stage's last layer only the residual stream matters; the LN output
+            // (computed with this layer's LN2 parameters) is unused
+            const void* ng = lastl ? (last ? Wt.lnf_w : L.ln2_w) : Wt.layers[l + 1].ln1_w;
+            const void* nb = lastl ? (last ? Wt.lnf_b : L.ln2_b) : Wt.layers[l + 1].ln1_b;
+            allreduce_ln(R.ws.x, L.fc2_b, nullptr, ng, nb);
+        }
+        if (last && !tapping) nl += fwd_lm_head(s, Wt, R.ws, B, M, cs);
+    };
+    const bool graphable = t == 1 && c->pp == 1 && !tapping && s.gemm_impl != 3 && graphs_enabled() &&
+                           c->fault_rank.load() < 0;
+    if (!graphable) {
+        compute();
+    } else {
+        if (R.graphs.size() > 512) {              // bound the cache (shapes x models x offsets)
+            for (auto& kv : R.graphs)
+                if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+            R.graphs.clear();
+        }
+        GraphRec& g = R.graphs[GraphKey{e.model, e.off, M, B}];
+        if (g.exec) {
+            MPSW_CU(cudaGraphLaunch(g.exec, cs));
+            nl += g.kernels;
+            point += g.points;
+        } else if (!g.seen) {                      // first batch of this shape: eager (sets kernel attributes)
+            g.seen = true;
+            compute();
+        } else {
+            const int nl0 = nl;
+            const uint64_t p0 = point;
+            cudaGraph_t graph = nullptr;
+            MPSW_CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            try {
+                compute();
+            } catch (...) {
+                cudaStreamEndCapture(cs, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                throw;
+            }
+            MPSW_CU(cudaStreamEndCapture(cs, &graph));
+            MPSW_CU(cudaGraphInstantiate(&g.exec, graph, 0));
+            MPSW_CU(cudaGraphDestroy(graph));
+            g.kernels = nl - nl0;
+            g.points = point - p0;
+            MPSW_CU(cudaGraphLaunch(g.exec, cs));
+        }
     }
     if (tapping && !tapped) {
         if (tap.what == MPSW_TAP_X) tap_copy(R.ws.x, (size_t)M * s.hidden * 4);
         else if (tap.what == MPSW_TAP_A) tap_copy(R.ws.a, (size_t)M * s.hidden * esz);
     }
     if (last && !tapping) {
-        nl += fwd_lm_head(s, Wt, R.ws, B, M, cs);
         float* logits_host = (float*)(ring) + (size_t)R.trank * s.vocab_local;
         MPSW_CU(cudaMemcpy2DAsync(logits_host, (size_t)s.vocab * 4, R.ws.logits, (size_t)s.vocab_local * 4,
                                   (size_t)s.vocab_local * 4, B, cudaMemcpyDeviceToHost, cs));

@@ -314,6 +314,9 @@ mpsw_status mpsw_shutdown(mpsw_ctx* c) {
             if (ev) cudaEventDestroy(ev);
         for (auto ev : R->ev_ag)
             if (ev) cudaEventDestroy(ev);
+        for (auto& kv : R->graphs)
+            if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        R->graphs.clear();
         if (R->ev_stage) cudaEventDestroy(R->ev_stage);
         for (auto ev : R->ev_hop) cudaEventDestroy(ev);
         if (R->hop_base) cudaFree(R->hop_base);

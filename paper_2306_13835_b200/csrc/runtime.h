@@ -8,6 +8,7 @@
 #include <immintrin.h>
 
 #include <functional>
+#include <tuple>
 #include <future>
 #include <map>
 #include <string>
@@ -159,6 +160,23 @@ struct Helper {
     std::mutex mu;
 };
 
+// CUDA graph of one batch's compute (TP = 1, PP = 1): keyed by the model, its range offset (so the
+// weight pointers are the captured ones), the token rows M and the batch size B.
+struct GraphKey {
+    int model;
+    uint64_t off;
+    int M, B;
+    bool operator<(const GraphKey& o) const {
+        return std::tie(model, off, M, B) < std::tie(o.model, o.off, o.M, o.B);
+    }
+};
+struct GraphRec {
+    cudaGraphExec_t exec = nullptr;
+    bool seen = false;       // the first batch of a key runs eagerly, the second is captured
+    int kernels = 0;         // kernels in the graph (launch accounting)
+    uint64_t points = 0;     // all-reduce points it advances
+};
+
 struct Rank {
     int index = 0, local = 0, device = 0, numa = -1;   // index = global rank = stage * tp + trank
     int stage = 0, trank = 0;              // pipeline stage, TP rank inside the stage
@@ -187,6 +205,7 @@ struct Rank {
     // k & 1; the parity must alternate across batch boundaries too (a batch has an odd number of
     // points), or with D > 1 a fast peer's next batch overwrites a partial this rank still reads.
     uint64_t ar_point = 0;
+    std::map<GraphKey, GraphRec> graphs;  // worker-thread private
     std::vector<cudaEvent_t> last_compute; // per model
     std::vector<char> last_compute_valid;
     unsigned long long* d_sum = nullptr;

@@ -55,6 +55,7 @@ for B, L in shapes:
             s1 = ctx.stats()
             nb = s1["fwd_gpu_n"] - s0["fwd_gpu_n"]
             ms = (s1["fwd_gpu_us_sum"] - s0["fwd_gpu_us_sum"]) / 1e3 / max(1, nb)
-            print(json.dumps({"model": name, "B": B, "L": L, "impl": ["auto", "simt", "tcgen05", "fused"][impl], "batches": nb, "batch_rows": B * L,
+            import os
+            print(json.dumps({"graphs": os.environ.get("MPSW_GRAPHS", "1"), "pair": os.environ.get("MPSW_TC_PAIR", "0"), "model": name, "B": B, "L": L, "impl": ["auto", "simt", "tcgen05", "fused"][impl], "batches": nb, "batch_rows": B * L,
                               "fwd_ms_device": ms, "GBps": S / (ms / 1e3) / 1e9, "wall_ms_per_round": wall * 1e3}),
                   flush=True)

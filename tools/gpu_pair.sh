@@ -21,3 +21,7 @@ for rs in 1152921504606846976 0; do
   MPSW_RS_MIN_BYTES=$rs timeout 900 python tools/fwd_tp.py opt-13b 8 32 8 >> $O/fwd_tp_rs.txt 2>&1
 done
 timeout 900 python -m pytest tests/test_gpu_multiprocess.py -q --tb=short -k test_process_group > $O/pytest_mp_rs.txt 2>&1
+timeout 600 python -m pytest tests/test_gpu_graphs.py -q --tb=short > $O/pytest_graphs.txt 2>&1
+for g in 0 1; do
+  for m in opt-125m opt-1.3b opt-13b; do MPSW_GRAPHS=$g timeout 900 python tools/fwd_bench.py $m tc shapes=1x2,8x8 >> $O/fwd_graphs.ndjson 2>&1; done
+done
