@@ -21,7 +21,7 @@ def budget_for(d, tp, pp, k=1):
 
 
 @pytest.mark.parametrize("tp,pp,name,D", [(1, 2, "mid", 1), (2, 2, "mid", 2), (1, 3, "small", 3), (1, 4, "mid", 2),
-                                         (2, 2, "small", 1)])
+                                         (2, 2, "tiny", 1)])
 def test_pp_swap_and_logits(tp, pp, name, D):
     M = need_gpu()
     d = opt_dims(name)
