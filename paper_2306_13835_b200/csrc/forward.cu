@@ -512,9 +512,13 @@ int fwd_reduce_ln(const FwdShape& s, int M, const float* const* peer_partials, i
 
 // Route one GEMM to the tcgen05/TMA kernel (bf16, M <= 256) or the SIMT weight-streaming kernel
 // (fp32 parity mode: true fp32 FMA, no TF32).
+// The tcgen05 kernel takes up to 256 token rows per launch (MMA N <= 256); more rows run as
+// consecutive launches over 256-row chunks of the same GEMM (each chunk re-streams the weights,
+// still far ahead of the SIMT kernel). The split-K decomposition depends on (N, K) only, so a
+// token's result does not depend on which chunk or chunk size it falls in: batch-invariant.
 static bool use_tc(const FwdShape& s, int M, int K) {
     if (s.dtype != MPSW_BF16 || s.gemm_impl == 1) return false;
-    return tc_supported(M, K);
+    return tc_supported(std::min(M, 256), K);
 }
 
 static void run_gemm(const FwdShape& s, int epi, GemmArgs& g, const FwdWorkspace& ws, const int32_t* row_of_m,
@@ -531,11 +535,17 @@ static void run_gemm(const FwdShape& s, int epi, GemmArgs& g, const FwdWorkspace
             tiles += (N[i] + 127) / 128;
         }
         // the split-K partials and tile counters live in the rank's workspace: never overrun them
-        const int Mp = std::max(16, (g.M + 15) / 16 * 16);
+        const int Mp = std::max(16, (std::min(g.M, 256) + 15) / 16 * 16);
         if (tc_partial_floats(tiles * 128, g.K, Mp) > ws.tc_partial_cap || tiles > ws.tc_counters_cap)
             throw Error(MPSW_EINVARIANT, "tcgen05 GEMM workspace too small for this shape");
-        tc_gemm(W, bias, N, sc, col0, g.nseg, g.A, s.max_rows, g.M, g.K, epi, g.out, g.ldo, row_of_m, ws.tc_partial,
-                ws.tc_counters, st);
+        const size_t aes = s.dtype == MPSW_BF16 ? 2 : 4, oes = epi == EPI_F32 ? 4 : aes;
+        for (int m0 = 0; m0 < g.M; m0 += 256) {
+            const int mc = std::min(256, g.M - m0);
+            const void* A = (const uint8_t*)g.A + (size_t)m0 * g.lda * aes;
+            void* out = row_of_m ? g.out : (void*)((uint8_t*)g.out + (size_t)m0 * g.ldo * oes);
+            tc_gemm(W, bias, N, sc, col0, g.nseg, A, s.max_rows - m0, mc, g.K, epi, out, g.ldo,
+                    row_of_m ? row_of_m + m0 : nullptr, ws.tc_partial, ws.tc_counters, st);
+        }
         return;
     }
     launch_gemm(s.dtype, epi, g, st);

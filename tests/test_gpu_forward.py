@@ -172,3 +172,33 @@ def test_full_size_opt1_3b_tp2_vs_oracle():
     for t, y in zip(toks, outs):
         PU.assert_logits(y, forward.forward_bf16_emulated(d, W, t[None])[0], forward.forward_exact(d, W, t[None])[0],
                          tag="opt-1.3b tp2 full size")
+
+
+def test_rows_beyond_256_run_in_tcgen05_chunks():
+    """M > 256 token rows (40 requests x 8 tokens = 320 in one batch) run through the tcgen05
+    kernel in 256-row chunks (no SIMT fallback): logits vs both oracles, and a request whose rows
+    fall in the second chunk is bitwise equal to the same request run alone (batch invariance
+    across chunk boundaries)."""
+    M = need_gpu()
+    d = opt_dims("mid")
+    toks = [request_tokens(15, 0, i, 8, d.vocab) for i in range(40)]
+    S_ = layout.shard_bytes(d, 1)
+    with M.Ctx(device_ids=(0,), budget=S_ + 4096, max_batch=40, max_tokens=8) as ctx:
+        m = ctx.register_model(d)
+        ctx.synth_fill(m, 33)
+        ctx.wait(ctx.swap_in(m))
+        rid0, y0 = ctx.request(m, toks[0])          # occupies the engine while the rest queue up
+        rids = [ctx.request(m, t) for t in toks[1:]]
+        ctx.wait_request(rid0, 120)
+        for rid, _ in rids:
+            ctx.wait_request(rid, 120)
+        st = ctx.stats()
+        outs = [y0] + [y for _, y in rids]
+        rid, alone = ctx.request(m, toks[37])
+        ctx.wait_request(rid, 120)
+    assert st["batches"] == 2                        # the 39 queued requests went in one M = 312 batch
+    assert np.array_equal(alone, outs[37])
+    W = layout.full_tensors(d, 33)
+    for i in (1, 20, 33, 39):
+        PU.assert_logits(outs[i], forward.forward_bf16_emulated(d, W, toks[i][None])[0],
+                         forward.forward_exact(d, W, toks[i][None])[0], tag="mid M>256")
