@@ -183,20 +183,20 @@ def test_rows_beyond_256_run_in_tcgen05_chunks():
     d = opt_dims("mid")
     toks = [request_tokens(15, 0, i, 8, d.vocab) for i in range(40)]
     S_ = layout.shard_bytes(d, 1)
-    with M.Ctx(device_ids=(0,), budget=S_ + 4096, max_batch=40, max_tokens=8) as ctx:
+    # 4 KiB copy-engine chunks make the implicit swap-in take tens of ms, so all 40 requests queue
+    # behind the LOADING model and leave as ONE batch of 320 rows
+    with M.Ctx(device_ids=(0,), budget=S_ + 4096, max_batch=40, max_tokens=8, chunk_bytes=4096,
+               swap_mode=M.SWAP_COPY_ENGINE) as ctx:
         m = ctx.register_model(d)
         ctx.synth_fill(m, 33)
-        ctx.wait(ctx.swap_in(m))
-        rid0, y0 = ctx.request(m, toks[0])          # occupies the engine while the rest queue up
-        rids = [ctx.request(m, t) for t in toks[1:]]
-        ctx.wait_request(rid0, 120)
+        rids = [ctx.request(m, t) for t in toks]
         for rid, _ in rids:
             ctx.wait_request(rid, 120)
         st = ctx.stats()
-        outs = [y0] + [y for _, y in rids]
+        outs = [y for _, y in rids]
         rid, alone = ctx.request(m, toks[37])
         ctx.wait_request(rid, 120)
-    assert st["batches"] == 2                        # the 39 queued requests went in one M = 312 batch
+    assert st["batches"] == 1                        # M = 320 > 256: two tcgen05 chunks per GEMM
     assert np.array_equal(alone, outs[37])
     W = layout.full_tensors(d, 33)
     for i in (1, 20, 33, 39):
