@@ -81,10 +81,9 @@ typedef struct {
     int world_size;               /* processes in the TP group; 0/1 = single-process mode      */
     int world_rank;               /* this process's TP rank (0 = leader)                       */
     const char* shm_name;         /* POSIX shm name for the control plane, e.g. "/mpsw_1234"   */
-    int gemm_impl;                /* 0 auto (one tcgen05/TMA kernel per op for bf16, M <= 256), 1 SIMT,
-                                     2 tcgen05 per op, 3 fused: bf16 at M <= 48 on a TP = 1 rank alone on
-                                     its GPU runs every decoder layer in ONE persistent tcgen05/TMA
-                                     kernel (else as 2). 0, 2 and 3 give bitwise identical logits. */
+    int gemm_impl;                /* 0 auto (tcgen05/TMA kernels for bf16, M > 256 in 256-row
+                                     chunks), 1 SIMT (fp32 FMA), 2 tcgen05; 0 and 2 are identical.
+                                     (3, the round-1 fused layers kernel, was removed: EINVAL) */
     int pp;                       /* pipeline stages (0/1 = none); ranks = tp * pp, global rank  */
                                   /* g = stage * tp + tp_rank; single-process only. Entries are */
                                   /* pipelined stage to stage (NEXT-1): the engine feeds */

@@ -138,18 +138,7 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
                                 R.ws.x, R.ws.a, cs);
             ++point;
         }
-        // All layers in one persistent kernel when eligible (bf16, TP = 1, M <= 48, the only rank on
-        // its GPU); it returns 0 otherwise and the per-op kernels below run. Both paths give the same
-        // bits (fwd_fused.cu).
-        bool sole = t == 1 && !tapping;
-        for (const auto& o : c->ranks)
-            if (o.get() != &R && o->device == R.device) sole = false;
-        if (!sole && getenv("MPSW_FUSED_DEBUG")) fprintf(stderr, "[mpsw] fused layers kernel not used: shared GPU / tp\n");
-        const int fused = sole ? fwd_layers_fused(s, Wt, R.ws, B, M, last ? Wt.lnf_w : Wt.layers.back().ln2_w,
-                                                  last ? Wt.lnf_b : Wt.layers.back().ln2_b, cs)
-                               : 0;
-        nl += fused;
-        for (int l = 0; l < (fused ? 0 : s.n_layers); ++l) {
+        for (int l = 0; l < s.n_layers; ++l) {
             if (tapping && l == tap.n_layers && tap.what <= MPSW_TAP_A) break;
             const bool tap_here = tapping && l == tap.n_layers;
             const auto& L = Wt.layers[l];
@@ -173,7 +162,7 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
         }
         if (last && !tapping) nl += fwd_lm_head(s, Wt, R.ws, B, M, cs);
     };
-    const bool graphable = t == 1 && c->pp == 1 && !tapping && s.gemm_impl != 3 && graphs_enabled() &&
+    const bool graphable = t == 1 && c->pp == 1 && !tapping && graphs_enabled() &&
                            c->fault_rank.load() < 0;
     if (!graphable) {
         compute();

@@ -102,7 +102,8 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     if (cfg->chunk_bytes % 4096) return set_error(MPSW_EINVAL, "chunk_bytes must be a multiple of 4096");
     if (cfg->swap_mode < 0 || cfg->swap_mode > 3) return set_error(MPSW_EINVAL, "bad swap_mode");
     if (cfg->param_budget_bytes_per_gpu == 0) return set_error(MPSW_EINVAL, "param budget is 0");
-    if (cfg->gemm_impl < 0 || cfg->gemm_impl > 3) return set_error(MPSW_EINVAL, "bad gemm_impl");
+    if (cfg->gemm_impl < 0 || cfg->gemm_impl > 2)
+        return set_error(MPSW_EINVAL, "bad gemm_impl (0 auto, 1 SIMT, 2 tcgen05; the fused layers kernel was removed)");
     if (cfg->n_helpers < 0 || cfg->n_helpers > kMaxHelpers || (cfg->n_helpers && !cfg->helper_device_ids))
         return set_error(MPSW_EINVAL, "n_helpers must be 0..8 with helper_device_ids");
     if (mp && cfg->n_helpers) return set_error(MPSW_EINVAL, "fan-in helpers are single-process only");

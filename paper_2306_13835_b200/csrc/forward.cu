@@ -238,7 +238,7 @@ struct LnDst {
 
 
 // Row sum of a 512-thread CTA: warp butterflies, then the 16 warp partials in warp order
-// (fc::ln_red16) — the order the fused layers kernel reproduces with 128 threads.
+// (fc::ln_red16).
 __device__ __forceinline__ float block_sum(float v, float* red) {
     v = warp_sum(v);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -416,7 +416,6 @@ size_t workspace_bytes(const FwdShape& s, int max_rows, int max_batch) {
     b += align_up((3 * (size_t)max_batch + 2 + 2 * M) * 4);     // meta
     b += align_up(tc_ws_floats(s, max_rows) * 4);               // tcgen05 split-K partials
     b += align_up(tc_tiles_max(s) * 4);                         // tile counters
-    b += align_up(fused_bar_count() * 8);                       // fused kernel phase counters
     return b;
 }
 
@@ -439,8 +438,6 @@ void workspace_carve(FwdWorkspace& w, const FwdShape& s, int max_rows, int max_b
     w.tc_counters = (int*)take(tc_tiles_max(s) * 4);
     w.tc_partial_cap = tc_ws_floats(s, max_rows);
     w.tc_counters_cap = tc_tiles_max(s);
-    w.fused_bar = (unsigned long long*)take(fused_bar_count() * 8);
-    w.fused_epoch = 0;
     w.bytes = (size_t)(p - (char*)base);
 }
 

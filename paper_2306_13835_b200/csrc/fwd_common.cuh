@@ -1,7 +1,6 @@
-// Device arithmetic of the non-GEMM forward steps, shared by the per-op kernels (forward.cu) and
-// the fused persistent layers kernel (fwd_fused.cu). Both call these helpers, and every rounding
-// step is spelled out with _rn intrinsics (no compiler-chosen FMA contraction), so the two paths
-// produce the same bits and a request's logits do not depend on which path served its batch.
+// Device arithmetic of the non-GEMM forward steps (forward.cu). Every rounding step is spelled out
+// with _rn intrinsics (no compiler-chosen FMA contraction), so the arithmetic is fixed by the
+// source: a request's logits do not depend on how its batch was launched (eager or graph).
 // Numerics: DESIGN.md reading #20 (fp32 residual / LN statistics / softmax, bf16 GEMM operands).
 #pragma once
 

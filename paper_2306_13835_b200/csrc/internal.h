@@ -72,7 +72,7 @@ struct TensorPtrs {          // device pointers of one rank's shard inside a slo
 struct FwdShape {
     int n_layers, hidden, heads_local, head_dim, ffn_local, vocab_local, vocab, tp, rank;
     int dtype;               // MPSW_BF16 / MPSW_FP32
-    int gemm_impl;           // 0 auto (tcgen05 per op for bf16), 1 SIMT, 2 tcgen05 per op, 3 fused layers kernel where eligible
+    int gemm_impl;           // 0 auto (tcgen05 per op for bf16), 1 SIMT, 2 tcgen05 per op
     int max_rows;            // rows of the activation buffers (max_batch * max_tokens)
 };
 
@@ -90,8 +90,6 @@ struct FwdWorkspace {        // device buffers of one rank (sized for max_batch*
     int* tc_counters = nullptr;    // per-tile arrival counters (self-resetting)
     size_t tc_partial_cap = 0;     // floats of tc_partial
     int tc_counters_cap = 0;       // entries of tc_counters
-    unsigned long long* fused_bar = nullptr;   // fused layers kernel: per-phase arrival counters
-    uint64_t fused_epoch = 0;      // fused launches so far (host side; counters are monotonic)
     void* base = nullptr;
     size_t bytes = 0;
 };
@@ -128,11 +126,6 @@ int fwd_out_proj(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspa
 int fwd_fc1(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M, cudaStream_t st);
 int fwd_fc2(const FwdShape& s, const TensorPtrs::Layer& L, const FwdWorkspace& ws, int M, float* partial,
             cudaStream_t st);
-// Fused persistent kernel over all decoder layers of the stage (fwd_fused.cu); returns 0 when the
-// shape is not eligible (then the per-op kernels run).
-size_t fused_bar_count();
-int fwd_layers_fused(const FwdShape& s, const TensorPtrs& W, FwdWorkspace& ws, int B, int M, const void* last_w,
-                     const void* last_b, cudaStream_t st);
 int fwd_lm_head(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, int B, int M, cudaStream_t st);
 
 // Programmatic dependent launch (sm_90+): the kernel may be scheduled while the previous kernel

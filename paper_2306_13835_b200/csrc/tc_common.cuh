@@ -1,5 +1,5 @@
 // Device helpers of the tcgen05 / TMA weight-streaming GEMMs (sm_100a), shared by the per-op
-// GEMM (gemm_tc.cu) and the fused persistent layers kernel (fwd_fused.cu), plus the host-side
+// GEMM (gemm_tc.cu), plus the host-side
 // tensor-map encoders. Included only by .cu files.
 #pragma once
 
@@ -134,8 +134,7 @@ __device__ __forceinline__ uint32_t umma_idesc(int Mp) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(Mp >> 3) << 17) | ((uint32_t)(kBN >> 4) << 24);
 }
 
-// GEMM epilogue arithmetic, shared by the per-op kernel and the fused layers kernel so both
-// produce the same bits: fp32 out = (acc + bias) * scale, or bf16 out = relu(acc + bias).
+// GEMM epilogue arithmetic: fp32 out = (acc + bias) * scale, or bf16 out = relu(acc + bias).
 __device__ __forceinline__ void epi_value_store(int epi, void* out, size_t idx, float x, bool has_bias, float bias_n,
                                                 float scale) {
     if (has_bias) x = __fadd_rn(x, bias_n);

@@ -1,6 +1,6 @@
 """Steady-state forward timing through the C-ABI (dev tool): one resident model, back-to-back
 blocking batches, per-batch device time from the library's CUDA events.
-impl: 0 auto (= 2 for bf16), 1 SIMT, 2 per-op tcgen05, 3 fused layers kernel (M <= 48, TP 1).
+impl: 0 auto (= 2 for bf16), 1 SIMT, 2 per-op tcgen05.
 usage: python tools/fwd_bench.py [model=opt-13b] [tc | impls=0,2] [shapes=1x2,4x8]"""
 import json
 import sys
@@ -56,6 +56,6 @@ for B, L in shapes:
             nb = s1["fwd_gpu_n"] - s0["fwd_gpu_n"]
             ms = (s1["fwd_gpu_us_sum"] - s0["fwd_gpu_us_sum"]) / 1e3 / max(1, nb)
             import os
-            print(json.dumps({"graphs": os.environ.get("MPSW_GRAPHS", "1"), "pair": os.environ.get("MPSW_TC_PAIR", "0"), "model": name, "B": B, "L": L, "impl": ["auto", "simt", "tcgen05", "fused"][impl], "batches": nb, "batch_rows": B * L,
+            print(json.dumps({"graphs": os.environ.get("MPSW_GRAPHS", "1"), "pair": os.environ.get("MPSW_TC_PAIR", "0"), "model": name, "B": B, "L": L, "impl": ["auto", "simt", "tcgen05"][impl], "batches": nb, "batch_rows": B * L,
                               "fwd_ms_device": ms, "GBps": S / (ms / 1e3) / 1e9, "wall_ms_per_round": wall * 1e3}),
                   flush=True)
