@@ -101,6 +101,9 @@ typedef struct {
                                   /* is in flight (NEXT-3, reading #29); never evicts  */
     int pp_broadcast;             /* pp > 1 ablation: 1 = the engine hands every entry to every  */
                                   /* worker at once (the design P:96 rules out); needs D = 1     */
+    int victim_policy;            /* no free range for a load: 0 = evict LRU victims until a     */
+                                  /* first fit appears (reading #28); 1 = the window that evicts */
+                                  /* the fewest bytes (knapsack, reading #30, NEXT-4)            */
 } mpsw_config;
 
 typedef struct {

@@ -48,6 +48,7 @@ class EngineConfig:
     cap: int = None             # region bytes per rank (reading #28); None: k_slots unit slots
     sizes: list = None          # placement bytes per model; None: 1 each
     prefetch: bool = False      # reading #29
+    victim_policy: int = 0      # reading #28 (0: LRU prefix, first fit) or #30 (1: min-cost window)
 
     def region(self):
         return self.k_slots if self.cap is None else self.cap
@@ -60,7 +61,7 @@ def config_from_trace(cfg):
     """EngineConfig from the {"cfg": ...} header line of the engine's trace (mpsw_trace_dump)."""
     c = cfg["cfg"]
     return EngineConfig(len(c["sizes"]), 0, c["acks"], c["max_batch"], c["D"], cap=c["cap"], sizes=list(c["sizes"]),
-                        prefetch=bool(c.get("prefetch", False)))
+                        prefetch=bool(c.get("prefetch", False)), victim_policy=int(c.get("victim_policy", 0)))
 
 
 def read_trace(path):
@@ -144,6 +145,28 @@ class Engine:
             o = max(o, hi)
         return o if self.cfg.region() - o >= need else None
 
+    def _min_cost_window(self, need, vics):
+        """Reading #30 (victim_policy 1): among windows [o, o + need) inside the region whose
+        every overlapping model is an eligible victim, the one minimising (bytes evicted, number
+        of victims, the newest victim key, o); a victim key is (queue non-empty, last_use, model).
+        Windows starting at 0 or at the end of an owned range suffice: sliding any feasible
+        window left to the nearest such start only drops overlapped ranges. None if no window is
+        feasible. Returns (o, set of victims)."""
+        key = lambda v: (1 if self.queue[v] else 0, self.last_use[v], v)
+        owned = [(self.off_of[v], self.off_of[v] + self.cfg.size(v), v) for v in range(self.cfg.n_models)
+                 if self.off_of[v] is not None]
+        best = None
+        for o in sorted({0} | {hi for _, hi, _ in owned}):
+            if o + need > self.cfg.region():
+                continue
+            over = [v for lo, hi, v in owned if lo < o + need and o < hi]
+            if any(v not in vics for v in over):
+                continue
+            cost = (sum(self.cfg.size(v) for v in over), len(over), max(key(v) for v in over) if over else (), o)
+            if best is None or cost < best[0]:
+                best = (cost, o, set(over))
+        return None if best is None else (best[1], best[2])
+
     # ---- SCHEDULE (P:74, P:114) ----------------------------------------------------------
     def schedule(self, now, out):
         blocked = set()
@@ -179,6 +202,16 @@ class Engine:
                                    if self.state[v] == RESIDENT and self.outstanding[v] == 0
                                    and (not self.queue[v] or self._head_key(v) > hk)),
                                   key=lambda v: (1 if self.queue[v] else 0, self.last_use[v], v))
+                    if self.cfg.victim_policy == 1:
+                        w = self._min_cost_window(need, vics)
+                        if w is not None:
+                            o, ws = w
+                            for v in vics:                       # evicted in victim-key order
+                                if v in ws:
+                                    self._offload(v, out)
+                            self._load(m, o, out)
+                        blocked.add(m)
+                        continue
                     for j in range(1, len(vics) + 1):
                         o = self._first_fit(need, set(vics[:j]))
                         if o is None:

@@ -102,6 +102,7 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     if (cfg->chunk_bytes % 4096) return set_error(MPSW_EINVAL, "chunk_bytes must be a multiple of 4096");
     if (cfg->swap_mode < 0 || cfg->swap_mode > 3) return set_error(MPSW_EINVAL, "bad swap_mode");
     if (cfg->param_budget_bytes_per_gpu == 0) return set_error(MPSW_EINVAL, "param budget is 0");
+    if (cfg->victim_policy < 0 || cfg->victim_policy > 1) return set_error(MPSW_EINVAL, "victim_policy must be 0 or 1");
     if (cfg->gemm_impl < 0 || cfg->gemm_impl > 2)
         return set_error(MPSW_EINVAL, "bad gemm_impl (0 auto, 1 SIMT, 2 tcgen05; the fused layers kernel was removed)");
     if (cfg->n_helpers < 0 || cfg->n_helpers > kMaxHelpers || (cfg->n_helpers && !cfg->helper_device_ids))
@@ -146,6 +147,7 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     c->sm.max_batch = cfg->max_batch;
     c->sm.D = c->D;
     c->sm.prefetch = cfg->prefetch != 0;
+    c->sm.victim_policy = cfg->victim_policy;
     for (auto& b : c->stage_barrier) b.n = mp ? 1 : c->tp;
     c->models.reserve(kMaxModels);
     for (auto& x : c->local_of) x = -1;
@@ -745,7 +747,8 @@ mpsw_status mpsw_trace_dump(mpsw_ctx* c, const char* path) {
         f << "{\"cfg\":{\"cap\":" << c->sm.cap << ",\"sizes\":[";
         for (int m = 0; m < c->sm.n_models; ++m) f << (m ? "," : "") << c->sm.size[m];
         f << "],\"acks\":" << c->sm.tp << ",\"max_batch\":" << c->sm.max_batch << ",\"D\":" << c->sm.D
-          << ",\"prefetch\":" << (c->sm.prefetch ? "true" : "false") << "}}\n";
+          << ",\"prefetch\":" << (c->sm.prefetch ? "true" : "false") << ",\"victim_policy\":" << c->sm.victim_policy
+          << "}}\n";
     }
     for (const auto& l : c->trace_lines) f << l << "\n";
     return MPSW_OK;

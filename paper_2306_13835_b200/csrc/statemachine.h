@@ -51,6 +51,7 @@ struct StateMachine {
     // prefetch (NEXT-3, reading #29): the last kHist arrivals, last arrival time per model
     static constexpr int kHist = 32;
     bool prefetch = false;
+    int victim_policy = 0;   // 0: LRU prefix + first fit (reading #28); 1: min-cost window (reading #30)
     std::deque<int> recent;
     std::vector<double> last_arr;
 
@@ -82,6 +83,69 @@ struct StateMachine {
         return cap >= cur + need ? (int64_t)cur : -1;
     }
     int64_t free_range(int m) const { return first_fit(size[m], std::vector<char>(n_models, 0)); }
+
+    // Reading #30 (victim_policy 1, NEXT-4 knapsack): among windows [o, o + need) inside the region
+    // whose every overlapping model is an eligible victim, take the one minimising (bytes evicted,
+    // number of victims, the newest victim key, o) — a victim key is (queue non-empty, last_use,
+    // model). Windows starting at 0 or at the end of an owned range suffice (sliding a feasible
+    // window left to the nearest such start only drops overlapped ranges). The overlapped victims
+    // are offloaded in victim-key order (vics is sorted by it), then m is loaded. No feasible
+    // window: nothing is emitted (the requester defers).
+    void min_cost_window(int m, const std::vector<int>& vics, std::vector<Decision>& out) {
+        const uint64_t need = size[m];
+        std::vector<char> elig(n_models, 0);
+        for (int v : vics) elig[v] = 1;
+        std::vector<uint64_t> starts{0};
+        for (int v = 0; v < n_models; ++v)
+            if (off_of[v] >= 0) starts.push_back((uint64_t)off_of[v] + size[v]);
+        std::sort(starts.begin(), starts.end());
+        starts.erase(std::unique(starts.begin(), starts.end()), starts.end());
+        bool found = false;
+        uint64_t best_bytes = 0, best_o = 0;
+        int best_n = 0;
+        int best_key_m = -1;      // model whose key is the window's newest victim key
+        std::vector<char> best_set;
+        auto key_less = [&](int a, int b) {
+            const int qa = queue[a].empty() ? 0 : 1, qb = queue[b].empty() ? 0 : 1;
+            if (qa != qb) return qa < qb;
+            if (last_use[a] != last_use[b]) return last_use[a] < last_use[b];
+            return a < b;
+        };
+        for (uint64_t o : starts) {
+            if (o + need > cap) continue;
+            std::vector<char> set(n_models, 0);
+            uint64_t bytes = 0;
+            int n = 0, newest = -1;
+            bool ok = true;
+            for (int v = 0; v < n_models && ok; ++v) {
+                if (off_of[v] < 0) continue;
+                const uint64_t lo = (uint64_t)off_of[v], hi = lo + size[v];
+                if (!(lo < o + need && o < hi)) continue;
+                if (!elig[v]) ok = false;
+                set[v] = 1;
+                bytes += size[v];
+                ++n;
+                if (newest < 0 || key_less(newest, v)) newest = v;
+            }
+            if (!ok) continue;
+            bool better = !found;
+            if (found) {
+                if (bytes != best_bytes) better = bytes < best_bytes;
+                else if (n != best_n) better = n < best_n;
+                else if (newest != best_key_m) better = key_less(newest, best_key_m);
+                else better = o < best_o;
+            }
+            if (better) {
+                found = true;
+                best_bytes = bytes, best_n = n, best_key_m = newest, best_o = o;
+                best_set = set;
+            }
+        }
+        if (!found) return;
+        for (int v : vics)
+            if (best_set[v]) offload(v, out);
+        load(m, best_o, out);
+    }
     void load(int m, uint64_t o, std::vector<Decision>& out) {
         Decision d{0, next_id++, m, o};
         off_of[m] = (int64_t)o;
@@ -140,6 +204,11 @@ struct StateMachine {
                         vics.push_back(v);
                     }
                     std::sort(vics.begin(), vics.end(), key_less);
+                    if (victim_policy == 1) {
+                        min_cost_window(m, vics, out);
+                        blocked[m] = 1;
+                        continue;
+                    }
                     std::vector<char> skip(n_models, 0);
                     for (int v : vics) {
                         skip[v] = 1;

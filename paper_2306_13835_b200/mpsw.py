@@ -39,7 +39,8 @@ class Config(C.Structure):
                 ("writeback", C.c_int), ("trace", C.c_int), ("zc_ctas", C.c_int),
                 ("world_size", C.c_int), ("world_rank", C.c_int), ("shm_name", C.c_char_p),
                 ("gemm_impl", C.c_int), ("pp", C.c_int), ("helper_device_ids", C.POINTER(C.c_int)),
-                ("n_helpers", C.c_int), ("max_dims", OptDims), ("prefetch", C.c_int), ("pp_broadcast", C.c_int)]
+                ("n_helpers", C.c_int), ("max_dims", OptDims), ("prefetch", C.c_int), ("pp_broadcast", C.c_int),
+                ("victim_policy", C.c_int)]
 
 
 class TensorDesc(C.Structure):
@@ -156,7 +157,7 @@ class Ctx:
     def __init__(self, device_ids=(0,), budget=1 << 30, max_batch=8, max_tokens=8, dtype=BF16,
                  max_inflight=1, swap_mode=SWAP_AUTO, chunk_bytes=0, writeback=1, trace=0, zc_ctas=0,
                  world_size=1, world_rank=0, shm_name=None, gemm_impl=0, pp=1, helper_device_ids=(),
-                 max_dims=None, prefetch=0, pp_broadcast=0):
+                 max_dims=None, prefetch=0, pp_broadcast=0, victim_policy=0):
         """Single-process: one ctx over len(device_ids) = tp * pp ranks (global rank
         g = stage * tp + tp_rank). Multi-process (world_size > 1): device_ids = (this process's
         GPU,), rank world_rank of a TP group of world_size. max_dims: the largest model shape the
@@ -175,7 +176,7 @@ class Ctx:
                      self._shm, gemm_impl, pp,
                      (C.c_int * max(1, len(helper_device_ids)))(*helper_device_ids) if helper_device_ids else None,
                      len(helper_device_ids), dims_of(max_dims) if max_dims is not None else OptDims(), prefetch,
-                     pp_broadcast)
+                     pp_broadcast, victim_policy)
         h = _P()
         _check(lib().mpsw_init(C.byref(cfg), C.byref(h)))
         self.h = h

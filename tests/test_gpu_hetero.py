@@ -26,9 +26,11 @@ def placement_bytes(d, tp):
     return (layout.shard_bytes(d, tp) + 4095) // 4096 * 4096
 
 
-@pytest.mark.parametrize("tp,writeback,mode,prefetch", [(1, 0, 0, 0), (1, 1, 1, 1), (2, 1, 1, 0), (2, 0, 2, 1),
-                                                        (1, 0, 0, 1)])
-def test_heterogeneous_models(tmp_path, tp, writeback, mode, prefetch):
+# vp: victim_policy (0: LRU prefix + first fit, reading #28; 1: minimum-cost window, reading #30)
+@pytest.mark.parametrize("tp,writeback,mode,prefetch,vp", [(1, 0, 0, 0, 0), (1, 1, 1, 1, 0), (2, 1, 1, 0, 0),
+                                                           (2, 0, 2, 1, 0), (1, 0, 0, 1, 0), (1, 1, 1, 0, 1),
+                                                           (2, 0, 0, 1, 1)])
+def test_heterogeneous_models(tmp_path, tp, writeback, mode, prefetch, vp):
     M = need_gpu()
     sizes = [placement_bytes(d, tp) for d in DIMS]
     budget = sizes[0] + sizes[1] + sizes[5] + 3 * 4096        # one mid + two smaller ones
@@ -38,7 +40,8 @@ def test_heterogeneous_models(tmp_path, tp, writeback, mode, prefetch):
     rnd = random.Random(tp * 100 + writeback * 10 + mode)
     outs = []
     with M.Ctx(device_ids=(0,) * tp, budget=budget, max_batch=4, max_tokens=8, trace=1, writeback=writeback,
-               swap_mode=mode, chunk_bytes=1 << 20, max_dims=opt_dims("mid"), prefetch=prefetch) as ctx:
+               swap_mode=mode, chunk_bytes=1 << 20, max_dims=opt_dims("mid"), prefetch=prefetch,
+               victim_policy=vp) as ctx:
         ids = [ctx.register_model(d) for d in DIMS]
         for m in ids:
             ctx.synth_fill(m, seeds[m])
@@ -65,7 +68,7 @@ def test_heterogeneous_models(tmp_path, tp, writeback, mode, prefetch):
         host = {m: [ctx.checksum(ids[m], r, on_device=False) for r in range(tp)] for m in range(len(DIMS))}
     cfg, evs, decs = S.read_trace(p)
     assert cfg.sizes == sizes and cfg.cap == budget // 4096 * 4096 and st["region_bytes"] == cfg.cap
-    assert cfg.prefetch == bool(prefetch)
+    assert cfg.prefetch == bool(prefetch) and cfg.victim_policy == vp
     rdecs, _ = S.replay(cfg, evs)
     assert rdecs == decs
     n_pf = sum(1 for d in decs if d.get("prefetch"))

@@ -300,3 +300,101 @@ def test_prefetch_random_traces(seed):
     for m in range(n):
         mine = [r for r in done if rid_model[r] == m]
         assert mine == sorted(mine)
+
+
+# ---- reading #30: victim_policy 1, the minimum-cost window (NEXT-4 knapsack) -------------------
+def cfg1(sizes, cap, mb=4, D=1, tp=1):
+    return S.EngineConfig(len(sizes), 0, tp, mb, D, cap=cap, sizes=list(sizes), victim_policy=1)
+
+
+def test_min_cost_window_worked_example():
+    # cap 10: A(4) loads at 0, C(4) at 4, B(2) at 8 (first fit), LRU order A, C, B. D(2) finds no
+    # free range: the LRU-prefix policy (#28) evicts A (the oldest, 4 bytes) and loads D at 0; the
+    # min-cost window (#30) evicts only B (2 bytes) and loads D at 8
+    for pol, want in ((0, [("offload", 0, 0), ("load", 3, 0)]), (1, [("offload", 1, 8), ("load", 3, 8)])):
+        e = S.Engine(S.EngineConfig(4, 0, 1, 4, 1, cap=10, sizes=[4, 2, 4, 2], victim_policy=pol))
+        for t, m in ((1.0, 0), (2.0, 2), (3.0, 1)):
+            drive_resident(e, m, t)
+        assert (e.off_of[0], e.off_of[2], e.off_of[1]) == (0, 4, 8)
+        assert swaps(drive_resident(e, 3, 4.0)) == want, pol
+
+
+def brute_window(before_off, sizes, cap, m, eligible, key):
+    """Every integer offset o (not only the candidate starts): the feasible window with the least
+    (bytes evicted, victims, newest victim key, o)."""
+    best = None
+    for o in range(cap - sizes[m] + 1):
+        over = [w for w, lo in before_off.items() if lo < o + sizes[m] and o < lo + sizes[w]]
+        if any(w not in eligible for w in over):
+            continue
+        cost = (sum(sizes[w] for w in over), len(over), max((key(w) for w in over), default=()), o)
+        if best is None or cost < best[0]:
+            best = (cost, o, over)
+    return best
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_min_cost_window_vs_brute_force(seed):
+    """Blocking requests over random heterogeneous sizes: every decision of victim_policy 1 equals
+    the brute force over all integer offsets (so the candidate-start restriction loses nothing),
+    offloads in victim-key order, invariants after every event."""
+    rng = random.Random(7000 + seed)
+    n = rng.randint(2, 6)
+    sizes = [rng.randint(1, 5) for _ in range(n)]
+    cap = rng.randint(max(sizes), 14)
+    e = S.Engine(cfg1(sizes, cap))
+    t = 0.0
+    for _ in range(30):
+        m = rng.randrange(n)
+        t += 1.0
+        if e.state[m] == S.RESIDENT:
+            drive_resident(e, m, t)
+            continue
+        before = {w: e.off_of[w] for w in range(n) if e.off_of[w] is not None}
+        key = lambda w: (0, e.last_use[w], w)
+        elig = {w for w in range(n) if e.state[w] == S.RESIDENT and e.outstanding[w] == 0}
+        got = swaps(drive_resident(e, m, t))
+        free = brute_window(before, sizes, cap, m, set(), key)
+        if free is not None:                      # a free range exists: plain first fit
+            assert got[0] == ("load", m, free[1]), (got, free)
+            continue
+        best = brute_window(before, sizes, cap, m, elig, key)
+        assert best is not None
+        want = [("offload", w, before[w]) for w in sorted(best[2], key=key)] + [("load", m, best[1])]
+        assert got[:len(want)] == want, (sizes, cap, before, got, want)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_min_cost_window_equal_sizes_is_textbook_lru(seed):
+    """Equal sizes: every window costs one model, the newest-key tie-break picks the LRU victim,
+    so victim_policy 1 reduces to textbook LRU exactly like policy 0."""
+    rng = random.Random(9000 + seed)
+    n, k = rng.randint(2, 8), rng.randint(1, 4)
+    size = rng.randint(2, 7)
+    cap = k * size + rng.randrange(size)
+    e = S.Engine(cfg1([size] * n, cap))
+    acc = [rng.randrange(n) for _ in range(60)]
+    evicted = []
+    for i, m in enumerate(acc):
+        for d in drive_resident(e, m, float(i + 1)):
+            if d["dec"] == "offload":
+                evicted.append(d["model"])
+    assert evicted == S.textbook_lru_evictions(acc, k)
+
+
+@pytest.mark.parametrize("seed", range(15))
+def test_min_cost_window_open_loop_invariants(seed):
+    """Open-loop arrivals with random ack / completion interleaving under victim_policy 1:
+    Engine.check invariants at every step and every request completes (replay of its own
+    event log reproduces the decisions)."""
+    rng = random.Random(11000 + seed)
+    n = rng.randint(3, 6)
+    sizes = [rng.randint(1, 5) for _ in range(n)]
+    cap = rng.randint(max(sizes) + 1, 14)
+    c = cfg1(sizes, cap, mb=rng.randint(1, 3), D=rng.randint(1, 2))
+    arrivals = sorted((rng.uniform(0, 5), rid, rng.randrange(n)) for rid in range(40))
+    events, decisions, t_done, _ = S.simulate(c, S.Costs(1, 1e9, 1e9, alpha=1e-3, gamma0=2e-3),
+                                              [(rid, m, t) for t, rid, m in arrivals], token_len=2)
+    assert len(t_done) == 40
+    rdecs, _ = S.replay(c, events)
+    assert rdecs == decisions
