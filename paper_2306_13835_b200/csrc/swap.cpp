@@ -165,8 +165,10 @@ void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
             }
         }
     }
-    retire_gates(R, lo, hi);
+    // completion marker right behind the last copy; the gate bookkeeping (event destroys) comes
+    // after it, so host work never sits between the copy and its completion on the stream
     MPSW_CU(cudaEventRecord(e.ev_done[r], R.h2d));
+    retire_gates(R, lo, hi);
 }
 
 void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
