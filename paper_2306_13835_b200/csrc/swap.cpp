@@ -4,6 +4,8 @@
 #include "runtime.h"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 
 namespace mpsw {
@@ -85,6 +87,8 @@ void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
     }
     MPSW_CU(cudaEventCreate(&e.ev_start[r]));
     MPSW_CU(cudaEventCreate(&e.ev_done[r]));
+    static const bool dbg = getenv("MPSW_SWAP_DEBUG") != nullptr;
+    const auto h0 = std::chrono::steady_clock::now();
     MPSW_CU(cudaEventRecord(e.ev_start[r], R.h2d));
     // gates that already completed are skipped (a stream wait on another stream's event costs
     // tens of microseconds, which dominates small-shard swaps: DESIGN.md §8 cfg5)
@@ -168,6 +172,10 @@ void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
     // completion marker right behind the last copy; the gate bookkeeping (event destroys) comes
     // after it, so host work never sits between the copy and its completion on the stream
     MPSW_CU(cudaEventRecord(e.ev_done[r], R.h2d));
+    if (dbg)
+        fprintf(stderr, "[mpsw] load m%d rank %d: %llu B issued in %.1f us (gates %zu, zc %d, chunks %d)\n", e.model, r,
+                (unsigned long long)S, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count(),
+                evs.size(), (int)zc, n_chunks);
     retire_gates(R, lo, hi);
 }
 
