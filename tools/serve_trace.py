@@ -61,6 +61,7 @@ def main():
     ap.add_argument("--out", default="")
     ap.add_argument("--check-logits", type=int, default=-1, help="requests to check vs the oracle (-1 = auto)")
     ap.add_argument("--prefetch", type=int, default=0, help="1 = NEXT-3 prefetch policy (reading #29)")
+    ap.add_argument("--victim-policy", type=int, default=0, help="1 = minimum-cost window (reading #30)")
     args = ap.parse_args()
     P = dict(PRESETS[args.preset])
     names = P.get("models") or [P["model"]] * P["n"]
@@ -91,11 +92,11 @@ def main():
             "device_param_bytes_per_gpu": budget, "models": names, "tp": tp}}))
         sys.exit(2)
     device_ids = tuple(range(tp)) if gpus >= tp else (0,) * tp
-    res = {"preset": args.preset, "prefetch": args.prefetch, "models": names, "tp": tp, "k": P.get("k"), "budget": budget, "cv": cv,
+    res = {"preset": args.preset, "prefetch": args.prefetch, "victim_policy": args.victim_policy, "models": names, "tp": tp, "k": P.get("k"), "budget": budget, "cv": cv,
            "seed": args.seed, "requests": len(trace), "shard_bytes": sizes_r}
     t_setup = time.perf_counter()
     with M.Ctx(device_ids=device_ids, budget=budget, max_batch=P["max_batch"], max_tokens=P["L"], trace=1,
-               writeback=0, max_dims=d, prefetch=args.prefetch) as ctx:
+               writeback=0, max_dims=d, prefetch=args.prefetch, victim_policy=args.victim_policy) as ctx:
         ids = [ctx.register_model(x) for x in dims]
         for m in ids:
             ctx.synth_fill(m, 7000 + m)
@@ -130,6 +131,7 @@ def main():
         lat = lat[1:]                       # cold first load reported separately
     res["latency_s"] = metrics.summary(lat)
     res["swaps_in"] = st["swaps_in"]
+    res["h2d_bytes"] = st["h2d_bytes"]
     res["prefetches"] = st["prefetches"]
     res["swap_in_GBps_median"] = float(np.median([tp * n / (ms / 1e3) / 1e9 for ms, n in h2d])) if h2d else None
     if len(set(names)) > 1:
