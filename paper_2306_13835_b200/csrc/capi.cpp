@@ -412,7 +412,10 @@ mpsw_status mpsw_register_model(mpsw_ctx* c, const mpsw_opt_dims* dims, int tp, 
             m->fs.push_back(fwd_shape(c, *dims, *R));
             const uint64_t S = m->rank_S[R->index];
             m->arena.push_back(pin_alloc(S, R->numa));
-            if (shards && shards[R->index]) parallel_memcpy(m->arena.back().p, (const uint8_t*)shards[R->index], S);
+            if (shards && shards[R->index]) {
+                parallel_memcpy(m->arena.back().p, (const uint8_t*)shards[R->index], S);
+                flush_to_memory(m->arena.back().p, S);
+            }
         }
     } catch (...) {
         for (auto& a : m->arena) pin_free(a);

@@ -325,6 +325,7 @@ uint64_t host_mem_available();
 PinnedBuf pin_alloc(uint64_t bytes, int numa_node);
 void pin_free(PinnedBuf& b);
 void parallel_memcpy(uint8_t* dst, const uint8_t* src, uint64_t n);
+void flush_to_memory(uint8_t* p, uint64_t n);
 void* shm_map(const std::string& name, size_t bytes, bool create);
 
 // engine.cpp

@@ -5,6 +5,10 @@
 // flat_index addresses the FULL tensor, so each rank fills exactly its slice.
 #include "internal.h"
 
+namespace mpsw {
+void flush_to_memory(uint8_t* p, uint64_t n);   // store.cpp
+}
+
 #include <cmath>
 #include <cstring>
 #include <thread>
@@ -98,6 +102,7 @@ void synth_fill_arena(const mpsw_opt_dims& d, int tp, int pp, int stage, int ran
             for (size_t k; (k = next.fetch_add(1)) < tasks.size();) run_rows(tasks[k].j, es, tasks[k].r0, tasks[k].r1);
         });
     for (auto& th : pool) th.join();
+    flush_to_memory(dst, L.bytes);      // leave the arena clean in DRAM for the swap DMA (store.cpp)
 }
 
 uint64_t host_checksum(const uint8_t* p, uint64_t bytes, int threads) {

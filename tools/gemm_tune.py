@@ -24,7 +24,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
             print(json.dumps(row), flush=True)
     sys.exit(0)
 mode = sys.argv[1] if len(sys.argv) > 1 else "default"
-models = "opt-13b"
+models = "opt-13b,opt-1.3b,opt-125m" if os.environ.get("MPSW_TC_DYN") or mode == "default" else "opt-13b"
 configs = [("2", {})]
 if mode == "ext":
     configs = [("2", {"MPSW_TC_EXT_MIN": v}) for v in ("16", "32", "64", "100000")]
