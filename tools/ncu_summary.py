@@ -25,7 +25,7 @@ def main():
             continue
         name = r[ki].split("(")[0].replace("(anonymous namespace)::", "")
         v = float(r[vi].replace(",", ""))
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
         tot[name][0] += 1
         tot[name][1] += v * scale
     all_us = sum(t for _, t in tot.values())
