@@ -73,7 +73,9 @@ typedef struct {
     int max_tokens;               /* tokens per request, 1..128 (P:138 uses 2, P:166 uses 8)   */
     int dtype;                    /* MPSW_BF16 (1e-2 parity) or MPSW_FP32 (1e-5 parity)        */
     int max_inflight_batches;     /* D per TP group (reading #26); 0 => 1            */
-    int swap_mode;                /* MPSW_SWAP_*: copy engine, zero-copy kernel, auto, hybrid  */
+    int swap_mode;                /* MPSW_SWAP_*: copy engine, zero-copy kernel, hybrid, or    */
+                                  /* auto = the measured winner per shard-size bucket (the copy */
+                                  /* engine at every size once arenas are clean) */
     uint64_t chunk_bytes;         /* swap chunk c (multiple of 4096); 0 => 64 MiB              */
     int writeback;                /* 1 = offload copies the slot back to the arena      */
     int trace;                    /* 1 = record the NDJSON event/decision trace                */
@@ -150,7 +152,9 @@ mpsw_status mpsw_register_model(mpsw_ctx* ctx, const mpsw_opt_dims* dims, int tp
                                 int* model_id);
 
 /* Host pointer and size of (model, rank)'s pinned arena, for in-place filling before the
- * first swap-in. Writing it while the model is LOADING/OFFLOADING is undefined. */
+ * first swap-in. Writing it while the model is LOADING/OFFLOADING is undefined. The arena is
+ * written back from the CPU caches (clflushopt) before its next load: a copy-engine read of
+ * lines still dirty in the CPU's L3 runs at 1/3 - 1/5 of the link rate. */
 mpsw_status mpsw_model_arena(mpsw_ctx* ctx, int model_id, int rank, void** host, uint64_t* bytes);
 
 /* Input-generation helper (not the hot path): fill (model, rank)'s arena with the

@@ -412,6 +412,7 @@ mpsw_status mpsw_register_model(mpsw_ctx* c, const mpsw_opt_dims* dims, int tp, 
             m->fs.push_back(fwd_shape(c, *dims, *R));
             const uint64_t S = m->rank_S[R->index];
             m->arena.push_back(pin_alloc(S, R->numa));
+            m->arena_dirty.push_back(0);
             if (shards && shards[R->index]) {
                 parallel_memcpy(m->arena.back().p, (const uint8_t*)shards[R->index], S);
                 flush_to_memory(m->arena.back().p, S);
@@ -452,7 +453,10 @@ mpsw_status mpsw_model_arena(mpsw_ctx* c, int model_id, int rank, void** host, u
     if (model_id < 0 || model_id >= (int)c->models.size()) return set_error(MPSW_ENOENT, "unknown model");
     const int li = local_index(c, rank);
     if (li < 0) return set_error(MPSW_EINVAL, "rank out of range or not driven by this process");
-    if (host) *host = c->models[model_id]->arena[li].p;
+    if (host) {
+        *host = c->models[model_id]->arena[li].p;
+        c->models[model_id]->arena_dirty[li] = 1;   // flushed from the CPU caches before its first load
+    }
     if (bytes) *bytes = c->models[model_id]->rank_S[c->ranks[li]->index];
     return MPSW_OK;
     API_END

@@ -450,278 +450,6 @@ __global__ void __launch_bounds__(kBN) tc_fixup_kernel(TcArgs g) {
         if (m0 + j < g.M) epi_store(g, seg, n, m0 + j, acc[j], bias_n);
 }
 
-// ----------------------------------------------------------------------------- dynamic runs
-// Dynamic variant (MPSW_TC_DYN): the split is a FIXED set of runs — each tile's k-blocks cut into
-// `nr` equal runs, nr from (tiles, kb, #SMs) only — but which CTA executes which run is decided
-// at run time: persistent CTAs take the next run from a global counter. A CTA on a slow SM simply
-// takes fewer runs, so the straggler tail of equal static shares disappears. Partials live in a
-// slot per run id and a split tile is reduced in run order by its last-finishing run, so the bits
-// depend only on the fixed runs: deterministic and batch-invariant like the static split.
-struct TcDyn {
-    int nr;              // runs per tile (k-block ranges [i*kb/nr, (i+1)*kb/nr))
-    int n_runs;          // tiles * nr
-    int* run_ctr;        // [2]: next run, CTAs done (slot of this launch; self-resetting)
-};
-
-constexpr int kRunQ = 4;   // run ids handed from the producer to the MMA and epilogue warps
-
-__device__ __forceinline__ int atomic_add_relaxed(int* p, int v) {
-    int old;
-    asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-    return old;
-}
-
-__global__ void __launch_bounds__(kThreads, 1)
-tc_gemm_dyn_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant__ CUtensorMap map_w1,
-                   const __grid_constant__ CUtensorMap map_w2, const __grid_constant__ CUtensorMap map_x, TcArgs g,
-                   TcDyn dy) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    const uint32_t tile_b_bytes = (uint32_t)g.Mp * kBK * 2;
-    const int kStages = g.stages;
-    uint8_t* sa = smem;
-    uint8_t* sb = smem + kStages * kTileABytes;
-    uint64_t* full = (uint64_t*)(sb + kStages * tile_b_bytes);
-    uint64_t* empty = full + kMaxStages;
-    uint64_t* tmem_full = empty + kMaxStages;
-    uint64_t* tmem_empty = tmem_full + 2;
-    uint32_t* tmem_slot = (uint32_t*)(tmem_empty + 2);
-    __shared__ uint64_t rq_full[kRunQ], rq_empty[kRunQ];
-    __shared__ int rq[kRunQ];
-    __shared__ int s_last;
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    pdl_trigger();
-    uint32_t nbuf = 32;
-    while ((int)nbuf < g.Mp) nbuf <<= 1;
-    const int nacc = g.nacc;
-    const uint32_t ncols = (uint32_t)nacc * nbuf;
-    if (warp == 0 && lane == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w0) : "memory");
-        if (g.nseg > 1) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w1) : "memory");
-        if (g.nseg > 2) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w2) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&tmem_full[b], 1);
-            mbar_init(&tmem_empty[b], 4);
-        }
-        for (int q = 0; q < kRunQ; ++q) {
-            mbar_init(&rq_full[q], 1);
-            mbar_init(&rq_empty[q], 5);            // the MMA thread + 4 epilogue warps
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(ncols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem_base = *tmem_slot;
-    auto run_range = [&](int run, int& tile, int& k0, int& k1) {
-        tile = run / dy.nr;
-        const int i = run - tile * dy.nr;
-        k0 = (int)((int64_t)i * g.kb / dy.nr);
-        k1 = (int)((int64_t)(i + 1) * g.kb / dy.nr);
-    };
-
-    if (warp == 0) {
-        if (lane == 0) {                           // ---- producer: grabs runs, streams their units
-            auto load_w = [&](int s, int tile, int kbi) {
-                const int si = seg_of(g, tile);
-                const CUtensorMap* mw = si == 0 ? &map_w0 : (si == 1 ? &map_w1 : &map_w2);
-                tma_load_2d(sa + s * kTileABytes, mw, &full[s], kbi * kBK, (tile - g.seg[si].tile0) * kBN);
-            };
-            int run = atomic_add_relaxed(&dy.run_ctr[0], 1);
-            // the first run's first weight tiles go out before griddepcontrol.wait (PDL)
-            int t0 = 0, k0 = 0, k1 = 0, pre = 0;
-            if (run < dy.n_runs) {
-                run_range(run, t0, k0, k1);
-                pre = k1 - k0 < kStages ? k1 - k0 : kStages;
-                for (int i = 0; i < pre; ++i) {
-                    mbar_expect_tx(&full[i], kTileABytes + tile_b_bytes);
-                    load_w(i, t0, k0 + i);
-                }
-            }
-            pdl_wait();
-            for (int i = 0; i < pre; ++i) tma_load_2d(sb + i * tile_b_bytes, &map_x, &full[i], (k0 + i) * kBK, 0);
-            int s = pre % kStages, q = 0;
-            uint32_t ph = (uint32_t)(pre / kStages) & 1u, qph = 0;
-            bool first = true;
-            while (true) {
-                mbar_wait(&rq_empty[q], qph ^ 1u);
-                rq[q] = run < dy.n_runs ? run : -1;
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&rq_full[q])) : "memory");
-                if (++q == kRunQ) { q = 0; qph ^= 1u; }
-                if (run >= dy.n_runs) break;
-                int tile, a, b;
-                run_range(run, tile, a, b);
-                for (int kbi = first ? a + pre : a; kbi < b; ++kbi) {
-                    mbar_wait(&empty[s], ph ^ 1u);
-                    mbar_expect_tx(&full[s], kTileABytes + tile_b_bytes);
-                    load_w(s, tile, kbi);
-                    tma_load_2d(sb + s * tile_b_bytes, &map_x, &full[s], kbi * kBK, 0);
-                    if (++s == kStages) { s = 0; ph ^= 1u; }
-                }
-                first = false;
-                run = atomic_add_relaxed(&dy.run_ctr[0], 1);
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {                           // ---- MMA issuer: one accumulator per run
-            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(g.Mp >> 3) << 17) |
-                                   ((uint32_t)(kBN >> 4) << 24);
-            int s = 0, q = 0, nrun = 0;
-            uint32_t ph = 0, qph = 0;
-            while (true) {
-                mbar_wait(&rq_full[q], qph);
-                const int run = rq[q];
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&rq_empty[q])) : "memory");
-                if (++q == kRunQ) { q = 0; qph ^= 1u; }
-                if (run < 0) break;
-                int tile, a, b;
-                run_range(run, tile, a, b);
-                const int buf = nacc == 2 ? (nrun & 1) : 0;
-                const int use = nacc == 2 ? (nrun >> 1) : nrun;
-                mbar_wait(&tmem_empty[buf], ((uint32_t)use & 1u) ^ 1u);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t tmem_d = tmem_base + (uint32_t)buf * nbuf;
-                for (int kbi = a; kbi < b; ++kbi) {
-                    mbar_wait(&full[s], ph);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t a0 = smem_u32(sa + s * kTileABytes), b0 = smem_u32(sb + s * tile_b_bytes);
-#pragma unroll
-                    for (int kk = 0; kk < kBK / 16; ++kk)
-                        umma_bf16(tmem_d, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc,
-                                  (kbi != a || kk) ? 1u : 0u);
-                    umma_commit(&empty[s]);
-                    if (++s == kStages) { s = 0; ph ^= 1u; }
-                }
-                umma_commit(&tmem_full[buf]);
-                ++nrun;
-            }
-        }
-    } else if (warp >= 4) {                        // ---- epilogue
-        pdl_wait();
-        const int qw = warp - 4;
-        const int row = qw * 32 + lane;
-        int q = 0, nrun = 0;
-        uint32_t qph = 0;
-        while (true) {
-            mbar_wait(&rq_full[q], qph);
-            const int run = rq[q];
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&rq_empty[q])) : "memory");
-            if (++q == kRunQ) { q = 0; qph ^= 1u; }
-            if (run < 0) break;
-            int tile, a, b;
-            run_range(run, tile, a, b);
-            const int si = seg_of(g, tile);
-            const TcSeg& seg = g.seg[si];
-            const int n = (tile - seg.tile0) * kBN + row;
-            const bool nvalid = n < seg.N;
-            const float bias_n = (seg.bias && nvalid) ? __bfloat162float(seg.bias[n]) : 0.f;
-            const bool whole = dy.nr == 1;
-            float* prow = g.partial + (size_t)run * g.Mp * kBN + row;
-            const int buf = nacc == 2 ? (nrun & 1) : 0;
-            const int use = nacc == 2 ? (nrun >> 1) : nrun;
-            mbar_wait(&tmem_full[buf], (uint32_t)use & 1u);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            float v[16];
-            for (int col = 0; col < g.Mp; col += 16) {
-                tmem_ld16(tmem_base + (uint32_t)buf * nbuf + ((uint32_t)(qw * 32) << 16) + (uint32_t)col, v);
-                if (!whole) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) prow[(size_t)(col + j) * kBN] = v[j];
-                } else if (nvalid) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (col + j < g.M) epi_store(g, seg, n, col + j, v[j], bias_n);
-                }
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[buf])) : "memory");
-            ++nrun;
-            if (!whole && !g.ext_fixup) {          // the tile's last-finishing run sums all its runs in run order
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (row == 0) {
-                    int old;
-                    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(&g.counters[tile]) : "memory");
-                    s_last = old == dy.nr - 1;
-                }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (s_last) {
-                    if (nvalid) {
-                        const float* p0 = g.partial + (size_t)tile * dy.nr * g.Mp * kBN + row;
-                        for (int m0 = 0; m0 < g.M; m0 += 8) {
-                            float acc[8];
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-                            for (int i = 0; i < dy.nr; ++i) {
-                                const float* p = p0 + ((size_t)i * g.Mp + m0) * kBN;
-                                float t[8];
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) t[j] = __ldcg(p + j * kBN);
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) acc[j] += t[j];
-                            }
-#pragma unroll
-                            for (int j = 0; j < 8; ++j)
-                                if (m0 + j < g.M) epi_store(g, seg, n, m0 + j, acc[j], bias_n);
-                        }
-                    }
-                    if (row == 0) g.counters[tile] = 0;
-                }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-            }
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {                        // last CTA out resets this launch's counter slot
-        int old;
-        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(&dy.run_ctr[1]) : "memory");
-        if (old == (int)gridDim.x - 1) {
-            dy.run_ctr[0] = 0;
-            dy.run_ctr[1] = 0;
-        }
-    }
-    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
-}
-
-__global__ void __launch_bounds__(kBN) tc_fixup_dyn_kernel(TcArgs g, TcDyn dy) {
-    pdl_wait();
-    pdl_trigger();
-    const int tile = blockIdx.x, row = threadIdx.x, m0 = blockIdx.y * 16;
-    if (dy.nr == 1 || m0 >= g.M) return;
-    const TcSeg& seg = g.seg[seg_of(g, tile)];
-    const int n = (tile - seg.tile0) * kBN + row;
-    if (n >= seg.N) return;
-    const float bias_n = seg.bias ? __bfloat162float(seg.bias[n]) : 0.f;
-    float acc[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-    const float* p0 = g.partial + (size_t)tile * dy.nr * g.Mp * kBN + row;
-    for (int i = 0; i < dy.nr; ++i) {
-        const float* p = p0 + ((size_t)i * g.Mp + m0) * kBN;
-        float t[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) t[j] = __ldcg(p + j * kBN);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] += t[j];
-    }
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-        if (m0 + j < g.M) epi_store(g, seg, n, m0 + j, acc[j], bias_n);
-}
-
 // ----------------------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -875,26 +603,8 @@ static int tc_grid(int tiles, int K) {
     return (int)g_sk;
 }
 
-// Dynamic-run mode (tc_gemm_dyn_kernel): process-wide like the pair mode; MPSW_TC_DYN=1 enables.
-int tc_dyn() {
-    static int v = env_int("MPSW_TC_DYN", 0);
-    return tc_pair() ? 0 : v;
-}
-
-// Runs per tile of the dynamic mode: about q runs per CTA slot over the whole GEMM (q =
-// MPSW_TC_DYN_Q, default 3), each run at least 4 k-blocks (64 KB of weights); from (tiles, kb,
-// #SMs) only.
-static int tc_dyn_runs_per_tile(int tiles, int kb) {
-    static int q = env_int("MPSW_TC_DYN_Q", 3);
-    const int slots = tc_ctas_per_sm() * sm_count();
-    int nr = (int)((double)q * slots / tiles + 0.5);
-    nr = std::max(1, std::min(nr, std::max(1, kb / 4)));
-    return nr;
-}
-
 size_t tc_partial_floats(int n_total, int K, int Mp) {
     const int tiles = (n_total + kBN - 1) / kBN;
-    if (tc_dyn()) return (size_t)tiles * tc_dyn_runs_per_tile(tiles, (K + kBK - 1) / kBK) * kBN * Mp;
     const int kt = tc_pair() ? 2 : 1;
     return (size_t)tc_grid(tiles, K) * kt * 2 * kBN * Mp;
 }
@@ -916,11 +626,7 @@ size_t tc_smem_bytes(int Mp) {
 static unsigned long long* g_tc_trace = nullptr;   // dev instrumentation (mpsw_bench_gemm only)
 void tc_set_trace(unsigned long long* p) { g_tc_trace = p; }
 // CTAs launched for a GEMM (pair mode: 2 per worker)
-int tc_grid_for(int n_total, int K) {
-    const int tiles = (n_total + kBN - 1) / kBN;
-    if (tc_dyn()) return std::min(tc_ctas_per_sm() * sm_count(), tiles * tc_dyn_runs_per_tile(tiles, (K + kBK - 1) / kBK));
-    return tc_grid(tiles, K) * (tc_pair() ? 2 : 1);
-}
+int tc_grid_for(int n_total, int K) { return tc_grid((n_total + kBN - 1) / kBN, K) * (tc_pair() ? 2 : 1); }
 int tc_grid_tiles(int tiles, int K) { return tc_grid(tiles, K); }
 
 bool tc_supported(int M, int K) { return M >= 1 && M <= 256 && K % 8 == 0; }
@@ -997,33 +703,7 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
     int nbuf = 32;
     while (nbuf < Mp) nbuf <<= 1;
     g.nacc = 2 * nbuf * tc_ctas_per_sm() <= 512 ? 2 : 1;
-    if (tc_dyn()) {
-        // run counters: 8 slots of {next run, CTAs done} per device and worker thread, one slot
-        // per launch in rotation (a slot is reset by the last CTA of its launch, long before it
-        // is reused: at most 2-3 GEMM launches overlap through PDL)
-        thread_local std::unordered_map<int, int*> ctr_of;
-        int dev = 0;
-        MPSW_CU(cudaGetDevice(&dev));
-        int*& ctr = ctr_of[dev];
-        if (!ctr) {
-            MPSW_CU(cudaMalloc(&ctr, 16 * sizeof(int)));
-            MPSW_CU(cudaMemset(ctr, 0, 16 * sizeof(int)));
-        }
-        thread_local uint64_t epoch = 0;
-        TcDyn dy;
-        dy.nr = tc_dyn_runs_per_tile(tiles, g.kb);
-        dy.n_runs = tiles * dy.nr;
-        dy.run_ctr = ctr + 2 * (int)(epoch++ % 8);
-        g.G = std::min(tc_ctas_per_sm() * sm_count(), dy.n_runs);
-        static thread_local size_t attr_dyn = 0;
-        if (attr_dyn < smem) {
-            MPSW_CU(cudaFuncSetAttribute(tc_gemm_dyn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            MPSW_CU(cudaFuncSetAttribute(tc_gemm_dyn_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-            attr_dyn = smem;
-        }
-        launch_pdl(tc_gemm_dyn_kernel, g.G, kThreads, smem, st, m0, m1, m2, mx, g, dy);
-        if (g.ext_fixup) launch_pdl(tc_fixup_dyn_kernel, dim3(g.tiles, g.Mp / 16), kBN, 0, st, g, dy);
-    } else if (pair) {
+    if (pair) {
         launch_tc<true>(g, smem, st, m0, m1, m2, mx);
     } else {
         launch_tc<false>(g, smem, st, m0, m1, m2, mx);

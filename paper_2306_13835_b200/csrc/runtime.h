@@ -219,6 +219,7 @@ struct Model {
     mpsw_opt_dims dims;
     uint64_t size = 0;             // placement bytes: max over global ranks of round_up(S_r, 4 KiB)
     std::vector<PinnedBuf> arena;  // per LOCAL rank
+    std::vector<char> arena_dirty; // per LOCAL rank: handed out for in-place writes, not yet flushed
     std::vector<Layout> layout;    // per LOCAL rank (stage-dependent)
     std::vector<FwdShape> fs;      // per LOCAL rank
     uint64_t rank_S[kMaxRanks] = {};   // arena bytes per GLOBAL rank

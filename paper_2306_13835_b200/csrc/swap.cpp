@@ -18,10 +18,23 @@ double hybrid_frac() {
     return f;
 }
 
+// AUTO: the measured winner per shard-size bucket (tools/auto_table.py). With the
+// arenas clean in DRAM (store.cpp flush_to_memory) the copy engine wins every bucket from 1 MiB to
+// 1 GiB, idle and under a concurrent forward (profiles/r02_auto_table_clean.ndjson): 1 MiB 25 vs
+// 36 us, 4 MiB 82 vs 94 us, 16 MiB 0.31 vs 0.34 ms, >= 64 MiB at the link rate vs 0.93 of it.
+// The round-1 zero-copy bucket (<= 8 MiB) only reflected copies from cache-dirty arenas.
+struct AutoBucket {
+    uint64_t max_bytes;
+    bool zero_copy;
+};
+static const AutoBucket kAutoTable[] = {{~0ull, false}};
+
 bool use_zero_copy(mpsw_ctx* c, uint64_t bytes) {
     if (c->cfg.swap_mode == MPSW_SWAP_ZERO_COPY) return true;
     if (c->cfg.swap_mode == MPSW_SWAP_COPY_ENGINE) return false;
-    return bytes <= (8ull << 20);   // AUTO: zero-copy for shards <= 8 MiB (cfg5 sweep crossover)
+    for (const auto& b : kAutoTable)
+        if (bytes <= b.max_bytes) return b.zero_copy;
+    return false;
 }
 
 int zc_ctas(mpsw_ctx* c) { return c->cfg.zc_ctas > 0 ? c->cfg.zc_ctas : 32; }
@@ -81,6 +94,10 @@ void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
     const uint8_t* src = arena_of(c, e.model, R);
     const bool zc = use_zero_copy(c, S);
     const int r = R.index;
+    if (md.arena_dirty[R.local]) {                 // caller-filled in place: write back from the CPU caches
+        flush_to_memory(arena_of(c, e.model, R), S);
+        c->models[e.model]->arena_dirty[R.local] = 0;
+    }
     {
         const FwdShape& f = md.fs[R.local];
         R.wptr[e.model] = make_ptrs(md.layout[R.local], base, R.stage * f.n_layers, f.n_layers);
