@@ -44,7 +44,7 @@ PRESETS = {
     # TP8, 7.5 GB per rank, 8 virtual ranks on cuda:0 sharing its one PCIe link), 2 models with
     # the first two Zipf rates (10, 5 req/s), budget 1 model, CV=4, max batch 32, L=8, 20 s
     "cfg4-slice": dict(model="opt-30b", n=2, tp=8, k=1, max_batch=32, L=8, kind="gamma",
-                       rates=zipf_rates(6, 10.0, 1.0)[:2], duration=20.0, gpus=1),
+                       rates=zipf_rates(6, 10.0, 1.0)[:2], duration=20.0, gpus=1, seed0=3000),
     # NEXT-4 (§6): models of different sizes in one 30 GB region (first-fit placement):
     # 1 x OPT-13B, 3 x OPT-1.3B, 2 x OPT-125M; Gamma CV=1, 30 s, L=8, max batch 8
     "hetero": dict(models=["opt-13b", "opt-1.3b", "opt-1.3b", "opt-1.3b", "opt-125m", "opt-125m"], tp=1,
@@ -99,7 +99,7 @@ def main():
                writeback=0, max_dims=d, prefetch=args.prefetch, victim_policy=args.victim_policy) as ctx:
         ids = [ctx.register_model(x) for x in dims]
         for m in ids:
-            ctx.synth_fill(m, 7000 + m)
+            ctx.synth_fill(m, P.get("seed0", 7000) + m)
         res["setup_s"] = time.perf_counter() - t_setup
         outs = []
         t0 = time.perf_counter()
@@ -118,6 +118,19 @@ def main():
             if not r.warmup:
                 lat.append(td - ta)
                 lat_by.setdefault(names[r.model], []).append(td - ta)
+        # resident shards vs the oracle's hashes of their C0 images, where tests/golden has them
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "c0_shard_hashes.json")))
+        checks = []
+        for mi, m in enumerate(ids):
+            if ctx.residency(m) != M.RESIDENT:
+                continue
+            for r in range(tp):
+                k = f"{names[mi]}/tp{tp}/r{r}/seed{P.get('seed0', 7000) + mi}/bf16"
+                if k in gold:
+                    checks.append(ctx.checksum(m, r) == int(gold[k], 16))
+        if checks:
+            res["resident_checksums_equal_oracle"] = all(checks)
+            res["resident_checksums_checked"] = len(checks)
         tpath = "/tmp/serve_trace.ndjson"
         ctx.trace_dump(tpath)
         ctx.timeline_dump("/tmp/serve_timeline.ndjson")
@@ -170,7 +183,7 @@ def main():
         for rid, r, out in pool[:: max(1, len(pool) // n_check)][:n_check]:
             if r.model not in Ws:
                 big = layout.shard_bytes(dims[r.model], 1) > 2**31
-                Ws[r.model] = (layout.LazyFull if big else layout.full_tensors)(dims[r.model], 7000 + r.model)
+                Ws[r.model] = (layout.LazyFull if big else layout.full_tensors)(dims[r.model], P.get("seed0", 7000) + r.model)
             ref = forward.forward_bf16_emulated(dims[r.model], Ws[r.model], r.tokens[None])[0]
             ex = forward.forward_exact(dims[r.model], Ws[r.model], r.tokens[None])[0]
             errs.append(forward.rel_l2(out, ref))
