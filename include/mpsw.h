@@ -106,6 +106,11 @@ typedef struct {
     int victim_policy;            /* no free range for a load: 0 = evict LRU victims until a     */
                                   /* first fit appears (reading #28); 1 = the window that evicts */
                                   /* the fewest bytes (knapsack, reading #30, NEXT-4)            */
+    int debug_checks;             /* 1 = device-side residency check (race detection): each load */
+                                  /* stamps its entry id into a per-rank device word of the     */
+                                  /* model after its copies, each offload stamps "evicted", and */
+                                  /* every forward first checks that the stamp is the load the  */
+                                  /* engine gated it on; a mismatch poisons the ctx (EINVARIANT)*/
 } mpsw_config;
 
 typedef struct {

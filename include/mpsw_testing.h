@@ -56,6 +56,11 @@ mpsw_status mpsw_test_tap(mpsw_ctx* ctx, int n_layers, int what, int rank, void*
  * Single-process ctx only. Errors: EINVAL. */
 mpsw_status mpsw_test_inject_fault(mpsw_ctx* ctx, int rank);
 
+/* Debug-check self test (mpsw_config.debug_checks = 1): overwrite every local rank's residency
+ * stamp of `model_id` with a value no load ever writes, so the model's next forward must trip the
+ * check (ctx poisoned, EINVARIANT in the poison message). Errors: EINVAL (checks off / model). */
+mpsw_status mpsw_test_corrupt_stamp(mpsw_ctx* ctx, int model_id);
+
 #ifdef __cplusplus
 }
 #endif

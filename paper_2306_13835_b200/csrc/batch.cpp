@@ -46,6 +46,10 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
                             cudaMemcpyHostToDevice, cs));
     const int32_t* pos = R.ws.meta + 2 * B + 1;
     int nl = 0;
+    if (R.d_stamp) {                               // debug checks: the model is resident from that load
+        launch_check_stamp(R.d_stamp + e.model, e.expect_stamp, R.d_err, cs);
+        ++nl;
+    }
     uint64_t& point = R.ar_point;                  // persistent: parity alternates across batches
     // Reduce-scatter all-reduce (large M·h·(t-1)): each rank reduces, adds bias + residual and
     // normalises only its own slice of the M rows, then writes that slice's bf16 LN output into

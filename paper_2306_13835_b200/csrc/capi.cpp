@@ -43,6 +43,8 @@ static void release_init_resources(mpsw_ctx* c) {
         }
         if (R->region) cudaFree(R->region);
         if (R->d_sum) cudaFree(R->d_sum);
+        if (R->d_stamp) cudaFree(R->d_stamp);
+        if (R->h_err) cudaFreeHost(R->h_err);
     }
     for (auto& H : c->helpers) {
         cudaSetDevice(H->device);
@@ -181,6 +183,13 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
             return set_error(MPSW_ENOMEM, std::string("cudaMalloc(param budget): ") + cudaGetErrorString(e));
         }
         MPSW_CU(cudaMalloc(&R->d_sum, sizeof(unsigned long long)));
+        if (cfg->debug_checks) {
+            MPSW_CU(cudaMalloc(&R->d_stamp, kMaxModels * sizeof(unsigned long long)));
+            MPSW_CU(cudaMemset(R->d_stamp, 0xFF, kMaxModels * sizeof(unsigned long long)));   // kStampEvicted
+            MPSW_CU(cudaHostAlloc(&R->h_err, sizeof(unsigned int), cudaHostAllocMapped | cudaHostAllocPortable));
+            *R->h_err = 0;
+            MPSW_CU(cudaHostGetDevicePointer(&R->d_err, R->h_err, 0));
+        }
         if (cfg->trace) {
             // one timeline origin per device, shared by the ranks that live on it
             for (auto& Q : c->ranks)
@@ -334,6 +343,8 @@ mpsw_status mpsw_shutdown(mpsw_ctx* c) {
         cudaFree(R->region);
         cudaFree(R->ws_base);
         cudaFree(R->d_sum);
+        if (R->d_stamp) cudaFree(R->d_stamp);
+        if (R->h_err) cudaFreeHost(R->h_err);
         cudaStreamDestroy(R->compute);
         cudaStreamDestroy(R->h2d);
         cudaStreamDestroy(R->d2h);
@@ -440,6 +451,7 @@ mpsw_status mpsw_register_model(mpsw_ctx* c, const mpsw_opt_dims* dims, int tp, 
         c->models.push_back(std::move(m));   // capacity reserved at init: no reallocation
         c->sm.add_model(size);
         c->f_off_of.push_back(-1);
+        c->load_id_of.push_back(~0ull);
         c->f_state.push_back(ST_EVICTED);
         *model_id = (int)c->models.size() - 1;
     }
@@ -725,6 +737,19 @@ mpsw_status mpsw_test_inject_fault(mpsw_ctx* c, int rank) {
     API_BEGIN
     if (!c || c->mp || rank < 0 || rank >= c->nr) return set_error(MPSW_EINVAL, "bad ctx / rank (single-process only)");
     c->fault_rank.store(rank);
+    return MPSW_OK;
+    API_END
+}
+
+mpsw_status mpsw_test_corrupt_stamp(mpsw_ctx* c, int model_id) {
+    API_BEGIN
+    if (!c || model_id < 0 || model_id >= (int)c->models.size()) return set_error(MPSW_EINVAL, "bad ctx / model");
+    if (!c->cfg.debug_checks) return set_error(MPSW_EINVAL, "debug_checks is off");
+    for (auto& R : c->ranks) {
+        MPSW_CU(cudaSetDevice(R->device));
+        const unsigned long long bogus = 0x5EEDull;
+        MPSW_CU(cudaMemcpy(R->d_stamp + model_id, &bogus, sizeof(bogus), cudaMemcpyHostToDevice));
+    }
     return MPSW_OK;
     API_END
 }

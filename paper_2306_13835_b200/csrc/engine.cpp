@@ -176,6 +176,7 @@ void publish(mpsw_ctx* c, const Entry& e) {
     rec.B = e.B;
     rec.M = e.M;
     rec.writeback = e.writeback;
+    rec.stamp = e.expect_stamp;
     s->log_tail.store(tail + 1, std::memory_order_release);
 }
 
@@ -189,7 +190,9 @@ void dispatch(mpsw_ctx* c, const std::vector<Decision>& ds, double now) {
         e->model = d.model;
         e->off = d.off;
         e->t_submit = now;
+        if (d.kind == E_LOAD) c->load_id_of[d.model] = e->id;
         if (d.kind == E_BATCH) {
+            e->expect_stamp = c->load_id_of[d.model];
             e->off = (uint64_t)c->sm.off_of[d.model];
             // pack tokens + meta into the pinned ring entry (shm in mp mode: every rank reads it)
             e->ring = c->ring_next;
@@ -347,6 +350,18 @@ void retire_ticket(mpsw_ctx* c, uint64_t id) {
     }
 }
 
+// Debug checks (mpsw_config.debug_checks): after a batch completed, a non-zero error word on
+// any local rank means its forward found the model's residency stamp different from the load the
+// engine gated the batch on — the batch read parameters that were not (or no longer) resident.
+void check_stamps(mpsw_ctx* c, const Entry& e) {
+    if (!c->cfg.debug_checks) return;
+    for (auto& R : c->ranks)
+        if (R->h_err && *(volatile unsigned int*)R->h_err)
+            throw Error(MPSW_EINVARIANT, "batch " + std::to_string(e.id) + " of model " + std::to_string(e.model) +
+                                             " ran on a range whose residency stamp is not load " +
+                                             std::to_string(e.expect_stamp) + " (rank " + std::to_string(R->index) + ")");
+}
+
 bool poll_inflight(mpsw_ctx* c) {
     bool progressed = false;
     for (size_t i = 0; i < c->inflight.size();) {
@@ -372,6 +387,7 @@ bool poll_inflight(mpsw_ctx* c) {
         if (e.n_acked == c->nr) {
             const double now = now_s(c->t0);
             if (e.kind == E_BATCH) {
+                check_stamps(c, e);
                 complete_batch(c, ep, now);
                 log_event(c, "{\"ev\":\"batch_done\",\"t\":" + fmt_d(now) + ",\"batch\":" + std::to_string(e.id) + "}");
                 step_and_dispatch(c, [&](std::vector<Decision>& ds) { c->sm.batch_done(e.id, now, ds); }, now);
@@ -481,6 +497,7 @@ void follower_main(mpsw_ctx* c) {
             e->B = rec.B;
             e->M = rec.M;
             e->writeback = rec.writeback;
+            e->expect_stamp = rec.stamp;
             e->t_submit = now_s(c->t0);
             if (e->kind != E_BATCH) {
                 c->swap_gen.fetch_add(1);
@@ -511,6 +528,7 @@ void follower_main(mpsw_ctx* c) {
                     if (e.kind == E_OFFLOAD && c->f_state[e.model] == ST_OFFLOADING) c->f_state[e.model] = ST_EVICTED;
                 }
                 if (e.kind == E_BATCH) {
+                    check_stamps(c, e);
                     record_fwd_time(c, e);
                     c->n_batches++;
                 } else {

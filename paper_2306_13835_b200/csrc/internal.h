@@ -55,6 +55,10 @@ uint64_t host_checksum(const uint8_t* p, uint64_t bytes, int threads);
 void launch_zero_copy(void* dst, const void* src, uint64_t bytes, int ctas, cudaStream_t s);
 // Order-independent checksum (C4) of a device buffer; result accumulated into *d_out.
 void launch_checksum(const void* buf, uint64_t bytes, unsigned long long* d_out, cudaStream_t s);
+// Residency stamps of the debug checks (mpsw_config.debug_checks).
+constexpr unsigned long long kStampEvicted = ~0ull;
+void launch_stamp(unsigned long long* slot, unsigned long long value, cudaStream_t s);
+void launch_check_stamp(const unsigned long long* slot, unsigned long long expect, unsigned int* err, cudaStream_t s);
 
 // ---------------------------------------------------------------- forward (per rank)
 struct TensorPtrs {          // device pointers of one rank's shard inside a slot

@@ -109,6 +109,23 @@ void launch_zero_copy(void* dst, const void* src, uint64_t bytes, int ctas, cuda
     MPSW_CU(cudaGetLastError());
 }
 
+// Residency stamps (mpsw_config.debug_checks): a load writes its entry id, an offload the evicted
+// marker, behind its copies on the copy stream; the forward checks the stamp first.
+__global__ void stamp_kernel(unsigned long long* slot, unsigned long long value) { *slot = value; }
+
+__global__ void check_stamp_kernel(const unsigned long long* slot, unsigned long long expect, unsigned int* err) {
+    const unsigned long long v = *(volatile const unsigned long long*)slot;
+    if (v != expect) *(volatile unsigned int*)err = 1u;   // mapped pinned host word: a plain store
+}
+
+void launch_stamp(unsigned long long* slot, unsigned long long value, cudaStream_t s) {
+    stamp_kernel<<<1, 1, 0, s>>>(slot, value);
+}
+
+void launch_check_stamp(const unsigned long long* slot, unsigned long long expect, unsigned int* err, cudaStream_t s) {
+    check_stamp_kernel<<<1, 1, 0, s>>>(slot, expect, err);
+}
+
 void launch_checksum(const void* buf, uint64_t bytes, unsigned long long* d_out, cudaStream_t s) {
     if (bytes & 7) throw Error(MPSW_EINVAL, "checksum needs a multiple of 8 bytes");
     const uint64_t n16 = bytes / 16;

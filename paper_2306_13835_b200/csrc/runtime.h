@@ -73,6 +73,7 @@ struct ShmRec {            // one decision published by the leader
     uint64_t off;          // load / offload: byte offset of the model's range
     int32_t kind, model, ring, B, M;
     int32_t writeback;     // offload: copy the range back to the arena (else clean eviction)
+    uint64_t stamp;        // batch (debug checks): id of the load it is gated on
 };
 
 struct ShmCtl {
@@ -115,6 +116,7 @@ struct Tap {
 
 struct Entry {
     Tap tap;                                     // batch: verification tap (dst == nullptr: none)
+    uint64_t expect_stamp = 0;                   // batch (debug checks): id of the load it is gated on
     uint64_t id = 0;
     int kind = 0, model = -1;
     uint64_t off = 0;                            // load / offload: byte offset in the region
@@ -209,6 +211,9 @@ struct Rank {
     std::vector<cudaEvent_t> last_compute; // per model
     std::vector<char> last_compute_valid;
     unsigned long long* d_sum = nullptr;
+    unsigned long long* d_stamp = nullptr;   // debug checks: per model, id of the load that made it resident
+    unsigned int* h_err = nullptr;           // debug checks: mapped pinned error word (set by the device)
+    unsigned int* d_err = nullptr;           // its device alias
     std::thread th;
     std::mutex mu;
     std::condition_variable cv;
@@ -302,6 +307,7 @@ struct mpsw_ctx {
     std::mutex tap_mu;
     mpsw::Tap tap_next;        // armed by mpsw_test_tap, taken by the next dispatched batch
     std::atomic<int> fault_rank{-1};   // mpsw_test_inject_fault: this rank throws at its next all-reduce point
+    std::vector<uint64_t> load_id_of;  // engine: id of the load entry that made each model resident
     // follower-local view of residency (mp followers)
     std::vector<int64_t> f_off_of;
     std::vector<int> f_state;

@@ -186,6 +186,10 @@ void issue_load(mpsw_ctx* c, Rank& R, Entry& e) {
             }
         }
     }
+    if (R.d_stamp) {                               // debug checks: this load made the model resident
+        launch_stamp(R.d_stamp + e.model, e.id, R.h2d);
+        c->launches++;
+    }
     // completion marker right behind the last copy; the gate bookkeeping (event destroys) comes
     // after it, so host work never sits between the copy and its completion on the stream
     MPSW_CU(cudaEventRecord(e.ev_done[r], R.h2d));
@@ -223,6 +227,10 @@ void issue_offload(mpsw_ctx* c, Rank& R, Entry& e) {
         }
     } else if (fwd_pending) {
         add_gate(R, lo, lo + S, false, R.d2h);                  // after the victim's last forward
+    }
+    if (R.d_stamp) {                               // debug checks: no longer resident
+        launch_stamp(R.d_stamp + e.model, kStampEvicted, R.d2h);
+        c->launches++;
     }
     // (clean eviction of a victim whose forwards have all completed needs no gate: the load that
     // reuses its bytes would otherwise pay a cross-stream event wait, ~40 us per swap at small

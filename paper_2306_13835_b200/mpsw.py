@@ -40,7 +40,7 @@ class Config(C.Structure):
                 ("world_size", C.c_int), ("world_rank", C.c_int), ("shm_name", C.c_char_p),
                 ("gemm_impl", C.c_int), ("pp", C.c_int), ("helper_device_ids", C.POINTER(C.c_int)),
                 ("n_helpers", C.c_int), ("max_dims", OptDims), ("prefetch", C.c_int), ("pp_broadcast", C.c_int),
-                ("victim_policy", C.c_int)]
+                ("victim_policy", C.c_int), ("debug_checks", C.c_int)]
 
 
 class TensorDesc(C.Structure):
@@ -86,6 +86,7 @@ _SIGS = {
     "mpsw_test_tap": [_P, C.c_int, C.c_int, C.c_int, _P, C.c_uint64],
     "mpsw_set_writeback": [_P, C.c_int],
     "mpsw_test_inject_fault": [_P, C.c_int],
+    "mpsw_test_corrupt_stamp": [_P, C.c_int],
 }
 
 _lib = None
@@ -157,7 +158,7 @@ class Ctx:
     def __init__(self, device_ids=(0,), budget=1 << 30, max_batch=8, max_tokens=8, dtype=BF16,
                  max_inflight=1, swap_mode=SWAP_AUTO, chunk_bytes=0, writeback=1, trace=0, zc_ctas=0,
                  world_size=1, world_rank=0, shm_name=None, gemm_impl=0, pp=1, helper_device_ids=(),
-                 max_dims=None, prefetch=0, pp_broadcast=0, victim_policy=0):
+                 max_dims=None, prefetch=0, pp_broadcast=0, victim_policy=0, debug_checks=0):
         """Single-process: one ctx over len(device_ids) = tp * pp ranks (global rank
         g = stage * tp + tp_rank). Multi-process (world_size > 1): device_ids = (this process's
         GPU,), rank world_rank of a TP group of world_size. max_dims: the largest model shape the
@@ -176,7 +177,7 @@ class Ctx:
                      self._shm, gemm_impl, pp,
                      (C.c_int * max(1, len(helper_device_ids)))(*helper_device_ids) if helper_device_ids else None,
                      len(helper_device_ids), dims_of(max_dims) if max_dims is not None else OptDims(), prefetch,
-                     pp_broadcast, victim_policy)
+                     pp_broadcast, victim_policy, debug_checks)
         h = _P()
         _check(lib().mpsw_init(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -291,6 +292,10 @@ class Ctx:
     def inject_fault(self, rank):
         """Test hook (include/mpsw_testing.h): rank throws at its next all-reduce point."""
         _check(lib().mpsw_test_inject_fault(self.h, rank))
+
+    def corrupt_stamp(self, model_id):
+        """Test hook (include/mpsw_testing.h): make the model's next forward trip the debug check."""
+        _check(lib().mpsw_test_corrupt_stamp(self.h, model_id))
 
     def set_writeback(self, writeback):
         _check(lib().mpsw_set_writeback(self.h, int(writeback)))

@@ -60,7 +60,7 @@ def test_engine_fuzz(tmp_path, seed):
     outs = []
     with M.Ctx(device_ids=(0,) * tp, budget=budget, max_batch=4, max_tokens=8, trace=1, max_inflight=o["D"],
                writeback=o["writeback"], swap_mode=o["mode"], chunk_bytes=o["chunk"], max_dims=dmax,
-               prefetch=o["prefetch"]) as ctx:
+               prefetch=o["prefetch"], debug_checks=1) as ctx:     # residency stamps checked in every forward
         ids = [ctx.register_model(d) for d in dims]
         for m in ids:
             ctx.synth_fill(m, seeds[m])
@@ -168,7 +168,7 @@ def test_engine_fuzz_pipeline(tmp_path, seed):
     ref = {m: [checksum.checksum(a) for a in v] for m, v in imgs.items()}
     outs = []
     with M.Ctx(device_ids=(0,) * nr, pp=pp, budget=budget, max_batch=4, max_tokens=8, trace=1, writeback=wb,
-               swap_mode=mode, chunk_bytes=1 << 20, max_dims=dmax) as ctx:
+               swap_mode=mode, chunk_bytes=1 << 20, max_dims=dmax, debug_checks=1) as ctx:
         ids = [ctx.register_model(d) for d in dims]
         for m in ids:
             ctx.synth_fill(m, seeds[m])
@@ -263,7 +263,7 @@ def test_long_run_many_swaps(tmp_path):
     S_ = placement_bytes(d, tp)
     seeds = [9300 + i for i in range(3)]
     with M.Ctx(device_ids=(0,) * tp, budget=S_ + 4096, max_batch=2, max_tokens=4, trace=1, max_inflight=2,
-               writeback=1, chunk_bytes=1 << 20) as ctx:
+               writeback=1, chunk_bytes=1 << 20, debug_checks=1) as ctx:
         ids = [ctx.register_model(d) for _ in range(3)]
         for m in ids:
             ctx.synth_fill(m, seeds[m])

@@ -97,3 +97,52 @@ def test_failed_init_frees_the_budget():
     with M.Ctx(device_ids=(0,), budget=big) as ctx:
         d = opt_dims("tiny")
         ctx.wait(ctx.swap_in(ctx.register_model(d)))
+
+
+@pytest.mark.parametrize("tp,writeback", [(1, 1), (2, 0)])
+def test_debug_checks_silent_on_correct_runs(tp, writeback):
+    """Residency stamps on (debug_checks): 30 alternating blocking requests over 3 models with room
+    for one — every request swaps, every forward checks the stamp of the load it was gated on —
+    and no check trips; logits still match the oracle."""
+    M = need_gpu()
+    from oracle import forward
+    from tests import parity_util as PU
+    d = opt_dims("small")
+    S_ = layout.shard_bytes(d, tp)
+    with M.Ctx(device_ids=(0,) * tp, budget=(S_ + 4095) // 4096 * 4096, max_batch=2, max_tokens=8,
+               writeback=writeback, debug_checks=1) as ctx:
+        ids = [ctx.register_model(d) for _ in range(3)]
+        for i, m in enumerate(ids):
+            ctx.synth_fill(m, 40 + i)
+        outs = []
+        for i in range(30):
+            m = ids[i % 3]
+            tok = request_tokens(8, m, i, 8, d.vocab)
+            rid, y = ctx.request(m, tok)
+            ctx.wait_request(rid, 120)
+            outs.append((m, tok, y.copy()))
+        assert ctx.stats()["swaps_in"] == 30
+    W = layout.full_tensors(d, 40 + outs[-1][0])
+    PU.assert_logits(outs[-1][2], forward.forward_bf16_emulated(d, W, outs[-1][1][None])[0], tag="debug checks")
+
+
+def test_debug_checks_detect_a_forward_on_a_non_resident_range():
+    """The detector fires: corrupt a resident model's stamp (as a load that never finished, or an
+    eviction racing the forward, would leave it); its next request poisons the ctx with
+    EINVARIANT naming the residency stamp, and shutdown still returns."""
+    M = need_gpu()
+    d = opt_dims("small")
+    ctx = M.Ctx(device_ids=(0, 0), budget=layout.shard_bytes(d, 2) + (2 << 20), max_batch=1, max_tokens=8,
+                debug_checks=1)
+    m = ctx.register_model(d)
+    ctx.synth_fill(m, 3)
+    rid, _ = ctx.request(m, request_tokens(0, 0, 0, 8, d.vocab))
+    ctx.wait_request(rid, 60)
+    ctx.corrupt_stamp(m)
+    rid, _ = ctx.request(m, request_tokens(0, 0, 1, 8, d.vocab))
+    with pytest.raises(M.MpswError) as e:
+        ctx.wait_request(rid, 60)
+    assert "residency stamp" in str(e.value)
+    done = threading.Event()
+    threading.Thread(target=lambda: (ctx.close(), done.set()), daemon=True).start()
+    assert done.wait(60)
