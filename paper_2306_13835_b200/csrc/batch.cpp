@@ -201,6 +201,9 @@ void issue_batch(mpsw_ctx* c, Rank& R, Entry& e) {
             MPSW_CU(cudaGraphDestroy(graph));
             g.kernels = nl - nl0;
             g.points = point - p0;
+            // the batch's device span starts at the graph launch, not before the host-side
+            // capture and instantiation (which the idle stream would otherwise count)
+            MPSW_CU(cudaEventRecord(e.ev_start[r], cs));
             MPSW_CU(cudaGraphLaunch(g.exec, cs));
         }
     }
