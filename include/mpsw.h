@@ -111,6 +111,7 @@ typedef struct {
                                   /* model after its copies, each offload stamps "evicted", and */
                                   /* every forward first checks that the stamp is the load the  */
                                   /* engine gated it on; a mismatch poisons the ctx (EINVARIANT)*/
+                                  /* (env MPSW_DEBUG_CHECKS=1 turns it on for any ctx)          */
 } mpsw_config;
 
 typedef struct {

@@ -122,6 +122,9 @@ mpsw_status mpsw_init(const mpsw_config* cfg, mpsw_ctx** out) {
     for (int h = 0; h < cfg->n_helpers; ++h)
         if (cfg->helper_device_ids[h] < 0 || cfg->helper_device_ids[h] >= ndev)
             return set_error(MPSW_EINVAL, "helper device id out of range");
+    mpsw_config cfg_eff = *cfg;
+    if (getenv("MPSW_DEBUG_CHECKS")) cfg_eff.debug_checks = 1;   // enable the race detector in any process
+    cfg = &cfg_eff;
     auto c = std::make_unique<mpsw_ctx>();
     struct Guard {
         mpsw_ctx* c;

@@ -37,6 +37,8 @@ def test_process_group(tmp_path, world, rs):
     out = str(tmp_path / "mp.json")
     port = free_port()
     env = dict(os.environ, MPSW_RS_MIN_BYTES="0" if rs else str(1 << 62))
+    if rs:
+        env["MPSW_DEBUG_CHECKS"] = "1"      # residency stamps travel in the shm records
     procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "mp_group_run.py"), str(r), str(world), str(port), out],
                               env=env)
              for r in range(world)]
