@@ -85,13 +85,23 @@ void pin_free(PinnedBuf& b) {
 // profiles/r02_ce_dirty_cache.ndjson), so every arena the library writes (synthetic fill,
 // caller shards copied in) is flushed once; a DMA read of clean lines runs at full speed.
 // MPSW_NO_FLUSH=1 skips it (A/B measurement).
+static bool has_clflushopt() {
+    unsigned a, b, c, d;
+    __asm__ __volatile__("cpuid" : "=a"(a), "=b"(b), "=c"(c), "=d"(d) : "a"(7), "c"(0));
+    return (b >> 23) & 1u;          // CPUID.(EAX=7,ECX=0):EBX[23] = CLFLUSHOPT
+}
+
 void flush_to_memory(uint8_t* p, uint64_t n) {
     static const bool off = getenv("MPSW_NO_FLUSH") != nullptr;
+    static const bool opt = has_clflushopt();
     if (off || !n) return;
     const uint64_t lines = (n + 63) / 64;
     const int T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     auto work = [=](uint64_t l0, uint64_t l1) {
-        for (uint64_t l = l0; l < l1; ++l) asm volatile("clflushopt (%0)" ::"r"(p + l * 64) : "memory");
+        if (opt)
+            for (uint64_t l = l0; l < l1; ++l) asm volatile("clflushopt (%0)" ::"r"(p + l * 64) : "memory");
+        else
+            for (uint64_t l = l0; l < l1; ++l) asm volatile("clflush (%0)" ::"r"(p + l * 64) : "memory");
         asm volatile("sfence" ::: "memory");
     };
     if (n < (16ull << 20)) {
