@@ -599,6 +599,11 @@ static int tc_grid(int tiles, int K) {
         for (int sp = 1; sp <= kb; ++sp)
             if (kb % sp == 0 && (uint64_t)ut * sp <= gmax && (uint64_t)(kb / sp) >= mu) best = sp;
         if (best && (uint64_t)ut * best * 5 >= g_sk * 4) return ut * best;
+        // small per-CTA shares (< 16 units under stream-K): straddling a tile boundary costs more
+        // than the lost CTAs, so take the aligned split down to 60 % of the slots (OPT-13B
+        // out_proj: 200 aligned CTAs of 16 units instead of 296 of 10.8; forward 5.31 -> 5.22 ms
+        // at M = 2 in the MPSW_TC_MINU = 16 sweep, profiles/r02_tc_knobs.ndjson)
+        if (best && units < 16 * g_sk && (uint64_t)ut * best * 5 >= gmax * 3) return ut * best;
     }
     return (int)g_sk;
 }
