@@ -603,7 +603,8 @@ static int tc_grid(int tiles, int K) {
         // than the lost CTAs, so take the aligned split down to 60 % of the slots (OPT-13B
         // out_proj: 200 aligned CTAs of 16 units instead of 296 of 10.8; forward 5.31 -> 5.22 ms
         // at M = 2 in the MPSW_TC_MINU = 16 sweep, profiles/r02_tc_knobs.ndjson)
-        if (best && units < 16 * g_sk && (uint64_t)ut * best * 5 >= gmax * 3) return ut * best;
+        static const int align60 = env_int("MPSW_TC_ALIGN60", 1);
+        if (align60 && best && units < 16 * g_sk && (uint64_t)ut * best * 5 >= gmax * 3) return ut * best;
     }
     return (int)g_sk;
 }
