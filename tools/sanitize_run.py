@@ -29,3 +29,15 @@ for mode in (M.SWAP_ZERO_COPY, M.SWAP_COPY_ENGINE):
             rid, _ = ctx.request(m, request_tokens(6, m, 0, 2, d.vocab))
             ctx.wait_request(rid, 600)
         print("checksums", [hex(ctx.checksum(a, r)) for r in range(tp)], "launches", ctx.stats()["kernel_launches"])
+
+# TP 1: the forward is captured into a CUDA graph on a shape's second batch and replayed after
+S1 = layout.shard_bytes(d, 1)
+with M.Ctx(device_ids=(0,), budget=(S1 + 4095) // 4096 * 4096, max_batch=4, max_tokens=8) as ctx:
+    a, b = ctx.register_model(d), ctx.register_model(d)
+    ctx.synth_fill(a, 1)
+    ctx.synth_fill(b, 2)
+    for it in range(4):
+        for m in (a, b):
+            rid, _ = ctx.request(m, request_tokens(7, m, it, 8, d.vocab))
+            ctx.wait_request(rid, 600)
+    print("tp1 graphs: launches", ctx.stats()["kernel_launches"])
