@@ -66,3 +66,12 @@ def test_stages_bf16_opt13b_full_size():
 @pytest.mark.parametrize("tp", [1, 2])
 def test_stages_fp32(tp):
     _run("small", tp, 8, 50 + tp, dtype="fp32")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,tp,layers", [("opt-13b", 8, [0, 39]), ("opt-30b", 8, [0, 47])])
+def test_stages_bf16_full_size_tp8(name, tp, layers):
+    """cfg3 at t = 8 and cfg4's model at its TP degree (8 virtual ranks on one B200): every stage of
+    the first and last layer, the final LN and lm_head, teacher-forced against the fp64 oracle —
+    per-rank slices of q/k/v, attention and ReLU on all 8 ranks, the 8-way all-reduce blocks."""
+    _run(name, tp, 8, 5, layers=layers)
