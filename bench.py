@@ -161,6 +161,18 @@ def ce_peaks(dev=0, nbytes=1 << 30):
     return best_h2d, best_bi
 
 
+def pcie_link(dev=0):
+    """PCIe generation and width of the GPU's link (nvidia-smi): the roofline's assumption, checked."""
+    try:
+        out = subprocess.run(["nvidia-smi", "-i", str(dev), "--query-gpu=pcie.link.gen.current,pcie.link.width.current,"
+                              "pcie.link.gen.max,pcie.link.width.max", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=30).stdout.strip().split(",")
+        g, w, gm, wm = (int(x.strip()) for x in out[:4])
+        return {"gen": g, "width": w, "gen_max": gm, "width_max": wm}
+    except Exception:
+        return None
+
+
 def host_info():
     model = ""
     try:
@@ -445,6 +457,7 @@ def run_ours(args, rank, world):
         raise SystemExit(f"bench: {args.n_models} models x {S_r / 1e9:.2f} GB pinned per rank need "
                          f"{need / 1e9:.1f} GB of host RAM, {avail / 1e9:.1f} GB available (ENOMEM)")
     ce_peak, ce_bidir = ce_peaks(dev)
+    link = pcie_link(dev)
     t_setup = time.perf_counter()
     kw = dict(budget=(S_r + 4095) // 4096 * 4096, max_batch=1, max_tokens=max(8, args.tokens),
               writeback=args.writeback, swap_mode=args.swap_mode, chunk_bytes=args.chunk_mb << 20, trace=1)
@@ -526,7 +539,7 @@ def run_ours(args, rank, world):
         "fwd_ms": (st1["fwd_gpu_us_sum"] - st0["fwd_gpu_us_sum"]) / 1e3 / max(1, st1["fwd_gpu_n"] - st0["fwd_gpu_n"]),
         "ce_peak": ce_peak, "ce_bidir": ce_bidir, "clocks": clk.summary(),
         "setup": {"register_pin_s": t_reg, "synth_fill_s": t_fill}, "wb": wb, "wb_h2d_ms_max": wb_h2d_local,
-        "parity": parity,
+        "parity": parity, "link": link,
     }
 
 
@@ -633,7 +646,7 @@ def main():
                      "frac": achieved / peak, "traffic": None,
                      "peak_source": "nominal PCIe Gen5 x16 per direction per GPU (north star); MEASURED_PEAKS.json has no PCIe entry",
                      "measured_ce_peak_GBps_per_gpu": r["ce_peak"], "frac_of_measured_ce_peak": achieved / (tp * r["ce_peak"]),
-                     "measured_ce_bidir_GBps_per_gpu": r["ce_bidir"],
+                     "measured_ce_bidir_GBps_per_gpu": r["ce_bidir"], "pcie_link": r["link"],
                      "kernel": "swap-in H2D (copy engine cudaMemcpyAsync chunks; not an SM kernel, so ncu dram traffic is n/a)"},
         "forward": {"ms_per_batch_device": r["fwd_ms"], "weight_bytes_per_rank": r["S_r"],
                     "achieved_hbm_GBps": r["S_r"] / (r["fwd_ms"] / 1e3) / 1e9 if r["fwd_ms"] > 0 else None,
