@@ -455,10 +455,27 @@ int fwd_embed(const FwdShape& s, const TensorPtrs& W, const FwdWorkspace& ws, in
     return 1;
 }
 
+// Timing instrumentation only (MPSW_DEV_NOOP_LN / MPSW_DEV_NOOP_ATTN): launch an empty kernel with
+// the same grid instead, to bound what a kernel costs on the forward's critical path. The results
+// are then wrong; never set outside a timing experiment.
+__global__ void dev_noop_kernel() {
+    pdl_trigger();
+    pdl_wait();
+}
+static bool dev_noop(const char* n) {
+    const char* e = getenv(n);
+    return e && atoi(e) != 0;
+}
+
 template <typename T, int VPT>
 static void launch_ln(int rows, int row0, const Peers& P, const float* residual, const void* bias, const void* pos_table,
                       const int32_t* pos, const void* gamma, const void* beta, float* x_out, const LnDst& D, int h,
                       cudaStream_t st) {
+    static const bool noop = dev_noop("MPSW_DEV_NOOP_LN");
+    if (noop) {
+        launch_pdl(dev_noop_kernel, rows, kLnThreads, 0, st);
+        return;
+    }
     launch_pdl(reduce_ln_kernel<T, VPT>, rows, kLnThreads, 0, st, P, residual, (const T*)bias, (const T*)pos_table, pos,
                (const T*)gamma, (const T*)beta, x_out, D, h, row0);
 }
@@ -565,7 +582,10 @@ int fwd_attention(const FwdShape& s, const FwdWorkspace& ws, int B, cudaStream_t
     const int hl = s.heads_local * s.head_dim;
     dim3 grid(B, s.heads_local);
     const int32_t* seq_start = ws.meta;
-    if (s.dtype == MPSW_BF16)
+    static const bool noop = dev_noop("MPSW_DEV_NOOP_ATTN");
+    if (noop)
+        launch_pdl(dev_noop_kernel, grid, 128, 0, st);
+    else if (s.dtype == MPSW_BF16)
         launch_pdl(attention_kernel<bf16>, grid, 128, 0, st, (const float*)ws.qkv, seq_start, (bf16*)ws.o, hl, s.head_dim);
     else
         launch_pdl(attention_kernel<float>, grid, 128, 0, st, (const float*)ws.qkv, seq_start, (float*)ws.o, hl,
