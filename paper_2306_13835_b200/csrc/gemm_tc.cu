@@ -38,17 +38,19 @@ struct TcSeg {
 struct TcArgs {
     TcSeg seg[3];
     int nseg, tiles, kb, K, M, Mp, stages, G;
-    uint64_t units;              // work units: tiles * kb (single CTA) or pairs * kb (CTA pairs)
+    uint64_t units;              // work units: unit tiles (tiles, or tile pairs) * kb
+    int vw;                      // workers per CTA (or CTA pair): consecutive ranges, one weight stream
     int epi;                     // 0: fp32 out (bias, scale); 1: bf16 out relu(acc + bias)
     void* out;
     int ldo;
     const int32_t* row_of_m;     // optional: output row for token m (-1 = drop); lm_head
-    float* partial;              // [CTAs][2][Mp][128]: a CTA's first / last partial run (row fastest)
+    float* partial;              // [G][kT][2][Mp][128]: a worker's first / last partial run per tile (row fastest)
     int* counters;               // [tiles], self-resetting
     int ext_fixup;               // 1: split tiles are reduced by tc_fixup_kernel, not in-kernel
     int nacc;                    // TMEM accumulator buffers (2 = epilogue overlaps the next run)
     unsigned long long* trace;   // dev: [CTAs][8] %globaltimer stamps per CTA phase, or null
     int l2_prefetch;             // weight units per CTA prefetched into L2 before griddepcontrol.wait
+    int l2hint;                  // 1: weights evict_first, token tile and partials evict_last in L2
 };
 
 __device__ __forceinline__ void stamp(const TcArgs& g, int c, int i) {
@@ -59,9 +61,8 @@ __device__ __forceinline__ void stamp(const TcArgs& g, int c, int i) {
     }
 }
 
-// Stream-K work split: worker w (a CTA, or a CTA pair) owns units [ubeg(w), ubeg(w+1)) of the
-// linearised (tile or tile pair, k-block) space. Depends only on (units, G) — never on M — so it
-// is batch-invariant.
+// Stream-K work split: worker w owns units [ubeg(w), ubeg(w+1)) of the linearised (unit tile,
+// k-block) space. Depends only on (units, G) — never on M — so it is batch-invariant.
 __device__ __forceinline__ uint64_t ubeg(const TcArgs& g, int c) { return (uint64_t)c * g.units / (uint64_t)g.G; }
 
 __device__ __forceinline__ int cta_of(const TcArgs& g, uint64_t u) {
@@ -71,20 +72,19 @@ __device__ __forceinline__ int cta_of(const TcArgs& g, uint64_t u) {
     return c;
 }
 
-// Tiles per work unit: 1 (single CTA, MMA M = 128) or 2 (CTA pair, MMA M = 256: CTA rank r of
-// the pair owns tile 2p + r of pair p).
-template <bool kPair> struct TileMap {
-    static constexpr int kT = kPair ? 2 : 1;
+// Tiles per work unit: kT = 1 (unit = (tile, k-block)) or 2 (unit = (tile pair, k-block); tile
+// 2p + r of pair p is the pair's tile r).
+template <int kT> struct TileMap {
     __device__ static int tile(uint64_t u, int kb, int r) { return (int)(u / kb) * kT + r; }
-    __device__ static int cta(int w, int r) { return w * kT + r; }
+    __device__ static int slot(int w, int r) { return w * kT + r; }   // partial slots of worker w, tile r of a unit
 };
 
-// Partial run of worker cc on a split tile: slot 0 if the tile is cc's first tile (pair), else 1
-// (a worker touches at most two split tiles / pairs: where its range starts and where it ends).
-template <bool kPair>
+// Partial run of worker cc on a split tile: slot 0 if the tile is cc's first unit tile, else 1
+// (a worker touches at most two split unit tiles: where its range starts and where it ends).
+template <int kT>
 __device__ __forceinline__ const float* partial_run(const TcArgs& g, int cc, int c_first, int unit_tile, int r, int row) {
     const int wh = (cc == c_first && (int)(ubeg(g, c_first) / g.kb) != unit_tile) ? 1 : 0;
-    return g.partial + ((size_t)TileMap<kPair>::cta(cc, r) * 2 + wh) * (size_t)g.Mp * kBN + row;
+    return g.partial + ((size_t)TileMap<kT>::slot(cc, r) * 2 + wh) * (size_t)g.Mp * kBN + row;
 }
 
 __device__ __forceinline__ void epi_store(const TcArgs& g, const TcSeg& seg, int n, int m, float x, float bias_n) {
@@ -122,6 +122,14 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
         "l"(map), "r"(bar_leader), "r"(c0), "r"(c1)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_pair_hint(void* dst, const CUtensorMap* map, uint32_t bar_leader, int c0, int c1,
+                                                      uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(bar_leader), "r"(c0), "r"(c1), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n"
@@ -139,23 +147,30 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
                  : "memory");
 }
 
-// One kernel, two work shapes (kPair):
-//  * single CTA: unit = (tile, k-block); the CTA's tcgen05.mma.cta_group::1 M = 128 reads its W
-//    tile [128 x 64] and the whole token tile [Mp x 64] from its own smem;
-//  * CTA pair (cluster of 2, cta_group::2): unit = (tile pair, k-block); each CTA loads its own W
-//    tile and HALF of the token tile (Mp/2 rows), the leader issues one M = 256 MMA that reads
-//    A from both CTAs (rows of each tile) and B split by N across them, D = each CTA's 128 rows
-//    x Mp in its own TMEM. Per SM and unit: 16 KB + Mp x 64 B through smem instead of
-//    16 KB + Mp x 128 B — half the token-tile re-reads, and deeper rings at large M.
-template <bool kPair>
-__global__ void __launch_bounds__(kThreads, 1)
+// One kernel, three executions of two splits:
+//  * kT = 1: unit = (tile, k-block); one CTA per worker, tcgen05.mma.cta_group::1 with M = 128
+//    reads its W tile [128 x 64] and the whole token tile [Mp x 64] from its own smem;
+//  * kT = 2, kCl = false: unit = (tile pair, k-block); each of the pair's tiles on its own CTA
+//    (CTA 2c + r streams tile r of worker c's units), cta_group::1 as above;
+//  * kT = 2, kCl = true: the same units on a CTA pair (cluster of 2, cta_group::2): each CTA loads
+//    its own W tile and HALF of the token tile (Mp/2 rows), the leader issues one M = 256 MMA that
+//    reads A from both CTAs and B split by N across them, D = each CTA's 128 rows x Mp in its own
+//    TMEM. Per SM and unit: 16 KB + Mp x 64 B through smem instead of 16 KB + Mp x 128 B.
+// Both executions of the pair split accumulate the same k-blocks of a tile in the same TMEM run
+// and sum the runs in the same worker order, so they give the same bits (tested); the choice may
+// follow M. A CTA (or pair) runs g.vw consecutive workers as one continuous weight stream; a run
+// ends at every worker boundary, so the bits do not depend on vw either.
+template <int kT, bool kCl>
+__global__ void __launch_bounds__(kThreads, 2)   // two resident CTAs per SM (stream-K grid of 2 x #SMs)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant__ CUtensorMap map_w1,
                const __grid_constant__ CUtensorMap map_w2, const __grid_constant__ CUtensorMap map_x, TcArgs g) {
-    using TM = TileMap<kPair>;
+    static_assert(kT == 1 || kT == 2, "1 or 2 tiles per unit");
+    static_assert(!kCl || kT == 2, "CTA pairs run the pair split");
+    using TM = TileMap<kT>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for the 128B swizzle atoms (same offset in both CTAs of a pair)
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    const int xrows = kPair ? g.Mp / 2 : g.Mp;     // token rows of the B tile this CTA holds
+    const int xrows = kCl ? g.Mp / 2 : g.Mp;       // token rows of the B tile this CTA holds
     const uint32_t tile_b_bytes = (uint32_t)xrows * kBK * 2;
     const int kStages = g.stages;
     uint8_t* sa = smem;
@@ -168,13 +183,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
     __shared__ int s_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int r = kPair ? (int)cluster_rank() : 0;           // rank in the pair
-    const bool leader = r == 0;
-    const int c = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // worker (CTA or pair)
-    const int cta = TM::cta(c, r);
-    const uint64_t u0 = ubeg(g, c), u1 = ubeg(g, c + 1);
+    const int r = kCl ? (int)cluster_rank() : (kT == 2 ? (int)(blockIdx.x & 1) : 0);   // tile of the unit
+    const bool leader = !kCl || r == 0;            // issues the MMAs (the pair's rank 0)
+    const int c = kT == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // CTA (pair) index
+    const int cta = (int)blockIdx.x;
+    const int w0 = c * g.vw, w1 = min(w0 + g.vw, g.G);   // workers of this CTA (pair)
     pdl_trigger();                                 // let the next kernel's CTAs get scheduled
-    if (u0 >= u1) return;                          // uniform for the whole CTA (and pair)
+    if (w0 >= w1) return;                          // uniform for the whole CTA (and pair)
+    const uint64_t u0 = ubeg(g, w0), u1 = ubeg(g, w1);
     if (threadIdx.x == 0) stamp(g, cta, 0);        // phase 0: CTA start
     uint32_t nbuf = 32;                            // TMEM columns per accumulator: pow2 >= max(32, Mp)
     while ((int)nbuf < g.Mp) nbuf <<= 1;
@@ -193,12 +209,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tmem_full[b], 1);
-            mbar_init(&tmem_empty[b], kPair ? 8 : 4);   // one arrive per epilogue warp (of both CTAs)
+            mbar_init(&tmem_empty[b], kCl ? 8 : 4);   // one arrive per epilogue warp (of both CTAs)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
-        if (kPair) {
+        if (kCl) {
             asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                          "r"(ncols));
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
@@ -209,27 +225,38 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    if (kPair) cluster_sync_all();                 // the peer's barriers exist before any remote arrive
+    if (kCl) cluster_sync_all();                   // the peer's barriers exist before any remote arrive
     else __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem_base = *tmem_slot;
     // leader's stage barriers: TMA bytes of both CTAs land there (pair mode)
-    const uint32_t stage_bytes = kPair ? 2 * (kTileABytes + tile_b_bytes) : kTileABytes + tile_b_bytes;
+    const uint32_t stage_bytes = kCl ? 2 * (kTileABytes + tile_b_bytes) : kTileABytes + tile_b_bytes;
 
     if (warp == 0) {
-        if (lane == 0) {                           // ---- TMA producer: continuous across tiles
+        if (lane == 0) {                           // ---- TMA producer: continuous across tiles and workers
+            const uint64_t pol_w = l2_policy_evict_first(), pol_x = l2_policy_evict_last();
             auto load_w = [&](int s, uint64_t u, int kbi) {
                 const int tile = TM::tile(u, g.kb, r);
                 const int si = seg_of(g, tile);
                 const CUtensorMap* mw = si == 0 ? &map_w0 : (si == 1 ? &map_w1 : &map_w2);
-                if (kPair)                         // rows past the last tile (odd tile count) are zero-filled
-                    tma_load_2d_pair(sa + s * kTileABytes, mw, leader_addr(&full[s]), kbi * kBK, (tile - g.seg[si].tile0) * kBN);
-                else
-                    tma_load_2d(sa + s * kTileABytes, mw, &full[s], kbi * kBK, (tile - g.seg[si].tile0) * kBN);
+                const int c0 = kbi * kBK, c1 = (tile - g.seg[si].tile0) * kBN;
+                // rows past the last tile (odd tile count, pair split) are zero-filled by TMA
+                if (kCl) {
+                    if (g.l2hint) tma_load_2d_pair_hint(sa + s * kTileABytes, mw, leader_addr(&full[s]), c0, c1, pol_w);
+                    else tma_load_2d_pair(sa + s * kTileABytes, mw, leader_addr(&full[s]), c0, c1);
+                } else {
+                    if (g.l2hint) tma_load_2d_hint(sa + s * kTileABytes, mw, &full[s], c0, c1, pol_w);
+                    else tma_load_2d(sa + s * kTileABytes, mw, &full[s], c0, c1);
+                }
             };
             auto load_x = [&](int s, int kbi) {
-                if (kPair) tma_load_2d_pair(sb + s * tile_b_bytes, &map_x, leader_addr(&full[s]), kbi * kBK, r * xrows);
-                else tma_load_2d(sb + s * tile_b_bytes, &map_x, &full[s], kbi * kBK, 0);
+                if (kCl) {
+                    if (g.l2hint) tma_load_2d_pair_hint(sb + s * tile_b_bytes, &map_x, leader_addr(&full[s]), kbi * kBK, r * xrows, pol_x);
+                    else tma_load_2d_pair(sb + s * tile_b_bytes, &map_x, leader_addr(&full[s]), kbi * kBK, r * xrows);
+                } else {
+                    if (g.l2hint) tma_load_2d_hint(sb + s * tile_b_bytes, &map_x, &full[s], kbi * kBK, 0, pol_x);
+                    else tma_load_2d(sb + s * tile_b_bytes, &map_x, &full[s], kbi * kBK, 0);
+                }
             };
             // Weights do not depend on the previous kernel: the first kStages weight tiles are in
             // flight before griddepcontrol.wait, overlapping the previous kernel's tail (PDL).
@@ -271,14 +298,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             // kind::f16: D fp32 (c_format 1), A = B = bf16 (format 1), both K-major,
             // N = Mp (n_dim = N >> 3), M = 128 / 256 (m_dim = M >> 4)
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(g.Mp >> 3) << 17) |
-                                   ((uint32_t)((kBN * TM::kT) >> 4) << 24);
+                                   ((uint32_t)((kBN * (kCl ? 2 : 1)) >> 4) << 24);
             int run = 0;
             uint32_t tmem_d = tmem_base;
             int s = 0, kbi = (int)(u0 % g.kb);
             uint32_t ph = 0;
+            int w = w0;
+            uint64_t wend = ubeg(g, w0 + 1);       // end of the current worker's range
             for (uint64_t u = u0; u < u1; ++u) {
-                const bool first = u == u0 || kbi == 0;
-                const bool last = u + 1 == u1 || kbi == g.kb - 1;
+                bool wstart = false;
+                while (u >= wend) { ++w; wend = ubeg(g, w + 1); wstart = true; }
+                const bool first = u == u0 || kbi == 0 || wstart;
+                const bool last = u + 1 == u1 || kbi == g.kb - 1 || u + 1 == wend;
                 if (first) {
                     const int b = nacc == 2 ? (run & 1) : 0;
                     const int use = nacc == 2 ? (run >> 1) : run;       // previous uses of buffer b
@@ -292,13 +323,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                 const uint32_t a0 = smem_u32(sa + s * kTileABytes), b0 = smem_u32(sb + s * tile_b_bytes);
 #pragma unroll
                 for (int kk = 0; kk < kBK / 16; ++kk) {
-                    if (kPair) umma_bf16_pair(tmem_d, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, (!first || kk) ? 1u : 0u);
+                    if (kCl) umma_bf16_pair(tmem_d, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, (!first || kk) ? 1u : 0u);
                     else umma_bf16(tmem_d, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, (!first || kk) ? 1u : 0u);
                 }
-                if (kPair) umma_commit_pair(&empty[s]);   // both CTAs' stage s free once read
+                if (kCl) umma_commit_pair(&empty[s]);   // both CTAs' stage s free once read
                 else umma_commit(&empty[s]);
                 if (last) {                        // accumulator of this run complete (both CTAs)
-                    if (kPair) umma_commit_pair(&tmem_full[nacc == 2 ? (run & 1) : 0]);
+                    if (kCl) umma_commit_pair(&tmem_full[nacc == 2 ? (run & 1) : 0]);
                     else umma_commit(&tmem_full[nacc == 2 ? (run & 1) : 0]);
                     ++run;
                 }
@@ -311,15 +342,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
         pdl_wait();                                // outputs / partials written only after it
         const int q = warp - 4;                    // TMEM lane quarter of this warp
         const int row = q * 32 + lane;             // row within the 128-row tile
-        const int cfirst_run_ut = (int)(u0 / g.kb);   // first tile (pair) of this worker's range
-        const uint32_t tmem_empty_leader = kPair ? leader_addr(&tmem_empty[0]) : 0;
+        const uint32_t tmem_empty_leader = kCl ? leader_addr(&tmem_empty[0]) : 0;
+        const uint64_t pol_p = l2_policy_evict_last();
         int run = 0;
+        int w = w0;
+        uint64_t wend = ubeg(g, w0 + 1);
         for (uint64_t u = u0; u < u1; ++run) {
+            while (u >= wend) { ++w; wend = ubeg(g, w + 1); }
             const int ut = (int)(u / g.kb);        // unit tile (tile, or tile pair)
-            const int tile = ut * TM::kT + r;
-            const bool phantom = tile >= g.tiles;  // pair mode, odd tile count: zero rows
+            const int tile = ut * kT + r;
+            const bool phantom = tile >= g.tiles;  // pair split, odd tile count: zero rows
             const uint64_t tend = (uint64_t)(ut + 1) * g.kb;
-            const uint64_t rend = u1 < tend ? u1 : tend;
+            const uint64_t rend = wend < tend ? wend : tend;   // a run ends at a tile or worker boundary
             const int si = seg_of(g, phantom ? g.tiles - 1 : tile);
             const TcSeg& seg = g.seg[si];
             const int n = (tile - seg.tile0) * kBN + row;
@@ -327,8 +361,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             const float bias_n = (seg.bias && nvalid) ? __bfloat162float(seg.bias[n]) : 0.f;
             const int c_first = cta_of(g, (uint64_t)ut * g.kb), c_last = cta_of(g, tend - 1);
             const bool whole = c_first == c_last;
-            const int which = ut == cfirst_run_ut ? 0 : 1;
-            float* prow = g.partial + ((size_t)cta * 2 + which) * (size_t)g.Mp * kBN + row;
+            const int which = ut == (int)(ubeg(g, w) / g.kb) ? 0 : 1;
+            float* prow = g.partial + ((size_t)TM::slot(w, r) * 2 + which) * (size_t)g.Mp * kBN + row;
             const int b = nacc == 2 ? (run & 1) : 0;
             const int use = nacc == 2 ? (run >> 1) : run;
             mbar_wait(&tmem_full[b], (uint32_t)use & 1u);
@@ -339,8 +373,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                 tmem_ld16(tmem_base + (uint32_t)b * nbuf + ((uint32_t)(q * 32) << 16) + (uint32_t)col, v);
                 if (phantom) continue;
                 if (!whole) {              // token-major partial: one 128-B store per warp per token
+                    if (g.l2hint) {        // kept in L2 for the fix-up (the weight stream goes first)
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) prow[(size_t)(col + j) * kBN] = v[j];
+                        for (int j = 0; j < 16; ++j) st_hint(prow + (size_t)(col + j) * kBN, v[j], pol_p);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) prow[(size_t)(col + j) * kBN] = v[j];
+                    }
                 } else if (nvalid) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
@@ -350,7 +389,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
-                if (kPair)
+                if (kCl)
                     asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(tmem_empty_leader + (uint32_t)b * 8)
                                  : "memory");
                 else
@@ -358,7 +397,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             }
             if (row == 0 && rend == u1) stamp(g, cta, 6);   // phase 6: last run drained
             if (!whole && !g.ext_fixup && !phantom) {
-                // fix-up: the last CTA to finish a run of this tile sums all runs in k order.
+                // fix-up: the last worker to finish a run of this tile sums all runs in k order.
                 // bar.sync orders the 128 threads' partial stores before thread 0's gpu-scope
                 // acq_rel atomic (release is cumulative); the acquire + bar.sync orders the
                 // reads of the other CTAs' partials after it. No full fences needed.
@@ -371,30 +410,27 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (s_last) {
                     if (nvalid) {
-                        // 8 tokens per step, two runs per iteration: 16 coalesced loads in
+                        // 8 tokens per step, four runs per iteration: 32 coalesced loads in
                         // flight per thread; the sums stay in fixed run (k) order
                         for (int m0 = 0; m0 < g.M; m0 += 8) {
                             float acc[8];
 #pragma unroll
                             for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-                            int cc = c_first;
-                            for (; cc + 1 <= c_last; cc += 2) {
-                                const float* p0 = partial_run<kPair>(g, cc, c_first, ut, r, row) + (size_t)m0 * kBN;
-                                const float* p1 = partial_run<kPair>(g, cc + 1, c_first, ut, r, row) + (size_t)m0 * kBN;
-                                float a[8], bb[8];
+                            for (int cc = c_first; cc <= c_last; cc += 4) {
+                                float t[4][8];
 #pragma unroll
-                                for (int j = 0; j < 8; ++j) a[j] = __ldcg(p0 + j * kBN);
+                                for (int k = 0; k < 4; ++k)
+                                    if (cc + k <= c_last) {
+                                        const float* p = partial_run<kT>(g, cc + k, c_first, ut, r, row) + (size_t)m0 * kBN;
 #pragma unroll
-                                for (int j = 0; j < 8; ++j) bb[j] = __ldcg(p1 + j * kBN);
+                                        for (int j = 0; j < 8; ++j) t[k][j] = __ldcg(p + j * kBN);
+                                    }
 #pragma unroll
-                                for (int j = 0; j < 8; ++j) acc[j] += a[j];
+                                for (int k = 0; k < 4; ++k)
+                                    if (cc + k <= c_last) {
 #pragma unroll
-                                for (int j = 0; j < 8; ++j) acc[j] += bb[j];
-                            }
-                            if (cc == c_last) {
-                                const float* p0 = partial_run<kPair>(g, cc, c_first, ut, r, row) + (size_t)m0 * kBN;
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) acc[j] += __ldcg(p0 + j * kBN);
+                                        for (int j = 0; j < 8; ++j) acc[j] += t[k][j];
+                                    }
                             }
 #pragma unroll
                             for (int j = 0; j < 8; ++j)
@@ -409,11 +445,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    if (kPair) cluster_sync_all();                 // no CTA leaves while its peer may still signal it
+    if (kCl) cluster_sync_all();                   // no CTA leaves while its peer may still signal it
     else __syncthreads();
     if (threadIdx.x == 0) stamp(g, cta, 7);        // phase 7: CTA done
     if (warp == 2) {
-        if (kPair) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
+        if (kCl) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
         else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
     }
 }
@@ -421,12 +457,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
 // Split-tile reduction as its own grid (ext_fixup, large M): CTA (tile, 16-token group), thread =
 // weight row. Same fixed run order as the in-kernel fix-up, so the bits do not depend on which
 // of the two reduces (the choice may follow M; the split itself never does).
-template <bool kPair>
+template <int kT>
 __global__ void __launch_bounds__(kBN) tc_fixup_kernel(TcArgs g) {
     pdl_wait();                                    // every partial of the GEMM is written
     pdl_trigger();
     const int tile = blockIdx.x, row = threadIdx.x, m0 = blockIdx.y * 16;
-    const int ut = tile / TileMap<kPair>::kT, r = tile % TileMap<kPair>::kT;
+    const int ut = tile / kT, r = tile % kT;
     const uint64_t tend = (uint64_t)(ut + 1) * g.kb;
     const int c_first = cta_of(g, (uint64_t)ut * g.kb), c_last = cta_of(g, tend - 1);
     if (c_first == c_last || m0 >= g.M) return;   // whole tile: stored by the GEMM itself
@@ -434,16 +470,26 @@ __global__ void __launch_bounds__(kBN) tc_fixup_kernel(TcArgs g) {
     const int n = (tile - seg.tile0) * kBN + row;
     if (n >= seg.N) return;
     const float bias_n = seg.bias ? __bfloat162float(seg.bias[n]) : 0.f;
+    // 4 runs x 16 tokens = 64 coalesced loads in flight per thread, then the adds in fixed run
+    // (k) order: one L2 round trip per 4 runs instead of one per run
     float acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-    for (int cc = c_first; cc <= c_last; ++cc) {
-        const float* p = partial_run<kPair>(g, cc, c_first, ut, r, row) + (size_t)m0 * kBN;
-        float t[16];
+    for (int cc = c_first; cc <= c_last; cc += 4) {
+        float t[4][16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) t[j] = __ldcg(p + j * kBN);
+        for (int k = 0; k < 4; ++k)
+            if (cc + k <= c_last) {
+                const float* p = partial_run<kT>(g, cc + k, c_first, ut, r, row) + (size_t)m0 * kBN;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] += t[j];
+                for (int j = 0; j < 16; ++j) t[k][j] = __ldcg(p + j * kBN);
+            }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (cc + k <= c_last) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[j] += t[k][j];
+            }
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j)
@@ -575,19 +621,54 @@ static int tc_align() {
     return v;
 }
 
-// CTA-pair mode (cta_group::2, see tc_gemm_kernel<true>): one process-wide choice, never a
-// function of M, so the split and the reduction order stay batch-invariant. MPSW_TC_PAIR
-// overrides the default (dev / A-B measurement).
+// Split (process-wide, never a function of M, so the split and the reduction order are
+// batch-invariant): tiles per work unit, 1 = (tile, k-block) units, 2 = (tile pair, k-block)
+// units. The pair split can run on independent CTAs or on CTA pairs with the same bits, so the
+// execution may follow M (tc_exec). MPSW_TC_SPLIT overrides the default; MPSW_TC_PAIR=1 is the
+// round-2 A/B mode (pair split, always CTA pairs, one worker per pair).
 int tc_pair() {
     static int v = env_int("MPSW_TC_PAIR", 0);
     return v;
 }
+int tc_split_kt() {
+    static int v = [] {
+        if (tc_pair()) return 2;
+        const int e = env_int("MPSW_TC_SPLIT", 2);
+        return e == 1 ? 1 : 2;
+    }();
+    return v;
+}
 
-// Workers (CTAs, or CTA pairs in pair mode) of a GEMM with `tiles` 128-row tiles: stream-K over
-// the (tile or pair, k-block) units with at least tc_min_units() units per worker and at most
-// tc_ctas_per_sm() x #SMs CTAs, or the tile-aligned split when it keeps >= 80 % of that grid.
+// Execution of one launch: CTA pairs (cta_group::2) or independent CTAs, workers per CTA (pair),
+// resident CTAs per SM (smem budget, TMEM accumulator buffers).
+struct TcExec {
+    bool cl;
+    int vw;
+    int cps;
+};
+// Padded token rows from which the pair split runs on CTA pairs, one CTA per SM with two
+// workers each: at large M the token tile dominates the L2 -> smem traffic (a CTA pair halves
+// it), and one CTA per SM double-buffers the 256-column accumulator and gets a 6-deep ring.
+static int tc_cl_min_mp() {
+    static int v = env_int("MPSW_TC_CL_MIN", 192);
+    return v;
+}
+static TcExec tc_exec(int Mp) {
+    const int cps = tc_ctas_per_sm();
+    if (tc_split_kt() == 1) return {false, 1, cps};
+    if (tc_pair()) return {true, 1, cps};
+    if (Mp >= tc_cl_min_mp()) {
+        static const int vw = std::max(1, env_int("MPSW_TC_VW", 1));
+        return {true, vw, std::max(1, cps / vw)};
+    }
+    return {false, 1, cps};
+}
+
+// Workers of a GEMM with `tiles` 128-row tiles: stream-K over the (unit tile, k-block) units with
+// at least tc_min_units() units per worker and at most tc_ctas_per_sm() x #SMs CTAs (a worker of
+// the pair split is two CTAs), or the tile-aligned split when it keeps >= 80 % of that grid.
 static int tc_grid(int tiles, int K) {
-    const int kt = tc_pair() ? 2 : 1;
+    const int kt = tc_split_kt();
     const int ut = (tiles + kt - 1) / kt;          // unit tiles (tiles or pairs)
     const int kb = (K + kBK - 1) / kBK;
     const uint64_t units = (uint64_t)ut * kb;
@@ -611,43 +692,44 @@ static int tc_grid(int tiles, int K) {
 
 size_t tc_partial_floats(int n_total, int K, int Mp) {
     const int tiles = (n_total + kBN - 1) / kBN;
-    const int kt = tc_pair() ? 2 : 1;
-    return (size_t)tc_grid(tiles, K) * kt * 2 * kBN * Mp;
+    return (size_t)tc_grid(tiles, K) * tc_split_kt() * 2 * kBN * Mp;
 }
 
-// Token rows of the B tile one CTA holds: Mp, or Mp / 2 in pair mode (N split across the pair).
-static int tc_xrows(int Mp) { return tc_pair() ? Mp / 2 : Mp; }
+// Token rows of the B tile one CTA holds: Mp, or Mp / 2 on a CTA pair (N split across the pair).
+static int tc_xrows(const TcExec& e, int Mp) { return e.cl ? Mp / 2 : Mp; }
 
-// Stages sized so that two CTAs fit per SM (<= ~110 KB each).
-int tc_stages(int Mp) {
+// Ring stages within the per-CTA smem budget (MPSW_TC_SMEM_KB per CTA at 2 CTAs per SM, twice that
+// at one CTA per SM).
+static int tc_stages(const TcExec& e, int Mp) {
     static int budget_kb = env_int("MPSW_TC_SMEM_KB", 104);
-    const size_t per = kTileABytes + (size_t)tc_xrows(Mp) * kBK * 2;
-    return (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, ((size_t)budget_kb * 1024) / per));
+    const size_t budget = (size_t)budget_kb * 1024 * (e.cps == 1 ? 2 : 1);
+    const size_t per = kTileABytes + (size_t)tc_xrows(e, Mp) * kBK * 2;
+    return (int)std::max<size_t>(2, std::min<size_t>(kMaxStages, budget / per));
 }
 
-size_t tc_smem_bytes(int Mp) {
-    return 1024 + tc_stages(Mp) * (kTileABytes + (size_t)tc_xrows(Mp) * kBK * 2) + (2 * kMaxStages + 4) * 8 + 16;
+static size_t tc_smem_bytes(const TcExec& e, int Mp) {
+    return 1024 + tc_stages(e, Mp) * (kTileABytes + (size_t)tc_xrows(e, Mp) * kBK * 2) + (2 * kMaxStages + 4) * 8 + 16;
 }
 
 static unsigned long long* g_tc_trace = nullptr;   // dev instrumentation (mpsw_bench_gemm only)
 void tc_set_trace(unsigned long long* p) { g_tc_trace = p; }
-// CTAs launched for a GEMM (pair mode: 2 per worker)
-int tc_grid_for(int n_total, int K) { return tc_grid((n_total + kBN - 1) / kBN, K) * (tc_pair() ? 2 : 1); }
+// CTAs a GEMM launches at most (any M): G workers x tiles per unit
+int tc_grid_for(int n_total, int K) { return tc_grid((n_total + kBN - 1) / kBN, K) * tc_split_kt(); }
 int tc_grid_tiles(int tiles, int K) { return tc_grid(tiles, K); }
 
 bool tc_supported(int M, int K) { return M >= 1 && M <= 256 && K % 8 == 0; }
 
-template <bool kPair>
+template <int kT, bool kCl>
 static void launch_tc(const TcArgs& g, size_t smem, cudaStream_t st, const CUtensorMap& m0, const CUtensorMap& m1,
                       const CUtensorMap& m2, const CUtensorMap& mx) {
     static thread_local size_t attr_set = 0;
     if (attr_set < smem) {
-        MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel<kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel<kPair>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel<kT, kCl>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        MPSW_CU(cudaFuncSetAttribute(tc_gemm_kernel<kT, kCl>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr_set = smem;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(g.G * (kPair ? 2 : 1));
+    cfg.gridDim = dim3(kCl ? 2 * ((g.G + g.vw - 1) / g.vw) : g.G * kT);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -655,13 +737,15 @@ static void launch_tc(const TcArgs& g, size_t smem, cudaStream_t st, const CUten
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     at[1].id = cudaLaunchAttributeClusterDimension;
-    at[1].val.clusterDim.x = kPair ? 2 : 1;
+    at[1].val.clusterDim.x = kCl ? 2 : 1;
     at[1].val.clusterDim.y = 1;
     at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = kPair ? 2 : 1;
-    MPSW_CU(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<kPair>, m0, m1, m2, mx, g));
-    if (g.ext_fixup) launch_pdl(tc_fixup_kernel<kPair>, dim3(g.tiles, g.Mp / 16), kBN, 0, st, g);
+    cfg.numAttrs = kCl ? 2 : 1;
+    MPSW_CU(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<kT, kCl>, m0, m1, m2, mx, g));
+    // MPSW_DEV_NOOP_FIXUP: timing instrumentation only (split tiles are left unreduced)
+    static const bool noop_fixup = env_int("MPSW_DEV_NOOP_FIXUP", 0) != 0;
+    if (g.ext_fixup && !noop_fixup) launch_pdl(tc_fixup_kernel<kT>, dim3(g.tiles, g.Mp / 16), kBN, 0, st, g);
 }
 
 // Launch: W segments (up to 3, each [N_i, K] bf16) times X [M, K] bf16 (rows of a buffer with
@@ -671,9 +755,10 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
              int nseg, const void* X, int x_rows, int M, int K, int epi, void* out, int ldo, const int32_t* row_of_m,
              float* partial, int* counters, cudaStream_t st) {
     const int Mp = std::max(16, (M + 15) / 16 * 16);
-    const bool pair = tc_pair() != 0;
+    const int kt = tc_split_kt();
+    const TcExec ex = tc_exec(Mp);
     TcArgs g{};
-    int tiles = 0, n_total = 0;
+    int tiles = 0;
     for (int i = 0; i < nseg; ++i) {
         g.seg[i].N = N[i];
         g.seg[i].tile0 = tiles;
@@ -681,17 +766,17 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
         g.seg[i].scale = scale[i];
         g.seg[i].out_col0 = out_col0[i];
         tiles += (N[i] + kBN - 1) / kBN;
-        n_total += N[i];
     }
     g.nseg = nseg;
     g.tiles = tiles;
     g.kb = (K + kBK - 1) / kBK;
-    g.units = (uint64_t)(pair ? (tiles + 1) / 2 : tiles) * g.kb;
+    g.units = (uint64_t)((tiles + kt - 1) / kt) * g.kb;
     g.G = tc_grid(tiles, K);
+    g.vw = ex.vw;
     g.K = K;
     g.M = M;
     g.Mp = Mp;
-    g.stages = tc_stages(Mp);
+    g.stages = tc_stages(ex, Mp);
     g.epi = epi;
     g.out = out;
     g.ldo = ldo;
@@ -701,19 +786,22 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
     const CUtensorMap& m0 = cached_map(W[0], N[0], K, kBN);
     const CUtensorMap& m1 = cached_map(W[nseg > 1 ? 1 : 0], N[nseg > 1 ? 1 : 0], K, kBN);
     const CUtensorMap& m2 = cached_map(W[nseg > 2 ? 2 : 0], N[nseg > 2 ? 2 : 0], K, kBN);
-    const CUtensorMap& mx = cached_map(X, (uint64_t)x_rows, K, (uint32_t)tc_xrows(Mp));
-    const size_t smem = tc_smem_bytes(Mp);
+    const CUtensorMap& mx = cached_map(X, (uint64_t)x_rows, K, (uint32_t)tc_xrows(ex, Mp));
+    const size_t smem = tc_smem_bytes(ex, Mp);
     g.ext_fixup = Mp >= tc_ext_fixup_min() ? 1 : 0;
     g.trace = g_tc_trace;
     g.l2_prefetch = tc_l2_prefetch();
+    static const int l2hint = env_int("MPSW_TC_L2HINT", 1);
+    g.l2hint = l2hint;
     int nbuf = 32;
     while (nbuf < Mp) nbuf <<= 1;
-    g.nacc = 2 * nbuf * tc_ctas_per_sm() <= 512 ? 2 : 1;
-    if (pair) {
-        launch_tc<true>(g, smem, st, m0, m1, m2, mx);
-    } else {
-        launch_tc<false>(g, smem, st, m0, m1, m2, mx);
-    }
+    g.nacc = 2 * nbuf * ex.cps <= 512 ? 2 : 1;
+    if (kt == 1)
+        launch_tc<1, false>(g, smem, st, m0, m1, m2, mx);
+    else if (ex.cl)
+        launch_tc<2, true>(g, smem, st, m0, m1, m2, mx);
+    else
+        launch_tc<2, false>(g, smem, st, m0, m1, m2, mx);
     MPSW_CU(cudaGetLastError());
 }
 

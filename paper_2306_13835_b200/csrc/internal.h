@@ -106,7 +106,8 @@ void tc_set_trace(unsigned long long* p);
 int tc_grid_for(int n_total, int K);
 int tc_grid_tiles(int tiles, int K);     // stream-K CTAs of a GEMM with `tiles` 128-row tiles
 bool tc_supported(int M, int K);
-int tc_pair();                           // 1: the GEMMs run as CTA pairs (cta_group::2)
+int tc_pair();                           // 1: A/B mode: pair split, always on CTA pairs (cta_group::2)
+int tc_split_kt();                       // tiles per stream-K work unit (1 or 2), process-wide
 void tc_gemm(const void* const* W, const void* const* bias, const int* N, const float* scale, const int* out_col0,
              int nseg, const void* X, int x_rows, int M, int K, int epi, void* out, int ldo, const int32_t* row_of_m,
              float* partial, int* counters, cudaStream_t st);

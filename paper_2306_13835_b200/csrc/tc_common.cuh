@@ -61,6 +61,32 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// L2 eviction-priority policies (createpolicy): the weight stream is read once per forward
+// (evict_first keeps it from pushing the activations and split-K partials out of L2); the token
+// tile and the partials are re-read (evict_last).
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(pol)
+        : "memory");
+}
+
+__device__ __forceinline__ void st_hint(float* p, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+
 // K-major, 128B-swizzled canonical UMMA layout: 8-row x 128 B atoms stacked along rows
 // (SBO = 1024 B), LBO unused (1), descriptor version 1 (sm_100), layout type 2 = SWIZZLE_128B.
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
@@ -152,8 +178,6 @@ __device__ __forceinline__ void epi_value_store(int epi, void* out, size_t idx, 
 CUtensorMap tc_make_map(const void* ptr, uint64_t rows, uint64_t K, uint32_t box_rows);
 int sm_count();
 int tc_ctas_per_sm();
-int tc_stages(int Mp);
-size_t tc_smem_bytes(int Mp);
 CUtensorMap tc_make_map_3d(const void* ptr, uint64_t rows, uint64_t K, uint64_t layers, uint64_t layer_stride,
                            uint32_t box_rows);
 

@@ -1,7 +1,7 @@
 """GEMM microbenchmark sweep (dev): per-layer GEMM shapes of OPT-13B / OPT-1.3B at TP1 x M, for
 tuning knobs given by env vars. Each configuration runs in a fresh process (knobs are read once).
 
-usage: python tools/gemm_tune.py [default|ext|grid|l2pf|smem|align|pair]"""
+usage: python tools/gemm_tune.py [default|ext|grid|l2pf|smem|align|pair|split]"""
 import json, os, subprocess, sys
 MODELS = {"opt-13b": {"qkv": (15360, 5120), "out": (5120, 5120), "fc1": (20480, 5120), "fc2": (5120, 20480)},
           "opt-1.3b": {"qkv": (6144, 2048), "out": (2048, 2048), "fc1": (8192, 2048), "fc2": (2048, 8192)},
@@ -11,7 +11,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     from paper_2306_13835_b200 import mpsw as M
     impl = int(sys.argv[2])
     for model in sys.argv[3].split(","):
-        for Mt in (2, 16, 64, 256):
+        for Mt in [int(x) for x in os.environ.get("GT_M", "2,16,64,256").split(",")]:
             row = {"model": model, "M": Mt, "impl": impl,
                    "env": {k: v for k, v in os.environ.items() if k.startswith("MPSW_TC")}}
             tot = 0
@@ -41,6 +41,23 @@ elif mode == "pair":
     models = "opt-13b,opt-1.3b,opt-125m"
     configs = [("2", {"MPSW_TC_PAIR": v}) for v in ("0", "1")] + [("2", {"MPSW_TC_PAIR": "1", "MPSW_TC_SMEM_KB": v})
                                                                  for v in ("88", "112")]
+elif mode == "split":
+    models = "opt-13b,opt-1.3b,opt-125m"
+    configs = [("2", {"MPSW_TC_SPLIT": "1"}), ("2", {"MPSW_TC_SPLIT": "2", "MPSW_TC_CL_MIN": "100000"}),
+               ("2", {"MPSW_TC_SPLIT": "2"}), ("2", {"MPSW_TC_SPLIT": "2", "MPSW_TC_CL_MIN": "64"}),
+               ("2", {"MPSW_TC_SPLIT": "2", "MPSW_TC_VW": "1"})]
+elif mode == "large":
+    models = "opt-13b,opt-1.3b"
+    base = {"MPSW_TC_SPLIT": "2", "MPSW_TC_VW": "1"}
+    configs = [("2", dict(base))] + [("2", dict(base, MPSW_TC_L2PF=v)) for v in ("4", "8", "16")] + \
+              [("2", dict(base, MPSW_TC_EXT_MIN="100000")), ("2", dict(base, MPSW_TC_CL_MIN="64")),
+               ("2", dict(base, MPSW_TC_SMEM_KB="112"))]
+elif mode == "rings":
+    models = "opt-13b,opt-1.3b"
+    configs = [("2", {"MPSW_TC_SPLIT": "1"}), ("2", {"MPSW_TC_SPLIT": "2", "MPSW_TC_CL_MIN": "100000"}),
+               ("2", {"MPSW_TC_SPLIT": "2", "MPSW_TC_VW": "1"}), ("2", {"MPSW_TC_SPLIT": "2", "MPSW_TC_VW": "2"}),
+               ("2", {"MPSW_TC_SPLIT": "2", "MPSW_TC_VW": "2", "MPSW_TC_STAGE_MIN": "64"}),
+               ("2", {"MPSW_TC_SPLIT": "2", "MPSW_TC_VW": "1", "MPSW_TC_WPRE": "4"})]
 elif mode == "grid":
     models = "opt-13b,opt-1.3b"
     configs = [("2", {}), ("2", {"MPSW_TC_CPS": "1", "MPSW_TC_SMEM_KB": "200"}), ("1", {})]
