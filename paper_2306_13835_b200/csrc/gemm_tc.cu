@@ -63,10 +63,12 @@ __device__ __forceinline__ void stamp(const TcArgs& g, int c, int i) {
 
 // Stream-K work split: worker w owns units [ubeg(w), ubeg(w+1)) of the linearised (unit tile,
 // k-block) space. Depends only on (units, G) — never on M — so it is batch-invariant.
-__device__ __forceinline__ uint64_t ubeg(const TcArgs& g, int c) { return (uint64_t)c * g.units / (uint64_t)g.G; }
+// 32-bit arithmetic: units * G < 2^32 (checked on the host); 64-bit divisions cost ~100
+// instructions each and sat in front of every fix-up load.
+__device__ __forceinline__ uint64_t ubeg(const TcArgs& g, int c) { return (uint32_t)c * (uint32_t)g.units / (uint32_t)g.G; }
 
 __device__ __forceinline__ int cta_of(const TcArgs& g, uint64_t u) {
-    int c = (int)(u * (uint64_t)g.G / g.units);
+    int c = (int)((uint32_t)u * (uint32_t)g.G / (uint32_t)g.units);
     while (c + 1 < g.G && ubeg(g, c + 1) <= u) ++c;
     while (c > 0 && ubeg(g, c) > u) --c;
     return c;
@@ -81,10 +83,14 @@ template <int kT> struct TileMap {
 
 // Partial run of worker cc on a split tile: slot 0 if the tile is cc's first unit tile, else 1
 // (a worker touches at most two split unit tiles: where its range starts and where it ends).
+// first_wh: the slot of c_first's run (first_slot below), computed once per tile.
 template <int kT>
-__device__ __forceinline__ const float* partial_run(const TcArgs& g, int cc, int c_first, int unit_tile, int r, int row) {
-    const int wh = (cc == c_first && (int)(ubeg(g, c_first) / g.kb) != unit_tile) ? 1 : 0;
+__device__ __forceinline__ const float* partial_run(const TcArgs& g, int cc, int c_first, int first_wh, int r, int row) {
+    const int wh = cc == c_first ? first_wh : 0;
     return g.partial + ((size_t)TileMap<kT>::slot(cc, r) * 2 + wh) * (size_t)g.Mp * kBN + row;
+}
+__device__ __forceinline__ int first_slot(const TcArgs& g, int c_first, int unit_tile) {
+    return (int)((uint32_t)ubeg(g, c_first) / (uint32_t)g.kb) != unit_tile ? 1 : 0;
 }
 
 __device__ __forceinline__ void epi_store(const TcArgs& g, const TcSeg& seg, int n, int m, float x, float bias_n) {
@@ -361,7 +367,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
             const float bias_n = (seg.bias && nvalid) ? __bfloat162float(seg.bias[n]) : 0.f;
             const int c_first = cta_of(g, (uint64_t)ut * g.kb), c_last = cta_of(g, tend - 1);
             const bool whole = c_first == c_last;
-            const int which = ut == (int)(ubeg(g, w) / g.kb) ? 0 : 1;
+            const int fwh = whole ? 0 : first_slot(g, c_first, ut);
+            const int which = ut == (int)((uint32_t)ubeg(g, w) / (uint32_t)g.kb) ? 0 : 1;
             float* prow = g.partial + ((size_t)TM::slot(w, r) * 2 + which) * (size_t)g.Mp * kBN + row;
             const int b = nacc == 2 ? (run & 1) : 0;
             const int use = nacc == 2 ? (run >> 1) : run;
@@ -421,7 +428,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
                                     if (cc + k <= c_last) {
-                                        const float* p = partial_run<kT>(g, cc + k, c_first, ut, r, row) + (size_t)m0 * kBN;
+                                        const float* p = partial_run<kT>(g, cc + k, c_first, fwh, r, row) + (size_t)m0 * kBN;
 #pragma unroll
                                         for (int j = 0; j < 8; ++j) t[k][j] = __ldcg(p + j * kBN);
                                     }
@@ -466,6 +473,7 @@ __global__ void __launch_bounds__(kBN) tc_fixup_kernel(TcArgs g) {
     const uint64_t tend = (uint64_t)(ut + 1) * g.kb;
     const int c_first = cta_of(g, (uint64_t)ut * g.kb), c_last = cta_of(g, tend - 1);
     if (c_first == c_last || m0 >= g.M) return;   // whole tile: stored by the GEMM itself
+    const int fwh = first_slot(g, c_first, ut);
     const TcSeg& seg = g.seg[seg_of(g, tile)];
     const int n = (tile - seg.tile0) * kBN + row;
     if (n >= seg.N) return;
@@ -480,7 +488,7 @@ __global__ void __launch_bounds__(kBN) tc_fixup_kernel(TcArgs g) {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
             if (cc + k <= c_last) {
-                const float* p = partial_run<kT>(g, cc + k, c_first, ut, r, row) + (size_t)m0 * kBN;
+                const float* p = partial_run<kT>(g, cc + k, c_first, fwh, r, row) + (size_t)m0 * kBN;
 #pragma unroll
                 for (int j = 0; j < 16; ++j) t[k][j] = __ldcg(p + j * kBN);
             }
@@ -772,6 +780,7 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
     g.kb = (K + kBK - 1) / kBK;
     g.units = (uint64_t)((tiles + kt - 1) / kt) * g.kb;
     g.G = tc_grid(tiles, K);
+    if (g.units * (uint64_t)g.G >= (1ull << 32)) throw Error(MPSW_EINVAL, "tcgen05 GEMM too large for the 32-bit split");
     g.vw = ex.vw;
     g.K = K;
     g.M = M;
