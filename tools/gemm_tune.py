@@ -58,6 +58,11 @@ elif mode == "rings":
                ("2", {"MPSW_TC_SPLIT": "2", "MPSW_TC_VW": "1"}), ("2", {"MPSW_TC_SPLIT": "2", "MPSW_TC_VW": "2"}),
                ("2", {"MPSW_TC_SPLIT": "2", "MPSW_TC_VW": "2", "MPSW_TC_STAGE_MIN": "64"}),
                ("2", {"MPSW_TC_SPLIT": "2", "MPSW_TC_VW": "1", "MPSW_TC_WPRE": "4"})]
+elif mode == "knobs2":
+    models = "opt-13b,opt-1.3b,opt-125m"
+    configs = [("2", {})] + [("2", {"MPSW_TC_L2PF": v}) for v in ("2", "4")] + \
+              [("2", {"MPSW_TC_EXT_MIN": v}) for v in ("32", "48", "128")] + \
+              [("2", {"MPSW_TC_MINU": v}) for v in ("6", "12")] + [("2", {"MPSW_TC_CL_MIN": "128"})]
 elif mode == "grid":
     models = "opt-13b,opt-1.3b"
     configs = [("2", {}), ("2", {"MPSW_TC_CPS": "1", "MPSW_TC_SMEM_KB": "200"}), ("1", {})]
