@@ -5,7 +5,9 @@ usage: python tools/gemm_tune.py [default|ext|grid|l2pf|smem|align|pair|split]""
 import json, os, subprocess, sys
 MODELS = {"opt-13b": {"qkv": (15360, 5120), "out": (5120, 5120), "fc1": (20480, 5120), "fc2": (5120, 20480)},
           "opt-1.3b": {"qkv": (6144, 2048), "out": (2048, 2048), "fc1": (8192, 2048), "fc2": (2048, 8192)},
-          "opt-125m": {"qkv": (2304, 768), "out": (768, 768), "fc1": (3072, 768), "fc2": (768, 3072)}}
+          "opt-125m": {"qkv": (2304, 768), "out": (768, 768), "fc1": (3072, 768), "fc2": (768, 3072)},
+          # cfg4's per-rank shapes (OPT-30B at TP 8; QKV as one GEMM of its three 896-row segments)
+          "opt-30b-tp8": {"qkv": (2688, 7168), "out": (7168, 896), "fc1": (3584, 7168), "fc2": (7168, 3584)}}
 if len(sys.argv) > 1 and sys.argv[1] == "child":
     sys.path.insert(0, ".")
     from paper_2306_13835_b200 import mpsw as M
