@@ -28,6 +28,18 @@ mpsw_status mpsw_test_gemm(int device, int dtype, int impl, const void* W, const
  * allocated, filled with a constant and freed inside. */
 mpsw_status mpsw_bench_gemm(int device, int impl, int M, int N, int K, int reps, float* us);
 
+/* Launch plan of one tcgen05 GEMM (host-side arithmetic only: no device, no CUDA call beyond the
+ * SM-count query, which falls back to 148 without a GPU). For N output rows (the sum of the
+ * segments' tile-rounded rows), K, M tokens (1..256) it returns in plan[12]:
+ *   [0] workers G of the stream-K split   [1] tiles per work unit (1 / 2)   [2] unit tiles
+ *   [3] k-blocks per tile                 [4] CTAs launched                 [5] 1 = CTA pairs
+ *   [6] ring stages                       [7] dynamic smem bytes per CTA    [8] TMEM columns per CTA
+ *   [9] split-tile reducer (0 in-kernel, 1 fix-up grid)                    [10] CTAs per SM (budget)
+ *   [11] padded tokens Mp
+ * The split ([0]-[3]) must not depend on M (batch invariance); tests/test_capi_cpu.py checks this
+ * and the resource bounds. Errors: EINVAL. */
+mpsw_status mpsw_tc_plan(int N, int K, int M, int64_t* plan);
+
 /* Intermediate-value tap of the TP forward (a6), for element-by-element parity with the oracle's
  * per-layer values (oracle/forward.py `taps`). Arms a ONE-SHOT tap on `ctx`: the next batch the
  * engine dispatches runs the same kernels as a normal batch (per-op path: the fused layers kernel

@@ -461,14 +461,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap map_w0, const __grid_constant
     }
 }
 
-// Split-tile reduction as its own grid (ext_fixup, large M): CTA (tile, 16-token group), thread =
+// Split-tile reduction as its own grid (ext_fixup, large M): CTA (tile, kTok-token group), thread =
 // weight row. Same fixed run order as the in-kernel fix-up, so the bits do not depend on which
 // of the two reduces (the choice may follow M; the split itself never does).
-template <int kT>
+template <int kT, int kTok>
 __global__ void __launch_bounds__(kBN) tc_fixup_kernel(TcArgs g) {
     pdl_wait();                                    // every partial of the GEMM is written
     pdl_trigger();
-    const int tile = blockIdx.x, row = threadIdx.x, m0 = blockIdx.y * 16;
+    const int tile = blockIdx.x, row = threadIdx.x, m0 = blockIdx.y * kTok;
     const int ut = tile / kT, r = tile % kT;
     const uint64_t tend = (uint64_t)(ut + 1) * g.kb;
     const int c_first = cta_of(g, (uint64_t)ut * g.kb), c_last = cta_of(g, tend - 1);
@@ -478,29 +478,29 @@ __global__ void __launch_bounds__(kBN) tc_fixup_kernel(TcArgs g) {
     const int n = (tile - seg.tile0) * kBN + row;
     if (n >= seg.N) return;
     const float bias_n = seg.bias ? __bfloat162float(seg.bias[n]) : 0.f;
-    // 4 runs x 16 tokens = 64 coalesced loads in flight per thread, then the adds in fixed run
+    // 4 runs x kTok tokens of coalesced loads in flight per thread, then the adds in fixed run
     // (k) order: one L2 round trip per 4 runs instead of one per run
-    float acc[16];
+    float acc[kTok];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+    for (int j = 0; j < kTok; ++j) acc[j] = 0.f;
     for (int cc = c_first; cc <= c_last; cc += 4) {
-        float t[4][16];
+        float t[4][kTok];
 #pragma unroll
         for (int k = 0; k < 4; ++k)
             if (cc + k <= c_last) {
                 const float* p = partial_run<kT>(g, cc + k, c_first, fwh, r, row) + (size_t)m0 * kBN;
 #pragma unroll
-                for (int j = 0; j < 16; ++j) t[k][j] = __ldcg(p + j * kBN);
+                for (int j = 0; j < kTok; ++j) t[k][j] = __ldcg(p + j * kBN);
             }
 #pragma unroll
         for (int k = 0; k < 4; ++k)
             if (cc + k <= c_last) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) acc[j] += t[k][j];
+                for (int j = 0; j < kTok; ++j) acc[j] += t[k][j];
             }
     }
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
+    for (int j = 0; j < kTok; ++j)
         if (m0 + j < g.M) epi_store(g, seg, n, m0 + j, acc[j], bias_n);
 }
 
@@ -753,7 +753,14 @@ static void launch_tc(const TcArgs& g, size_t smem, cudaStream_t st, const CUten
     MPSW_CU(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<kT, kCl>, m0, m1, m2, mx, g));
     // MPSW_DEV_NOOP_FIXUP: timing instrumentation only (split tiles are left unreduced)
     static const bool noop_fixup = env_int("MPSW_DEV_NOOP_FIXUP", 0) != 0;
-    if (g.ext_fixup && !noop_fixup) launch_pdl(tc_fixup_kernel<kT>, dim3(g.tiles, g.Mp / 16), kBN, 0, st, g);
+    // 8 tokens per fix-up CTA: 56 registers, twice the CTAs of 16 tokens (88 registers) and more of
+    // them resident: OPT-1.3B forward at M = 256 2.67 -> 2.51 ms, OPT-30B TP8 layer 101 -> 94 us
+    // (profiles/r02s3_fixup_grid_shape.ndjson). MPSW_TC_FIX_TOK=16 restores the wider CTA (dev).
+    static const int fix_tok = env_int("MPSW_TC_FIX_TOK", 8) == 16 ? 16 : 8;
+    if (g.ext_fixup && !noop_fixup) {
+        if (fix_tok == 8) launch_pdl(tc_fixup_kernel<kT, 8>, dim3(g.tiles, g.Mp / 8), kBN, 0, st, g);
+        else launch_pdl(tc_fixup_kernel<kT, 16>, dim3(g.tiles, g.Mp / 16), kBN, 0, st, g);
+    }
 }
 
 // Launch: W segments (up to 3, each [N_i, K] bf16) times X [M, K] bf16 (rows of a buffer with
@@ -815,3 +822,31 @@ void tc_gemm(const void* const* W, const void* const* bias, const int* N, const 
 }
 
 }  // namespace mpsw
+
+#include "../../include/mpsw_testing.h"
+
+extern "C" mpsw_status mpsw_tc_plan(int N, int K, int M, int64_t* plan) {
+    using namespace mpsw;
+    if (N < 1 || K < 8 || K % 8 || M < 1 || M > 256 || !plan) return set_error(MPSW_EINVAL, "bad shape");
+    const int Mp = std::max(16, (M + 15) / 16 * 16);
+    const int kt = tc_split_kt();
+    const TcExec ex = tc_exec(Mp);
+    const int tiles = (N + kBN - 1) / kBN;
+    const int G = tc_grid(tiles, K);
+    int nbuf = 32;
+    while (nbuf < Mp) nbuf <<= 1;
+    const int nacc = 2 * nbuf * ex.cps <= 512 ? 2 : 1;
+    plan[0] = G;
+    plan[1] = kt;
+    plan[2] = (tiles + kt - 1) / kt;
+    plan[3] = (K + kBK - 1) / kBK;
+    plan[4] = kt == 1 ? G : (ex.cl ? 2 * ((G + ex.vw - 1) / ex.vw) : 2 * G);
+    plan[5] = ex.cl ? 1 : 0;
+    plan[6] = tc_stages(ex, Mp);
+    plan[7] = (int64_t)tc_smem_bytes(ex, Mp);
+    plan[8] = (int64_t)nacc * nbuf;
+    plan[9] = Mp >= tc_ext_fixup_min() ? 1 : 0;
+    plan[10] = ex.cps;
+    plan[11] = Mp;
+    return MPSW_OK;
+}

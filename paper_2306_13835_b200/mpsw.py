@@ -81,6 +81,7 @@ _SIGS = {
     "mpsw_timeline_dump": [_P, C.c_char_p],
     "mpsw_get_stats": [_P, C.POINTER(Stats)],
     "mpsw_bench_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)],
+    "mpsw_tc_plan": [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)],
     "mpsw_test_gemm": [C.c_int, C.c_int, C.c_int, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float,
                        C.POINTER(C.c_float)],
     "mpsw_test_tap": [_P, C.c_int, C.c_int, C.c_int, _P, C.c_uint64],
@@ -128,6 +129,17 @@ def test_gemm(W, X, bias=None, impl=2, epi=0, scale=1.0, dtype=BF16, device=0):
                                 None if b is None else b.ctypes.data, M, N, K, epi, scale,
                                 out.ctypes.data_as(C.POINTER(C.c_float))))
     return out
+
+
+TC_PLAN_KEYS = ("workers", "tiles_per_unit", "unit_tiles", "kblocks", "ctas", "cta_pairs", "stages", "smem_bytes",
+                "tmem_cols", "fixup_grid", "ctas_per_sm", "mp")
+
+
+def tc_plan(N, K, M):
+    """Launch plan of one tcgen05 GEMM, host arithmetic only (include/mpsw_testing.h)."""
+    out = (C.c_int64 * 12)()
+    _check(lib().mpsw_tc_plan(N, K, M, out))
+    return dict(zip(TC_PLAN_KEYS, (int(v) for v in out)))
 
 
 def bench_gemm(M, N, K, impl=2, reps=20, device=0):

@@ -15,7 +15,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     for model in sys.argv[3].split(","):
         for Mt in [int(x) for x in os.environ.get("GT_M", "2,16,64,256").split(",")]:
             row = {"model": model, "M": Mt, "impl": impl,
-                   "env": {k: v for k, v in os.environ.items() if k.startswith("MPSW_TC")}}
+                   "env": {k: v for k, v in os.environ.items() if k.startswith("MPSW_TC") or k.startswith("MPSW_DEV")}}
             tot = 0
             for name, (N, K) in MODELS[model].items():
                 us = M.bench_gemm(Mt, N, K, impl=impl, reps=10)
@@ -65,6 +65,10 @@ elif mode == "knobs2":
     configs = [("2", {})] + [("2", {"MPSW_TC_L2PF": v}) for v in ("2", "4")] + \
               [("2", {"MPSW_TC_EXT_MIN": v}) for v in ("32", "48", "128")] + \
               [("2", {"MPSW_TC_MINU": v}) for v in ("6", "12")] + [("2", {"MPSW_TC_CL_MIN": "128"})]
+elif mode == "fixup":
+    models = "opt-13b,opt-1.3b,opt-30b-tp8"
+    configs = [("2", {}), ("2", {"MPSW_TC_FIX_TOK": "8"}), ("2", {"MPSW_TC_FIX_EARLY": "1"}),
+               ("2", {"MPSW_TC_FIX_TOK": "8", "MPSW_TC_FIX_EARLY": "1"}), ("2", {"MPSW_DEV_NOOP_FIXUP": "1"})]
 elif mode == "grid":
     models = "opt-13b,opt-1.3b"
     configs = [("2", {}), ("2", {"MPSW_TC_CPS": "1", "MPSW_TC_SMEM_KB": "200"}), ("1", {})]
