@@ -4,7 +4,7 @@
 # --set full of the tcgen05 GEMM at M = 2 and M = 256, forward table, TP8 virtual-rank forward,
 # serving traces (cfg1, cfg4-slice with logits), sanitizers.
 set -x
-O=gpurun_out/final_s3
+O=${OUT:-gpurun_out/final_s3}
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()"
 MPSW_PARITY_LOG=$O/parity.ndjson timeout 2400 python -m pytest tests -m gpu -q -rf --tb=short > $O/pytest_gpu.txt 2>&1
