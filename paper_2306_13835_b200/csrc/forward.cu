@@ -356,121 +356,6 @@ __global__ void __launch_bounds__(kLnThreads) reduce_ln_kernel(Peers peers, cons
     }
 }
 
-// Cluster variant: one row over a cluster of kLnC CTAs (kLnCThreads threads each), CTA rank q
-// owning columns [q*h/kLnC, (q+1)*h/kLnC). Each CTA reduces its columns' sum in a fixed order,
-// the kLnC partials are combined through distributed shared memory in rank order (every CTA
-// computes the same mean / variance), so a row's latency-bound chain is spread over kLnC SMs.
-// Same per-element adds (peers in rank order, + bias, + position, residual + that) and the same
-// LN formula as reduce_ln_kernel; only the order of the row-sum reduction differs, and one model
-// always uses one of the two (chosen by h).
-constexpr int kLnC = 4;
-constexpr int kLnCThreads = 256;
-
-__device__ __forceinline__ float cluster_sum(float v, float* red, float* part) {
-    v = warp_sum(v);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float s = 0.f;
-#pragma unroll
-        for (int i = 0; i < kLnCThreads / 32; ++i) s = __fadd_rn(s, red[i]);
-        *part = s;
-    }
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    float tot = 0.f;
-#pragma unroll
-    for (int q = 0; q < kLnC; ++q) {
-        uint32_t a;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"((uint32_t)__cvta_generic_to_shared(part)), "r"(q));
-        float pq;
-        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(pq) : "r"(a) : "memory");
-        tot = __fadd_rn(tot, pq);
-    }
-    // nobody may overwrite `part` (next reduction) before every CTA has read it
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    return tot;
-}
-
-template <typename T, int VPT>
-__global__ void __launch_bounds__(kLnCThreads) reduce_ln_cluster_kernel(
-    Peers peers, const float* __restrict__ residual, const T* __restrict__ bias, const T* __restrict__ pos_table,
-    const int32_t* __restrict__ pos, const T* __restrict__ gamma, const T* __restrict__ beta, float* __restrict__ x_out,
-    LnDst dst, int h, int row0) {
-    __shared__ float red[kLnCThreads / 32];
-    __shared__ float part;
-    pdl_trigger();
-    uint32_t q;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(q));
-    const int m = row0 + (int)(blockIdx.x / kLnC);
-    const size_t row = (size_t)m * h;
-    const int hc = h / kLnC, c0 = (int)q * hc;          // this CTA's columns
-    const int h4 = hc / 4;
-    float4 bi[VPT], ga[VPT], be[VPT];
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-        const int j4 = threadIdx.x + i * kLnCThreads;
-        if (j4 < h4) {
-            const int col = c0 + 4 * j4;
-            bi[i] = bias ? ld4<T>(bias + col) : make_float4(0.f, 0.f, 0.f, 0.f);
-            ga[i] = ld4<T>(gamma + col);
-            be[i] = ld4<T>(beta + col);
-        }
-    }
-    pdl_wait();
-    float4 x[VPT], rs[VPT], ps[VPT];
-    const T* prow = pos_table ? pos_table + (size_t)pos[m] * h : nullptr;
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-        const int j4 = threadIdx.x + i * kLnCThreads;
-        if (j4 < h4) {
-            const size_t off = row + c0 + 4 * j4;
-            x[i] = *reinterpret_cast<const float4*>(peers.p[0] + off);
-            if (residual) rs[i] = *reinterpret_cast<const float4*>(residual + off);
-            if (prow) ps[i] = ld4<T>(prow + c0 + 4 * j4);
-        }
-    }
-    for (int r = 1; r < peers.n; ++r) {
-        float4 qv[VPT];
-#pragma unroll
-        for (int i = 0; i < VPT; ++i)
-            if (threadIdx.x + i * kLnCThreads < h4)
-                qv[i] = *reinterpret_cast<const float4*>(peers.p[r] + row + c0 + 4 * (threadIdx.x + i * kLnCThreads));
-#pragma unroll
-        for (int i = 0; i < VPT; ++i)
-            if (threadIdx.x + i * kLnCThreads < h4) x[i] = add4(x[i], qv[i]);
-    }
-    float lsum = 0.f;
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-        const int j4 = threadIdx.x + i * kLnCThreads;
-        if (j4 >= h4) break;
-        if (bias) x[i] = add4(x[i], bi[i]);
-        if (prow) x[i] = add4(x[i], ps[i]);
-        if (residual) x[i] = add4(rs[i], x[i]);
-        *reinterpret_cast<float4*>(x_out + row + c0 + 4 * j4) = x[i];
-        lsum = __fadd_rn(lsum, ln_sum4(x[i]));
-    }
-    const float mean = __fdiv_rn(cluster_sum(lsum, red, &part), (float)h);
-    float lvar = 0.f;
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-        if (threadIdx.x + i * kLnCThreads >= h4) break;
-        lvar = __fadd_rn(lvar, ln_var4(x[i], mean));
-    }
-    const float var = __fdiv_rn(cluster_sum(lvar, red, &part), (float)h);
-    const float den = __fsqrt_rn(__fadd_rn(var, 1e-5f));
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-        const int j4 = threadIdx.x + i * kLnCThreads;
-        if (j4 >= h4) break;
-        const float o0 = ln_norm(x[i].x, mean, den, ga[i].x, be[i].x), o1 = ln_norm(x[i].y, mean, den, ga[i].y, be[i].y),
-                    o2 = ln_norm(x[i].z, mean, den, ga[i].z, be[i].z), o3 = ln_norm(x[i].w, mean, den, ga[i].w, be[i].w);
-        for (int d = 0; d < dst.n; ++d) store4<T>((T*)dst.p[d] + row + c0 + 4 * j4, o0, o1, o2, o3);
-    }
-}
-
 // ------------------------------------------------------------------ attention (L <= 128)
 template <typename T>
 __global__ void __launch_bounds__(128) attention_kernel(const float* __restrict__ qkv, const int32_t* __restrict__ seq_start,
@@ -595,52 +480,10 @@ static void launch_ln(int rows, int row0, const Peers& P, const float* residual,
                (const T*)gamma, (const T*)beta, x_out, D, h, row0);
 }
 
-// Cluster variant eligibility: h splits into kLnC column blocks of whole float4 groups, at most
-// 2 float4 per thread (h <= 8192). A function of h only, so one model always uses one kernel.
-static bool ln_cluster(int h) {
-    static const int on = [] {
-        const char* e = getenv("MPSW_LN_CLUSTER");
-        return e ? atoi(e) : 0;
-    }();
-    return on && h % (4 * kLnC) == 0 && h / (4 * kLnC) <= 2 * kLnCThreads;
-}
-
-template <typename T, int VPT>
-static void launch_ln_cluster(int rows, int row0, const Peers& P, const float* residual, const void* bias,
-                              const void* pos_table, const int32_t* pos, const void* gamma, const void* beta,
-                              float* x_out, const LnDst& D, int h, cudaStream_t st) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(rows * kLnC);
-    cfg.blockDim = dim3(kLnCThreads);
-    cfg.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    at[1].id = cudaLaunchAttributeClusterDimension;
-    at[1].val.clusterDim.x = kLnC;
-    at[1].val.clusterDim.y = 1;
-    at[1].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
-    MPSW_CU(cudaLaunchKernelEx(&cfg, reduce_ln_cluster_kernel<T, VPT>, P, residual, (const T*)bias, (const T*)pos_table, pos,
-                               (const T*)gamma, (const T*)beta, x_out, D, h, row0));
-}
-
 template <typename T>
 static void launch_ln_t(int rows, int row0, const Peers& P, const float* residual, const void* bias,
                         const void* pos_table, const int32_t* pos, const void* gamma, const void* beta, float* x_out,
                         const LnDst& D, int h, cudaStream_t st) {
-    if (ln_cluster(h)) {
-        static const bool noop = dev_noop("MPSW_DEV_NOOP_LN");
-        if (noop) {
-            launch_pdl(dev_noop_kernel, rows, kLnThreads, 0, st);
-        } else if (h / (4 * kLnC) <= kLnCThreads) {
-            launch_ln_cluster<T, 1>(rows, row0, P, residual, bias, pos_table, pos, gamma, beta, x_out, D, h, st);
-        } else {
-            launch_ln_cluster<T, 2>(rows, row0, P, residual, bias, pos_table, pos, gamma, beta, x_out, D, h, st);
-        }
-        return;
-    }
     const int vpt = (h / 4 + kLnThreads - 1) / kLnThreads;
     switch (vpt) {
         case 1: launch_ln<T, 1>(rows, row0, P, residual, bias, pos_table, pos, gamma, beta, x_out, D, h, st); break;
