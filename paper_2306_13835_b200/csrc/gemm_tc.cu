@@ -11,9 +11,12 @@
 //   * warp 1 (one elected thread): tcgen05.mma.cta_group::1.kind::f16, 4 x (K=16) per stage,
 //     accumulator D[128 x Mp] fp32 in TMEM; tcgen05.commit frees the smem stage;
 //   * warp 2: TMEM allocator; warps 4..7: epilogue (tcgen05.ld 32x32b, lane = weight row).
-// Split-K over CTAs is chosen from (N, K) only — never from M — and the partial sums are
-// reduced by the last-arriving CTA of each tile in fixed split order, so results are
-// deterministic and bitwise batch-invariant.
+// Split-K over CTAs (stream-K over (tile pair, k-block) units) is chosen from (N, K) only —
+// never from M — and the partial sums of a split tile are reduced in fixed split order (by its
+// last-arriving CTA below 64 padded tokens, by tc_fixup_kernel from 64), so results are
+// deterministic and bitwise batch-invariant. The two tiles of a pair run on two independent CTAs,
+// or from 192 padded tokens on a CTA pair (cta_group::2): same bits. Weights are streamed with an
+// L2 evict_first policy, the token tile and the partials with evict_last.
 #include "tc_common.cuh"
 
 #include <cstdio>
@@ -654,9 +657,10 @@ struct TcExec {
     int vw;
     int cps;
 };
-// Padded token rows from which the pair split runs on CTA pairs, one CTA per SM with two
-// workers each: at large M the token tile dominates the L2 -> smem traffic (a CTA pair halves
-// it), and one CTA per SM double-buffers the 256-column accumulator and gets a 6-deep ring.
+// Padded token rows from which the pair split runs on CTA pairs: at large M the token tile
+// dominates the L2 -> smem traffic, and a CTA pair halves it (OPT-13B layer at M = 256: 234 ->
+// 217 us; slower below 192 tokens). MPSW_TC_VW=2 runs two workers per pair at one CTA per SM
+// (double-buffered 256-column accumulator, 6-deep ring): measured slower, 229 us (dev knob).
 static int tc_cl_min_mp() {
     static int v = env_int("MPSW_TC_CL_MIN", 192);
     return v;
